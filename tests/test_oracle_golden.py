@@ -1,0 +1,112 @@
+"""Pin the CPU oracle against golden vectors produced by the reference.
+
+CPU only.  If the oracle reproduces the reference's own outputs bit for bit
+here, it can stand in for the reference on the GPU box (where
+/root/reference does not exist).
+"""
+
+import numpy as np
+import pytest
+
+from conftest import bits_equal, golden_cases, load_golden
+
+
+def _fmt(O, row):
+    sig, exp, sub = (int(v) for v in row)
+    for f in O.REGISTRY.values():
+        if (f.sig, f.exp, f.subnormals) == (sig, exp, bool(sub)):
+            return f
+    return O.Fmt(f"p{sig}e{exp}", sig, exp, bool(sub))
+
+
+def _mats_from_flat(flat, N, L):
+    T = flat.shape[0]
+    mats, off = [], 0
+    for s in range(0, N, L):
+        Lk = min(L, N - s)
+        mats.append(flat[:, off:off + Lk * Lk].reshape(T, Lk, Lk))
+        off += Lk * Lk
+    return mats
+
+
+@pytest.mark.parametrize("name", golden_cases())
+def test_gram_matched_filter_bit_exact(oracle, name):
+    g = load_golden(name)
+    A, b = oracle.gram_mf(g["H"], g["y"], float(g["sigma2"]))
+    assert bits_equal(A, g["A"])
+    assert bits_equal(b, g["b"])
+
+
+@pytest.mark.parametrize("name", golden_cases())
+def test_cg_bit_exact_with_reference_blocks(oracle, name):
+    g = load_golden(name)
+    w, mv, ip = (_fmt(oracle, r) for r in g["fmts"])
+    N = g["b"].shape[1]
+    mats = _mats_from_flat(g["Minv"], N, int(g["L"])) if "Minv" in g else None
+    out = oracle.cg_batch(g["A"], g["b"], int(g["iters"]), w, mv, ip, mats, str(g["rho_update"]))
+    assert bits_equal(out.x, g["x"])
+    np.testing.assert_array_equal(out.breakdown_at, g["breakdown_at"])
+    np.testing.assert_array_equal(out.diverged_at, g["diverged_at"])
+    np.testing.assert_array_equal(out.converged_at, g["converged_at"])
+    assert bits_equal(out.residual_norms, g["residual_norms"])
+
+
+@pytest.mark.parametrize("name", golden_cases())
+def test_bj_inverses_and_slicer(oracle, name):
+    g = load_golden(name)
+    if "Minv" in g:
+        mats = oracle.bj_inverses(g["A"], int(g["L"]))
+        flat = np.concatenate([m.reshape(m.shape[0], -1) for m in mats], axis=1)
+        # same LAPACK on the same host -> same bits; tolerance if BLAS differs
+        np.testing.assert_allclose(flat, g["Minv"], rtol=1e-12, atol=1e-15)
+    bits = oracle.demod16(g["x"])
+    np.testing.assert_array_equal(bits, g["rx_bits"])
+    np.testing.assert_array_equal(oracle.bit_errors(bits, g["tx_bits"]), g["bit_errors"])
+
+
+def test_solver_edge_flags(oracle):
+    g = load_golden("solver_edges")
+    for tag in ("fp16", "p5e4", "fp64"):
+        w, mv, ip = (_fmt(oracle, r) for r in g[f"{tag}_fmts"])
+        out = oracle.cg_batch(g["A"], g["b"], 6, w, mv, ip)
+        assert bits_equal(out.x, g[f"{tag}_x"]), tag
+        np.testing.assert_array_equal(out.breakdown_at, g[f"{tag}_breakdown_at"])
+        np.testing.assert_array_equal(out.diverged_at, g[f"{tag}_diverged_at"])
+    mats = _mats_from_flat(g["ragged_Minv"], 8, 3)
+    for rv in ("as_written", "textbook"):
+        out = oracle.cg_batch(g["ragged_A"], g["ragged_b"], 5, oracle.FP64, oracle.FP16,
+                              oracle.FP16, mats, rv)
+        assert bits_equal(out.x, g[f"ragged_{rv}_x"]), rv
+
+
+def test_kernel_kats(oracle):
+    g = load_golden("kernel_kats")
+    names = {"fp64": oracle.FP64, "fp32": oracle.FP32, "fp16": oracle.FP16, "bfloat16": oracle.BF16}
+    for n, f in names.items():
+        assert bits_equal(oracle.matvec(g["A"], g["v"], f), g[f"matvec_{n}"]), n
+        assert bits_equal(oracle.dot(g["A"][:, 0, :], g["v"], f), g[f"dot_{n}"]), n
+        assert bits_equal(oracle.axpy(g["a"], g["A"][:, 1, :], g["v"], f), g[f"axpy_{n}"]), n
+
+
+def test_slicer_known_answers(oracle):
+    g = load_golden("slicer")
+    np.testing.assert_array_equal(oracle.demod16(g["x"]), g["bits"])
+
+
+def test_division_is_numpy_smith(oracle):
+    rng = np.random.default_rng(3)
+    n = rng.standard_normal((4, 50000)) * np.exp(rng.uniform(-40, 40, (4, 50000)))
+    num = n[0] + 1j * n[1]
+    den = n[2] + 1j * n[3]
+    den[:5] = [0, -0.0, complex(0, -0.0), complex(np.inf, 0), complex(np.nan, 1)]
+    with np.errstate(all="ignore"):
+        assert bits_equal(oracle.cdiv(num, den), num / den)
+
+
+def test_qam64_round_trip_extension(oracle):
+    # 64-QAM is not in the reference (parity unpinned); check self-consistency.
+    rng = np.random.default_rng(4)
+    bits = rng.integers(0, 2, (16, 6 * 8), dtype=np.uint8)
+    s = oracle.mod64(bits)
+    np.testing.assert_array_equal(oracle.demod64(s), bits)
+    assert np.mean(np.abs(s) ** 2) == pytest.approx(1.0, rel=0.1)
