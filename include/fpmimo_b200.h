@@ -1,0 +1,132 @@
+/*
+ * fpmimo_b200 -- C ABI of the B200-native batched FP-CG / FP-BJ-CG detector.
+ *
+ * Drop-in boundary for the reference package `fpmimo` (pure Python/NumPy, no
+ * FFI of its own).  Each entry point replaces the reference interface cited
+ * beside it (paths relative to /root/reference/pkg/src/fpmimo/):
+ *
+ *   fpm_gram        <- Gram / matched filter inline in simulate_trials,
+ *                      detect.py:215-218 (A = H^H H sym + s2 I, b = H^H y)
+ *   fpm_bj_setup    <- build_blocks_batch, solvers.py:232-253
+ *   fpm_cg          <- run_batch, solvers.py:262-393 (x, breakdown_at,
+ *                      diverged_at; histories are not produced)
+ *   fpm_slice_count <- demodulate_16qam + error sum, detect.py:78-84, :260-262
+ *   fpm_detect      <- _detect_batch, detect.py:223-237, fused with the Gram
+ *                      of simulate_trials and the slicer/counter of
+ *                      run_ber_sweep (one kernel, A never leaves the SM)
+ *   fpm_detect_host <- the same call on HOST buffers (chunked H2D / compute /
+ *                      D2H pipeline on two streams)
+ *
+ * Conventions
+ *   - complex128 arrays are interleaved (re, im) doubles, C-contiguous,
+ *     exactly NumPy's layout: H (T, M, N), y (T, M), A (T, N, N), b/x (T, N).
+ *   - Block-Jacobi inverses ("Minv") are packed per realization with a fixed
+ *     stride of N*L complex entries: block k (size Lk = min(L, N - kL)) is the
+ *     row-major Lk x Lk matrix starting at entry k*L*L.
+ *   - All pointers except in fpm_detect_host are DEVICE pointers owned by the
+ *     caller; inputs are never modified (solvers.py:297-298).  `stream` is a
+ *     cudaStream_t (NULL = legacy default stream).  Calls are asynchronous on
+ *     `stream`, carry no global mutable state and are re-entrant.
+ *   - Return: FPM_OK, or an error code; precondition failures (the reference's
+ *     ContractViolation, errors.py:4-9) are FPM_EINVAL / FPM_ENOTPD.
+ *     Numerical failures are flags, not errors (solvers.py:302-303).
+ *   - counters (int64[FPM_NCOUNTERS]) are ACCUMULATED into (zero them first).
+ */
+#ifndef FPMIMO_B200_H
+#define FPMIMO_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* FloatFormat (formats.py:51-98): significand bits incl. hidden bit,
+ * exponent bits, subnormals.  binary16 = {11,5,1}, bfloat16 = {8,8,1},
+ * binary32 = {24,8,1}, binary64 = {53,11,1}. */
+typedef struct fpm_format {
+  int32_t sig_bits;
+  int32_t exp_bits;
+  int32_t subnormals;
+} fpm_format;
+
+/* PrecisionConfig (solvers.py:56-85): work must be at least as fine as the
+ * other two. */
+typedef struct fpm_precision {
+  fpm_format work;
+  fpm_format matvec;
+  fpm_format inner;
+} fpm_precision;
+
+enum {
+  FPM_OK = 0,
+  FPM_EINVAL = 1,      /* bad argument (ContractViolation) */
+  FPM_ENOTPD = 2,      /* non-PD diagonal block (solvers.py:246-249) */
+  FPM_ECUDA = 3,       /* CUDA runtime error */
+  FPM_EUNSUPPORTED = 4 /* configuration outside this build's limits */
+};
+
+enum { FPM_RHO_AS_WRITTEN = 0, FPM_RHO_TEXTBOOK = 1 };
+
+/* DetectorSpec.algorithm (detect.py:115); "cg" computes at fp64 throughout */
+enum { FPM_ALG_CG = 1, FPM_ALG_FP_CG = 2, FPM_ALG_FP_BJ_CG = 3 };
+
+enum {
+  FPM_CNT_BIT_ERRORS = 0,
+  FPM_CNT_SYMBOL_ERRORS = 1, /* extension: the reference counts bits only */
+  FPM_CNT_DIVERGED = 2,
+  FPM_CNT_BREAKDOWN = 3,
+  FPM_CNT_TRIALS = 4,
+  FPM_CNT_NONPD = 5,
+  FPM_NCOUNTERS = 8
+};
+
+int fpm_version(void);
+const char* fpm_strerror(int code);
+
+/* Largest N / L / M this build accepts (N <= 128, L <= 16, M <= 4096). */
+int fpm_limits(int32_t* max_n, int32_t* max_l, int32_t* max_m);
+
+int fpm_gram(const double* H, const double* y, int64_t T, int32_t M, int32_t N, double sigma2,
+             double* A, double* b, void* stream);
+
+/* bad_block: optional int32[T], set to the first non-PD block start or -1.
+ * Returns FPM_ENOTPD if any block of any realization is not PD. */
+int fpm_bj_setup(const double* A, int64_t T, int32_t N, int32_t L, int32_t allow_ragged, double* Minv,
+                 int32_t* bad_block, void* stream);
+
+/* Minv == NULL -> plain FP-CG, else FP-BJ-CG with block size L. */
+int fpm_cg(const double* A, const double* b, const double* Minv, int64_t T, int32_t N, int32_t L,
+           int32_t iters, const fpm_precision* prec, int32_t rho_update, double* x, int32_t* breakdown_at,
+           int32_t* diverged_at, void* stream);
+
+/* qam = 16 (reference) or 64 (extension).  tx_bits / rx_bits: (T, bits*N)
+ * uint8 in the reference's layout, both nullable. */
+int fpm_slice_count(const double* x, const uint8_t* tx_bits, int64_t T, int32_t N, int32_t qam,
+                    uint8_t* rx_bits, int64_t* counters, void* stream);
+
+/* Fused H, y -> x_hat, flags, sliced bits, counters.  Minv_in != NULL
+ * injects precomputed block inverses (bit-exact mode); otherwise they are
+ * built on-chip in fp64 from the Gram's diagonal blocks. */
+int fpm_detect(const double* H, const double* y, const uint8_t* tx_bits, int64_t T, int32_t M, int32_t N,
+               double sigma2, int32_t algorithm, int32_t L, int32_t iters, const fpm_precision* prec,
+               int32_t rho_update, int32_t qam, const double* Minv_in, double* x, int32_t* breakdown_at,
+               int32_t* diverged_at, uint8_t* rx_bits, int64_t* counters, void* stream);
+
+/* As fpm_detect but every pointer is a HOST pointer (pinned memory gives
+ * full PCIe rate).  chunk = realizations per pipeline stage (0 = auto).
+ * Synchronous: returns when all outputs are in host memory. */
+int fpm_detect_host(const double* H, const double* y, const uint8_t* tx_bits, int64_t T, int32_t M,
+                    int32_t N, double sigma2, int32_t algorithm, int32_t L, int32_t iters,
+                    const fpm_precision* prec, int32_t rho_update, int32_t qam, const double* Minv_in,
+                    double* x, int32_t* breakdown_at, int32_t* diverged_at, uint8_t* rx_bits,
+                    int64_t* counters, int64_t chunk);
+
+/* Number of kernels this library launched in the calling process (all
+ * entry points), for launch accounting in benchmarks. */
+int64_t fpm_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FPMIMO_B200_H */

@@ -1,0 +1,202 @@
+"""GPU drop-in for the reference solver layer (solvers.py).
+
+    PrecisionConfig      <- solvers.py:56-85
+    BatchResult          <- solvers.py:188-204 (x and flags; histories None)
+    build_blocks_batch   <- solvers.py:232-253  (fpm_bj_setup)
+    run_batch            <- solvers.py:262-393  (fpm_cg)
+
+Arrays may be NumPy (host; results come back as NumPy, like the
+reference) or torch CUDA tensors (results stay on the device).  Every
+computation runs in libfpmimo_b200.so; there is no CPU path.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .errors import ContractViolation
+from .formats import FP64, FloatFormat, get_format
+
+__all__ = ["PrecisionConfig", "BatchResult", "BatchBlocks", "build_blocks_batch", "run_batch",
+           "pack_blocks"]
+
+
+@dataclass(frozen=True)
+class PrecisionConfig:
+    work: FloatFormat = FP64
+    matvec: FloatFormat = FP64
+    inner: FloatFormat = FP64
+
+    def __post_init__(self):
+        for k in ("work", "matvec", "inner"):
+            object.__setattr__(self, k, get_format(getattr(self, k)))
+        if (self.work.unit_roundoff > self.matvec.unit_roundoff
+                or self.work.unit_roundoff > self.inner.unit_roundoff):
+            raise ContractViolation("working precision must be at least as fine as the "
+                                    "matrix-vector and inner-product precisions")
+
+    @classmethod
+    def uniform(cls, fmt) -> "PrecisionConfig":
+        fmt = get_format(fmt)
+        return cls(work=fmt, matvec=fmt, inner=fmt)
+
+    @property
+    def is_native(self) -> bool:
+        return self.work.is_native and self.matvec.is_native and self.inner.is_native
+
+    def labels(self):
+        return (self.work.name, self.matvec.name, self.inner.name)
+
+
+@dataclass
+class BatchResult:
+    x: object                 # (T, N) complex128
+    breakdown_at: object      # (T,) int64, -1 if none
+    diverged_at: object       # (T,) int64, -1 if none
+    iterations_run: int = 0
+    residual_norms: object = None
+    iterate_norms: object = None
+    alphas: object = None
+    betas: object = None
+    b_norm: object = None
+    converged_at: object = None
+
+
+class BatchBlocks:
+    """Block-diagonal inverses, packed per realization with stride N*L
+    (block k = row-major Lk x Lk at entry k*L*L), as the C ABI expects.
+    `.mats` gives the reference's list-of-(T, Lk, Lk) view."""
+
+    def __init__(self, packed, N: int, L: int):
+        self.packed = packed
+        self.N = N
+        self.L = L
+
+    @property
+    def sizes(self):
+        return [min(self.L, self.N - s) for s in range(0, self.N, self.L)]
+
+    @property
+    def mats(self):
+        out, T = [], self.packed.shape[0]
+        for k, Lk in enumerate(self.sizes):
+            off = k * self.L * self.L
+            out.append(self.packed[:, off:off + Lk * Lk].reshape(T, Lk, Lk))
+        return out
+
+
+def pack_blocks(mats, N: int, L: int):
+    """list of (T, Lk, Lk) arrays (reference _BatchBlocks.mats) -> packed (T, N*L)."""
+    T = mats[0].shape[0]
+    out = np.zeros((T, N * L), np.complex128)
+    for k, m in enumerate(mats):
+        Lk = m.shape[-1]
+        out[:, k * L * L:k * L * L + Lk * Lk] = np.asarray(m, np.complex128).reshape(T, -1)
+    return out
+
+
+# ---------------------------------------------------------------------------
+# device helpers
+# ---------------------------------------------------------------------------
+
+def _torch():
+    import torch
+    return torch
+
+
+def _to_dev(a, dtype):
+    torch = _torch()
+    if isinstance(a, torch.Tensor):
+        if not a.is_cuda:
+            a = a.cuda()
+        return a.to(dtype).contiguous()
+    return torch.from_numpy(np.ascontiguousarray(a)).to(device="cuda", dtype=dtype)
+
+
+def _is_torch(a):
+    try:
+        import torch
+        return isinstance(a, torch.Tensor)
+    except ImportError:  # pragma: no cover
+        return False
+
+
+def _stream():
+    return ctypes_stream(_torch().cuda.current_stream())
+
+
+def ctypes_stream(s):
+    return s.cuda_stream
+
+
+def _out(t, host):
+    return t.cpu().numpy() if host else t
+
+
+def build_blocks_batch(A, L: int, *, allow_ragged: bool = False) -> BatchBlocks:
+    """Batched block-Jacobi setup (solvers.py:232-253) on the GPU: fp64
+    Cholesky PD check + Hermitian inverse per diagonal block."""
+    torch = _torch()
+    host = not _is_torch(A)
+    Ad = _to_dev(A, torch.complex128)
+    T, N = Ad.shape[0], Ad.shape[-1]
+    if N % L and not allow_ragged:
+        raise ContractViolation(f"L={L} must divide the system dimension {N}")
+    packed = torch.zeros((T, N * L), dtype=torch.complex128, device=Ad.device)
+    bad = torch.empty((T,), dtype=torch.int32, device=Ad.device)
+    lib = _lib.load()
+    rc = lib.fpm_bj_setup(Ad.data_ptr(), T, N, L, int(allow_ragged), packed.data_ptr(), bad.data_ptr(),
+                          _stream())
+    if rc == _lib.FPM_ENOTPD:
+        first = int(bad[bad >= 0][0].item()) if bool((bad >= 0).any()) else -1
+        raise ContractViolation(f"non-PD diagonal block at {first}")
+    _lib.check(rc, "build_blocks_batch")
+    return BatchBlocks(_out(packed, host), N, L)
+
+
+def run_batch(A, b, max_iters: int, prec: PrecisionConfig | None = None, blocks=None, *,
+              rho_update: str = "as_written", rtol: float = 1e-6, **unsupported) -> BatchResult:
+    """Lockstep mixed-precision (BJ-)CG on the GPU (solvers.py:262-393).
+
+    `blocks` may be a BatchBlocks, or anything with a `.mats` list of
+    (T, Lk, Lk) arrays (the reference's _BatchBlocks).  Returns x and the
+    breakdown/diverged flags bit-identical to the reference; the optional
+    history recording of the reference is not produced.
+    """
+    torch = _torch()
+    if prec is None:
+        prec = PrecisionConfig()
+    if rho_update not in _lib.FPM_RHO:
+        raise ContractViolation(f"unknown rho_update variant {rho_update!r}")
+    if max_iters < 1:
+        raise ContractViolation("max_iters must be at least 1")
+    if any(unsupported.get(k) for k in ("record_gaps", "record_iterates", "record_residual_vectors")):
+        raise NotImplementedError("history recording is not part of the GPU hot path")
+    host = not _is_torch(b)
+    Ad = _to_dev(A, torch.complex128)
+    bd = _to_dev(b, torch.complex128)
+    T, N = bd.shape
+    minv = None
+    L = 1
+    if blocks is not None:
+        if isinstance(blocks, BatchBlocks):
+            L, packed = blocks.L, blocks.packed
+        else:
+            mats = blocks.mats
+            L = mats[0].shape[-1]
+            packed = pack_blocks([np.asarray(m) for m in mats], N, L)
+        minv = _to_dev(packed, torch.complex128)
+    x = torch.empty((T, N), dtype=torch.complex128, device=bd.device)
+    brk = torch.empty((T,), dtype=torch.int32, device=bd.device)
+    div = torch.empty((T,), dtype=torch.int32, device=bd.device)
+    lib = _lib.load()
+    ps = _lib.precision_struct(prec)
+    rc = lib.fpm_cg(Ad.data_ptr(), bd.data_ptr(), None if minv is None else minv.data_ptr(), T, N, L,
+                    int(max_iters), ps, _lib.FPM_RHO[rho_update], x.data_ptr(), brk.data_ptr(),
+                    div.data_ptr(), _stream())
+    _lib.check(rc, "run_batch")
+    return BatchResult(x=_out(x, host), breakdown_at=_out(brk.to(torch.int64), host),
+                       diverged_at=_out(div.to(torch.int64), host), iterations_run=int(max_iters))

@@ -1,0 +1,243 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's
+golden vectors and the oracle.  Run on a B200: pytest -m gpu.
+
+Bars (BASELINE.json north_star):
+  * Gram / matched filter, x_hat with injected block inverses, flags, sliced
+    bits, error counts: BIT-EXACT.
+  * x_hat with on-chip (GPU fp64 Cholesky) block inverses: normwise relative
+    difference per realization <= 1e-12 for fp64 paths and <= 2**-(p-2) for
+    p-bit paths (p = stored fraction bits: fp16 10, bf16 7, fp32 23); sliced
+    bits identical.
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+from conftest import bits_equal, golden_cases, load_golden
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2504_09820_b200 import build
+    build.build()
+
+
+def _spec_from_golden(g):
+    from paper_2504_09820_b200.detect import DetectorSpec
+    names = {(53, 11): "fp64", (24, 8): "fp32", (11, 5): "fp16", (8, 8): "bfloat16"}
+    w, mv, ip = (names[(int(r[0]), int(r[1]))] for r in g["fmts"])
+    L = int(g["L"]) or None
+    return DetectorSpec(str(g["algorithm"]), iters=int(g["iters"]), L=L, work=w, matvec=mv, inner=ip,
+                        rho_update=str(g["rho_update"]))
+
+
+def _prec_tol(g):
+    sig = int(g["fmts"][1][0])          # matvec significand bits incl. hidden
+    return 1e-12 if sig == 53 else 2.0 ** -(sig - 1 - 2)
+
+
+@pytest.mark.parametrize("name", golden_cases())
+def test_gram_bit_exact(name):
+    from paper_2504_09820_b200.detect import gram_mf
+    g = load_golden(name)
+    A, b = gram_mf(g["H"], g["y"], float(g["sigma2"]))
+    assert bits_equal(A, g["A"])
+    assert bits_equal(b, g["b"])
+
+
+@pytest.mark.parametrize("name", golden_cases())
+def test_fused_detect_bit_exact_injected_blocks(name):
+    from paper_2504_09820_b200.detect import detect
+    g = load_golden(name)
+    det = _spec_from_golden(g)
+    res = detect(det, g["H"], g["y"], float(g["sigma2"]), g["tx_bits"], minv=g.get("Minv"), want_bits=True)
+    assert bits_equal(res.x, g["x"])
+    np.testing.assert_array_equal(res.breakdown_at, g["breakdown_at"])
+    np.testing.assert_array_equal(res.diverged_at, g["diverged_at"])
+    np.testing.assert_array_equal(res.bits, g["rx_bits"])
+    assert res.counters["bit_errors"] == int(g["bit_errors"].sum())
+    assert res.counters["trials"] == g["H"].shape[0]
+    assert res.counters["diverged"] == int((g["diverged_at"] >= 0).sum())
+
+
+@pytest.mark.parametrize("name", golden_cases())
+def test_fused_detect_onchip_blocks(name):
+    from paper_2504_09820_b200.detect import detect
+    g = load_golden(name)
+    det = _spec_from_golden(g)
+    res = detect(det, g["H"], g["y"], float(g["sigma2"]), g["tx_bits"], want_bits=True)
+    if "Minv" not in g:
+        assert bits_equal(res.x, g["x"])
+    rel = np.linalg.norm(res.x - g["x"], axis=1) / np.linalg.norm(g["x"], axis=1)
+    assert rel.max() <= _prec_tol(g), rel.max()
+    np.testing.assert_array_equal(res.bits, g["rx_bits"])
+    assert res.counters["bit_errors"] == int(g["bit_errors"].sum())
+
+
+@pytest.mark.parametrize("name", golden_cases())
+def test_run_batch_bit_exact(name):
+    from paper_2504_09820_b200.solvers import BatchBlocks, run_batch
+    g = load_golden(name)
+    det = _spec_from_golden(g)
+    N = g["b"].shape[1]
+    blocks = BatchBlocks(g["Minv"], N, int(g["L"])) if "Minv" in g else None
+    res = run_batch(g["A"], g["b"], det.iters, det.precision(), blocks, rho_update=det.rho_update)
+    assert bits_equal(res.x, g["x"])
+    np.testing.assert_array_equal(res.breakdown_at, g["breakdown_at"])
+    np.testing.assert_array_equal(res.diverged_at, g["diverged_at"])
+
+
+@pytest.mark.parametrize("name", [n for n in golden_cases() if "bj" in n])
+def test_block_inverses_close_to_lapack(name):
+    from paper_2504_09820_b200.solvers import build_blocks_batch
+    g = load_golden(name)
+    bb = build_blocks_batch(g["A"], int(g["L"]))
+    np.testing.assert_allclose(bb.packed, g["Minv"], rtol=1e-11, atol=1e-13)
+
+
+def test_generic_emulation_path_matches_native(monkeypatch):
+    """The integer RNE emulation kernels (any (sig, exp)) must reproduce the
+    native fp16/bf16/fp32 kernels bit for bit."""
+    from paper_2504_09820_b200.detect import detect
+    for name in ("c2_fpcg_fp16_snr0", "c2_fpcg_bf16_snr10", "c5_bj4_textbook_fp32", "mix_w16_all_bj4",
+                 "mix_w32_mv16_ip16"):
+        g = load_golden(name)
+        det = _spec_from_golden(g)
+        monkeypatch.setenv("FPM_FORCE_GENERIC", "1")
+        res = detect(det, g["H"], g["y"], float(g["sigma2"]), g["tx_bits"], minv=g.get("Minv"))
+        monkeypatch.delenv("FPM_FORCE_GENERIC")
+        assert bits_equal(res.x, g["x"]), name
+
+
+def test_solver_edge_flags():
+    from paper_2504_09820_b200.formats import FP16, make_format
+    from paper_2504_09820_b200.solvers import BatchBlocks, PrecisionConfig, run_batch
+    g = load_golden("solver_edges")
+    precs = {"fp16": PrecisionConfig(matvec=FP16, inner=FP16),
+             "p5e4": PrecisionConfig(matvec=make_format(5, 4), inner=make_format(6, 5)),
+             "fp64": PrecisionConfig()}
+    for tag, prec in precs.items():
+        res = run_batch(g["A"], g["b"], 6, prec)
+        assert bits_equal(res.x, g[f"{tag}_x"]), tag
+        np.testing.assert_array_equal(res.breakdown_at, g[f"{tag}_breakdown_at"])
+        np.testing.assert_array_equal(res.diverged_at, g[f"{tag}_diverged_at"])
+    for rv in ("as_written", "textbook"):
+        res = run_batch(g["ragged_A"], g["ragged_b"], 5, precs["fp16"], BatchBlocks(g["ragged_Minv"], 8, 3),
+                        rho_update=rv)
+        assert bits_equal(res.x, g[f"ragged_{rv}_x"]), rv
+
+
+def test_slicer_known_answers():
+    from paper_2504_09820_b200.detect import demodulate_16qam
+    g = load_golden("slicer")
+    np.testing.assert_array_equal(demodulate_16qam(g["x"]), g["bits"])
+
+
+def test_nonpd_block_raises():
+    from paper_2504_09820_b200.errors import ContractViolation
+    from paper_2504_09820_b200.solvers import build_blocks_batch
+    A = np.tile(np.eye(8, dtype=np.complex128), (3, 1, 1))
+    A[1, 4, 4] = -1.0
+    with pytest.raises(ContractViolation):
+        build_blocks_batch(A, 4)
+
+
+def _oracle_inputs(M, N, zeta, snr, T, seed=20261020, qam=16):
+    import fpm_oracle as O
+    return O.simulate(M, N, zeta, snr, range(T), seed, qam=qam)
+
+
+@pytest.mark.parametrize("cfg", [
+    # (M, N, zeta, snr, T, algorithm, L, iters, mv)
+    (128, 16, 0.0, 10.0, 300, "cg", None, 8, "fp64"),
+    (128, 32, 0.5, 6.0, 160, "fp_cg", None, 10, "fp16"),
+    (128, 64, 0.5, 15.0, 48, "fp_bj_cg", 4, 8, "fp16"),
+    (128, 64, 0.5, 15.0, 48, "fp_bj_cg", 4, 8, "fp64"),
+    (96, 24, 0.6, 12.0, 40, "fp_bj_cg", 6, 7, "fp32"),   # N not a multiple of 8
+    (64, 12, 0.3, 9.0, 70, "fp_cg", None, 5, "bfloat16"),
+])
+def test_random_batches_against_oracle(cfg):
+    import fpm_oracle as O
+    from paper_2504_09820_b200.detect import DetectorSpec, detect
+    M, N, zeta, snr, T, alg, L, iters, mv = cfg
+    H, y, bits, s2 = _oracle_inputs(M, N, zeta, snr, T)
+    det = DetectorSpec(alg, iters=iters, L=L, matvec=mv, inner=mv)
+    fm = O.REGISTRY[mv]
+    A, b = O.gram_mf(H, y, s2)
+    mats = O.bj_inverses(A, L) if alg == "fp_bj_cg" else None
+    work = O.FP64
+    ref = O.cg_batch(A, b, iters, work, fm if alg != "cg" else O.FP64, fm if alg != "cg" else O.FP64, mats)
+    res = detect(det, H, y, s2, bits, minv=mats, want_bits=True)
+    assert bits_equal(res.x, ref.x)
+    np.testing.assert_array_equal(res.diverged_at, ref.diverged_at)
+    ob = O.demod16(ref.x)
+    np.testing.assert_array_equal(res.bits, ob)
+    assert res.counters["bit_errors"] == int(O.bit_errors(ob, bits).sum())
+
+
+def test_chunking_and_host_pipeline_invariance():
+    """Counts do not depend on batching (tests/test_detect.py:133-140 analogue)
+    and the host-buffer pipeline equals the device call."""
+    from paper_2504_09820_b200.detect import DetectorSpec, detect, detect_host
+    H, y, bits, s2 = _oracle_inputs(128, 64, 0.5, 15.0, 200)
+    det = DetectorSpec("fp_bj_cg", iters=8, L=4, matvec="fp16", inner="fp16")
+    full = detect(det, H, y, s2, bits, want_bits=True)
+    parts = [detect(det, H[a:a + 37], y[a:a + 37], s2, bits[a:a + 37]) for a in range(0, 200, 37)]
+    assert sum(p.counters["bit_errors"] for p in parts) == full.counters["bit_errors"]
+    assert bits_equal(np.concatenate([p.x for p in parts]), full.x)
+    hp = detect_host(det, H, y, s2, bits, want_bits=True, chunk=64)
+    assert bits_equal(hp.x, full.x)
+    np.testing.assert_array_equal(hp.bits, full.bits)
+    assert hp.counters == full.counters
+
+
+def test_qam64_extension_round_trip():
+    """64-QAM slicer (extension; no reference oracle): noiseless decisions
+    are exact and bits round-trip."""
+    import fpm_oracle as O
+    from paper_2504_09820_b200.detect import slice_count
+    rng = np.random.default_rng(9)
+    bits = rng.integers(0, 2, (32, 6 * 16), dtype=np.uint8)
+    s = O.mod64(bits)
+    got, cnt = slice_count(s, bits, qam=64)
+    np.testing.assert_array_equal(got, bits)
+    assert cnt["bit_errors"] == 0
+    noisy = s + 0.03 * (rng.standard_normal(s.shape) + 1j * rng.standard_normal(s.shape))
+    got, cnt = slice_count(noisy, bits, qam=64)
+    np.testing.assert_array_equal(got, O.demod64(noisy))
+
+
+def _gpu_batch(T, M, N, seed):
+    gen = torch.Generator(device="cuda").manual_seed(seed)
+    H = (torch.randn((T, M, N), dtype=torch.complex128, device="cuda", generator=gen)) / np.sqrt(M)
+    bits = torch.randint(0, 2, (T, 4 * N), dtype=torch.uint8, device="cuda", generator=gen)
+    lv = torch.tensor([-3.0, -1.0, 3.0, 1.0], dtype=torch.float64, device="cuda") / np.sqrt(10.0)
+    q = bits.view(T, N, 4).long()
+    s = torch.complex(lv[2 * q[..., 0] + q[..., 1]], lv[2 * q[..., 2] + q[..., 3]])
+    y = torch.einsum("tmn,tn->tm", H, s)
+    return H, y, bits
+
+
+def test_large_batch_properties():
+    """Full-size batches: chunk-size invariance at the c5 shape (2**14
+    realizations) and a noiseless zero-error sanity check
+    (tests/test_detect.py:114-123 analogue) for CG run to N iterations."""
+    from paper_2504_09820_b200.detect import DetectorSpec, detect
+    T = 1 << 14
+    H, y, bits = _gpu_batch(T, 128, 64, 1)
+    det = DetectorSpec("fp_bj_cg", iters=8, L=4, matvec="fp16", inner="fp16")
+    res = detect(det, H, y, 0.015811, bits)
+    assert res.counters["trials"] == T
+    half = detect(det, H[: T // 2], y[: T // 2], 0.015811, bits[: T // 2])
+    assert torch.equal(half.x, res.x[: T // 2])
+    H, y, bits = _gpu_batch(T, 128, 16, 2)
+    res = detect(DetectorSpec("cg", iters=16), H, y, 1e-30, bits)
+    assert res.counters["bit_errors"] == 0
