@@ -1,0 +1,381 @@
+#!/usr/bin/env python
+"""Throughput benchmark: FP-BJ-CG massive-MIMO detection (BASELINE.json c5).
+
+Workload (BASELINE.json configs[4], the metric's config): M=128 antennas x
+K=64 users (N=64), Kronecker exponential correlation zeta=0.5 both sides,
+16-QAM Gray unit energy, SNR 15 dB (reference convention sigma^2 =
+(N/M) 10^(-SNR/10)), FP-BJ-CG with block size L=4, 8 iterations, work fp64,
+matvec/inner fp16 (p=10) by default (--precision fp64 for the reference's
+all-fp64 default), batch 2^20 realizations per step.
+
+One step = one fused-kernel pass (Gram/MF -> BJ -> CG -> slice -> count) over
+the whole batch, inputs resident in HBM (synthetic: the reference's own
+channel model sampled on the GPU; 137 GB of H >> L2, so no flush needed).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Under torchrun each rank takes a contiguous 1/N of the 2^20 realizations
+(strong scaling); the only collective is the int64 counter all-reduce.
+`--impl reference` times the oracle port of the reference CPU path
+(oracle/fpm_oracle.py) on all host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import multiprocessing as mp
+import os
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
+
+M, N, ZETA, SNR_DB, L, ITERS = 128, 64, 0.5, 15.0, 4, 8
+SIGMA2 = (N / M) * 10.0 ** (-SNR_DB / 10.0)
+SEED = 20261020
+METRIC = "MIMO detections/sec (FP-BJ-CG, 128x64, 8 iters)"
+UNIT = "detections/s"
+
+
+def f_gram():
+    """Gram + matched-filter fp64 ops per detection."""
+    return 4 * M * N * (N + 1) + 8 * M * N
+
+
+def io_bytes():
+    """HBM bytes per detection: H, y read, x_hat written +
+    tx bits read (4N uint8)."""
+    return 16 * M * N + 16 * M + 16 * N + 4 * N
+
+
+# ---------------------------------------------------------------------------
+# CPU side (oracle port of the reference path), multiprocess
+# ---------------------------------------------------------------------------
+
+def _cpu_worker(args):
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    wid, per, prec = args
+    import numpy as np  # noqa: F401
+    import fpm_oracle as O
+    H, y, bits, s2 = O.simulate(M, N, ZETA, SNR_DB, range(wid * per, (wid + 1) * per), SEED)
+    fm = O.FP16 if prec == "fp16" else O.FP64
+    t0 = time.perf_counter()
+    A, b = O.gram_mf_einsum(H, y, s2)                   # detect.py:215-218
+    mats = O.bj_inverses(A, L)                          # solvers.py:232-253
+    out = O.cg_batch(A, b, ITERS, O.FP64, fm, fm, mats) # solvers.py:262-393
+    errs = int(O.bit_errors(O.demod16(out.x), bits).sum())  # detect.py:260-261
+    return time.perf_counter() - t0, per, errs
+
+
+def cpu_throughput(prec, per_worker, workers=None):
+    workers = workers or os.cpu_count() or 1
+    ctx = mp.get_context("spawn")
+    with ctx.Pool(workers) as pool:
+        res = pool.map(_cpu_worker, [(w, per_worker, prec) for w in range(workers)])
+    wall = max(r[0] for r in res)
+    n = sum(r[1] for r in res)
+    return n / wall, workers, n, wall
+
+
+# ---------------------------------------------------------------------------
+# GPU side
+# ---------------------------------------------------------------------------
+
+def _psd_sqrt(n, zeta):
+    import numpy as np
+    idx = np.arange(n)
+    R = zeta ** np.abs(idx[:, None] - idx[None, :])
+    w, V = np.linalg.eigh(R)
+    S = (V * np.sqrt(np.clip(w, 0, None))) @ V.T
+    return 0.5 * (S + S.T)
+
+
+def gen_inputs(T, rank, device, chunk=8192):
+    """Reference channel model (channel.py:138-161, detect.py:189-214) sampled
+    on the GPU: H = sqrt(Rr) W sqrt(Rt), W ~ CN(0, 1/M); 16-QAM Gray bits;
+    y = H s + CN(0, sigma^2)."""
+    import torch
+    Sr = torch.from_numpy(_psd_sqrt(M, ZETA)).to(device=device, dtype=torch.complex128)
+    St = torch.from_numpy(_psd_sqrt(N, ZETA)).to(device=device, dtype=torch.complex128)
+    H = torch.empty((T, M, N), dtype=torch.complex128, device=device)
+    y = torch.empty((T, M), dtype=torch.complex128, device=device)
+    bits = torch.empty((T, 4 * N), dtype=torch.uint8, device=device)
+    lv = torch.tensor([-3.0, -1.0, 3.0, 1.0], dtype=torch.float64, device=device) / math.sqrt(10.0)
+    for c0 in range(0, T, chunk):
+        c1 = min(T, c0 + chunk)
+        g = torch.Generator(device=device).manual_seed(SEED * 1000003 + rank * 65537 + c0)
+        W = torch.randn((c1 - c0, M, N), dtype=torch.complex128, device=device, generator=g) / math.sqrt(M)
+        Hc = Sr @ W @ St
+        H[c0:c1] = Hc
+        bt = torch.randint(0, 2, (c1 - c0, 4 * N), dtype=torch.uint8, device=device, generator=g)
+        bits[c0:c1] = bt
+        q = bt.view(c1 - c0, N, 4).long()
+        s = torch.complex(lv[2 * q[..., 0] + q[..., 1]], lv[2 * q[..., 2] + q[..., 3]])
+        noise = torch.randn((c1 - c0, M), dtype=torch.complex128, device=device, generator=g) * math.sqrt(SIGMA2)
+        y[c0:c1] = torch.einsum("tmn,tn->tm", Hc, s) + noise
+        del W, Hc, s, noise, q, bt
+    return H, y, bits
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_rank{index}.csv")
+
+    def __enter__(self):
+        os.makedirs(os.path.dirname(self.path), exist_ok=True)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=self.f, stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.f.close()
+
+    def summary(self):
+        try:
+            rows = [r.split(",") for r in open(self.path).read().strip().splitlines()]
+        except OSError:
+            return None
+        rows = [[c.strip() for c in r] for r in rows if len(r) >= 9]
+        if not rows:
+            return None
+        sm = sorted(float(r[1]) for r in rows)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[5 + k].lower().startswith("active")})
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": float(rows[0][2]), "reasons": reasons,
+                "samples": len(rows), "power_w_max": max(float(r[3]) for r in rows)}
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2504_09820_b200 import _lib
+    from paper_2504_09820_b200.detect import DetectorSpec, detect_host
+    from paper_2504_09820_b200.solvers import _stream
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    lib = _lib.load()
+    det = DetectorSpec("fp_bj_cg", iters=ITERS, L=L, matvec=args.precision, inner=args.precision)
+    ps = _lib.precision_struct(det.precision())
+
+    # cpu baseline first (rank 0, N=1), before the GPU allocations
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        v, w, n, wall = cpu_throughput(args.precision, args.cpu_per_worker)
+        cpu = {"value": round(v, 2), "unit": UNIT, "cores": w, "kind": "port",
+               "sample": f"{n} realizations ({args.cpu_per_worker}/worker x {w} processes) of the same "
+                         f"workload, oracle/fpm_oracle.py (NumPy port of the reference path), wall {wall:.1f}s"}
+
+    T_total = args.T
+    per = T_total // world
+    t0 = rank * per
+    T = per if rank < world - 1 else T_total - t0
+    free, total = torch.cuda.mem_get_info(dev)
+    need = T * (16 * M * N + 16 * M + 4 * N + 16 * N + 8) + (6 << 30)
+    pool = T
+    if need > free:  # resident pool reused within a step (documented in config)
+        pool = 1 << int(math.log2(max(1, (free - (8 << 30)) // (16 * M * N + 16 * M + 4 * N + 16 * N + 8))))
+    tg = time.time()
+    H, y, bits = gen_inputs(pool, rank, dev)
+    torch.cuda.synchronize()
+    gen_s = time.time() - tg
+    x = torch.empty((pool, N), dtype=torch.complex128, device=dev)
+    brk = torch.empty((pool,), dtype=torch.int32, device=dev)
+    div = torch.empty((pool,), dtype=torch.int32, device=dev)
+    cnt = torch.zeros((_lib.NCOUNTERS,), dtype=torch.int64, device=dev)
+    st = _stream()
+
+    def step():
+        done = 0
+        while done < T:
+            n = min(pool, T - done)
+            rc = lib.fpm_detect(H.data_ptr(), y.data_ptr(), bits.data_ptr(), n, M, N, SIGMA2,
+                                _lib.FPM_ALG["fp_bj_cg"], L, ITERS, ps, 0, 16, None, x.data_ptr(),
+                                brk.data_ptr(), div.data_ptr(), None, cnt.data_ptr(), st)
+            _lib.check(rc, "fpm_detect")
+            done += n
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    cnt.zero_()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    l0 = lib.fpm_launch_count()
+    with ClockSampler(local) as clk:
+        e0.record()
+        for _ in range(args.steps):
+            step()
+        e1.record()
+        e1.synchronize()
+    launches = lib.fpm_launch_count() - l0
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t_max = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+        dist.all_reduce(cnt, op=dist.ReduceOp.SUM)   # the one data-path collective: error counters
+    ms = float(t_max.item())
+    counters = {k: int(v) for k, v in zip(_lib.COUNTERS, cnt.cpu().tolist())}
+    kernel_ms = ms / args.steps / max(1, math.ceil(T / pool))    # one launch per pool pass
+    dets = T_total * args.steps
+    value = dets / (ms / 1e3)
+
+    # fp64 roofline of the fused kernel (Gram ops dominate; bit-exact => no DFMA / tensor cores)
+    peak_dp = None
+    if rank == 0:
+        import ctypes
+        out = ctypes.c_double()
+        _lib.check(lib.fpm_probe_fp64(200000, ctypes.byref(out)), "probe")
+        peak_dp = out.value
+    ach_dp = f_gram() * min(pool, T) / (kernel_ms / 1e3)
+
+    # e2e: host (pinned) buffers through the C-ABI host pipeline, copies in the timed region
+    e2e = None
+    if not args.no_e2e:
+        Te = min(args.e2e_T, pool)
+        Hh = torch.empty((Te, M, N), dtype=torch.complex128, pin_memory=True)
+        yh = torch.empty((Te, M), dtype=torch.complex128, pin_memory=True)
+        bh = torch.empty((Te, 4 * N), dtype=torch.uint8, pin_memory=True)
+        Hh.copy_(H[:Te])
+        yh.copy_(y[:Te])
+        bh.copy_(bits[:Te])
+        del H, y, bits, x
+        torch.cuda.empty_cache()
+        Hn, yn, bn = Hh.numpy(), yh.numpy(), bh.numpy()
+        detect_host(det, Hn, yn, SIGMA2, bn)  # warm-up (allocations)
+        if world > 1:
+            dist.barrier()
+        te = time.perf_counter()
+        esteps = max(1, min(args.steps, 3))
+        for _ in range(esteps):
+            r = detect_host(det, Hn, yn, SIGMA2, bn)
+        el = time.perf_counter() - te
+        el_t = torch.tensor([el], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(el_t, op=dist.ReduceOp.MAX)
+        e2e = {"value": round(Te * world * esteps / float(el_t.item()), 1), "unit": UNIT,
+               "h2d_bytes_per_step": int(Te * (16 * M * N + 16 * M + 4 * N)),
+               "d2h_bytes_per_step": int(Te * (16 * N + 8) + 8 * _lib.NCOUNTERS),
+               "realizations_per_step": Te * world, "steps": esteps,
+               "path": "fpm_detect_host (C ABI, pinned host buffers, 2-stream H2D/kernel/D2H pipeline)"}
+        _ = r
+
+    if rank == 0:
+        clocks = clk.summary()
+        line = {
+            "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": f"f64 work / {args.precision} matvec+inner",
+            "data": "synthetic (reference channel model sampled on GPU: Kronecker zeta=0.5, CN(0,1/M), 16-QAM, AWGN)",
+            "config": {"workload": f"c5: FP-BJ-CG L={L}, M={M} x N={N}, zeta={ZETA}, 16-QAM, SNR {SNR_DB} dB, "
+                                   f"{ITERS} iters, batch {T_total} realizations/step",
+                       "precision": {"work": "fp64", "matvec": args.precision, "inner": args.precision},
+                       "batch": T_total, "resident_pool": pool, "l2": "inputs (137 GB) >> L2; no flush",
+                       "parallelism": f"dp{world} (contiguous realization shards)",
+                       "input_gen_s": round(gen_s, 2)},
+            "gpu_launches": int(launches),
+            "counters": counters,
+            "ber": counters["bit_errors"] / max(1, counters["trials"] * 4 * N),
+            "roofline": {"bound": "fp64", "achieved": round(ach_dp / 1e12, 3),
+                         "peak": round(peak_dp / 1e12, 3) if peak_dp else None, "unit": "TFLOP/s",
+                         "frac": round(ach_dp / peak_dp, 4) if peak_dp else None, "traffic": None,
+                         "kernel": "fpm_detect_kernel", "kernel_ms": round(kernel_ms, 3),
+                         "work_per_unit": f"F_gram = 4MN(N+1)+8MN = {f_gram()} non-fused fp64 ops/detection",
+                         "peak_source": "fpm_probe_fp64 (measured non-fused DMUL/DADD rate, this GPU)",
+                         "hbm": {"achieved_gbs": round(io_bytes() * min(pool, T) / (kernel_ms / 1e3) / 1e9, 1),
+                                 "peak_gbs": 6554.9, "bytes_per_unit": io_bytes()}},
+            "clocks": clocks,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_reference(args):
+    """Reference arm: the oracle port of the reference CPU path on all host
+    cores (the reference is pure Python and cannot travel to the GPU box)."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    for _ in range(args.warmup):
+        cpu_throughput(args.precision, max(4, args.cpu_per_worker // 8))
+    vals = []
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        v, w, n, wall = cpu_throughput(args.precision, args.cpu_per_worker)
+        vals.append((v, n, wall))
+    tot = time.perf_counter() - t0
+    value = sum(n for _, n, _ in vals) / sum(wl for _, _, wl in vals)
+    line = {"metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(1e3 * tot / args.steps, 1), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": f"f64 work / {args.precision} matvec+inner (emulated)",
+            "data": "synthetic (reference generator restated in oracle/)", "impl": "reference",
+            "config": {"workload": f"c5: FP-BJ-CG L={L}, M={M} x N={N}, zeta={ZETA}, 16-QAM, SNR {SNR_DB} dB, "
+                                   f"{ITERS} iters", "batch_per_step": vals[0][1]},
+            "cpu_baseline": {"value": round(value, 2), "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+                             "sample": f"{vals[0][1]} realizations per step, {args.cpu_per_worker}/process"},
+            "e2e": {"value": round(value, 2), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--precision", choices=["fp16", "fp64"], default="fp16")
+    ap.add_argument("--T", type=int, default=1 << 20)
+    ap.add_argument("--e2e-T", dest="e2e_T", type=int, default=1 << 15)
+    ap.add_argument("--cpu-per-worker", dest="cpu_per_worker", type=int, default=64)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

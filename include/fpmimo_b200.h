@@ -126,6 +126,10 @@ int fpm_detect_host(const double* H, const double* y, const uint8_t* tx_bits, in
  * entry points), for launch accounting in benchmarks. */
 int64_t fpm_launch_count(void);
 
+/* Diagnostic: measured rate of non-fused fp64 DMUL/DADD operations per
+ * second on the current device (synchronous; the fp64 roofline denominator). */
+int fpm_probe_fp64(int64_t iters, double* dp_ops_per_s);
+
 #ifdef __cplusplus
 }
 #endif

@@ -465,6 +465,26 @@ __global__ void fpm_slice_kernel(const double2* __restrict__ x, const uint8_t* _
   }
 }
 
+// ---------------------------------------------------------------------------
+// FP64 issue-rate probe: independent non-fused DMUL/DADD chains (the only DP
+// ops the bit-exact Gram may use).  Gives the denominator of the fp64
+// roofline, which MEASURED_PEAKS.json does not carry.
+// ---------------------------------------------------------------------------
+__global__ void fpm_dp_probe_kernel(double* out, long iters) {
+  double a[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) a[k] = 1.0 + 1e-3 * (threadIdx.x + k);
+  const double c1 = 0.999999999, c2 = 1e-9;
+  for (long i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = __dadd_rn(__dmul_rn(a[k], c1), c2);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += a[k];
+  if (s == 12345.678) out[0] = s;  // keep the work alive
+}
+
 // ===========================================================================
 // Host side
 // ===========================================================================
@@ -727,6 +747,32 @@ int fpm_limits(int32_t* max_n, int32_t* max_l, int32_t* max_m) {
 }
 
 int64_t fpm_launch_count(void) { return (int64_t)g_launches.load(); }
+
+int fpm_probe_fp64(int64_t iters, double* dp_ops_per_s) {
+  if (iters < 1 || !dp_ops_per_s) return FPM_EINVAL;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  double* d = nullptr;
+  if (cudaMalloc(&d, sizeof(double)) != cudaSuccess) return FPM_ECUDA;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int tpb = 512, blocks = sms * 4;
+  fpm_dp_probe_kernel<<<blocks, tpb>>>(d, iters / 10 + 1);  // warm-up
+  cudaEventRecord(e0);
+  fpm_dp_probe_kernel<<<blocks, tpb>>>(d, iters);
+  cudaEventRecord(e1);
+  g_launches += 2;
+  int rc = cudaEventSynchronize(e1) == cudaSuccess ? FPM_OK : FPM_ECUDA;
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  *dp_ops_per_s = (double)blocks * tpb * (double)iters * 16.0 / (ms * 1e-3);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(d);
+  return rc;
+}
 
 int fpm_gram(const double* H, const double* y, int64_t T, int32_t M, int32_t N, double sigma2, double* A,
              double* b, void* stream) {

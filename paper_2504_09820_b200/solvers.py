@@ -71,6 +71,14 @@ class BatchBlocks:
     `.mats` gives the reference's list-of-(T, Lk, Lk) view."""
 
     def __init__(self, packed, N: int, L: int):
+        # a ragged tail block makes the natural concatenation shorter than
+        # the fixed N*L stride; pad it
+        if packed.shape[1] < N * L:
+            if _is_torch(packed):
+                torch = _torch()
+                packed = torch.nn.functional.pad(packed, (0, N * L - packed.shape[1]))
+            else:
+                packed = np.pad(np.asarray(packed), ((0, 0), (0, N * L - packed.shape[1])))
         self.packed = packed
         self.N = N
         self.L = L

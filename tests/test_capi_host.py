@@ -24,7 +24,7 @@ def lib():
 
 def _declared():
     text = open(HEADER).read()
-    return sorted(set(re.findall(r"\b(fpm_[a-z_]+)\s*\(", text)))
+    return sorted(set(re.findall(r"\b(fpm_[a-z0-9_]+)\s*\(", text)))
 
 
 def test_header_declares_expected_entry_points():

@@ -110,3 +110,16 @@ def test_qam64_round_trip_extension(oracle):
     s = oracle.mod64(bits)
     np.testing.assert_array_equal(oracle.demod64(s), bits)
     assert np.mean(np.abs(s) ** 2) == pytest.approx(1.0, rel=0.1)
+
+
+def test_fast_paths_equal_restatement(oracle):
+    rng = np.random.default_rng(11)
+    x = rng.standard_normal(100000) * np.exp(rng.uniform(-40, 40, 100000))
+    x = np.concatenate([x, [0.0, -0.0, np.inf, -np.inf, np.nan, 65504, 65520, 2**-24, 2**-25, 3 * 2**-26]])
+    for f in (oracle.FP16, oracle.FP32):
+        assert bits_equal(oracle.fmt_round(x, f), oracle.fmt_round_bits(x, f)), f.name
+    H = (rng.standard_normal((3, 40, 12)) + 1j * rng.standard_normal((3, 40, 12))) / 9
+    y = rng.standard_normal((3, 40)) + 1j * rng.standard_normal((3, 40))
+    a1, b1 = oracle.gram_mf(H, y, 0.03)
+    a2, b2 = oracle.gram_mf_einsum(H, y, 0.03)
+    assert bits_equal(a1, a2) and bits_equal(b1, b2)
