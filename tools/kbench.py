@@ -1,0 +1,105 @@
+#!/usr/bin/env python
+"""Per-kernel timing on the c5 shape (development tool, not the bench).
+
+    python tools/kbench.py [--T 65536] [--reps 5] [--only detect|gram|cg]
+
+Times fpm_gram, fpm_cg (A from HBM) and the fused fpm_detect with CUDA events
+on the launching stream; prints ms per launch, detections/s and the fp64 /
+HBM rooflines of each.
+"""
+
+import argparse
+import ctypes
+import json
+import math
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+from paper_2504_09820_b200 import _lib  # noqa: E402
+from paper_2504_09820_b200.detect import DetectorSpec  # noqa: E402
+from paper_2504_09820_b200.solvers import _stream  # noqa: E402
+
+
+def timeit(fn, reps):
+    fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        fn()
+    e1.record()
+    e1.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--T", type=int, default=65536)
+    ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--only", default="")
+    ap.add_argument("--precision", default="fp16")
+    ap.add_argument("--M", type=int, default=bench.M)
+    ap.add_argument("--N", type=int, default=bench.N)
+    ap.add_argument("--L", type=int, default=bench.L)
+    a = ap.parse_args()
+    bench.M, bench.N, bench.L = a.M, a.N, a.L
+    M, N, L, T = a.M, a.N, a.L, a.T
+    lib = _lib.load()
+    dev = torch.device("cuda", 0)
+    H, y, bits = bench.gen_inputs(T, 0, dev)
+    det = DetectorSpec("fp_bj_cg", iters=bench.ITERS, L=L, matvec=a.precision, inner=a.precision)
+    ps = _lib.precision_struct(det.precision())
+    A = torch.empty((T, N, N), dtype=torch.complex128, device=dev)
+    b = torch.empty((T, N), dtype=torch.complex128, device=dev)
+    x = torch.empty((T, N), dtype=torch.complex128, device=dev)
+    mv = torch.zeros((T, N * L), dtype=torch.complex128, device=dev)
+    brk = torch.empty((T,), dtype=torch.int32, device=dev)
+    div = torch.empty((T,), dtype=torch.int32, device=dev)
+    cnt = torch.zeros((8,), dtype=torch.int64, device=dev)
+    st = _stream()
+    out = {}
+    fg = 4 * M * N * (N + 1) + 8 * M * N
+    pk = ctypes.c_double()
+    _lib.check(lib.fpm_probe_fp64(200000, ctypes.byref(pk)), "probe")
+    out["fp64_peak_tops"] = pk.value / 1e12
+
+    def gram():
+        _lib.check(lib.fpm_gram(H.data_ptr(), y.data_ptr(), T, M, N, bench.SIGMA2, A.data_ptr(), b.data_ptr(), st),
+                   "gram")
+
+    def bj():
+        _lib.check(lib.fpm_bj_setup(A.data_ptr(), T, N, L, 0, mv.data_ptr(), None, st), "bj")
+
+    def cg():
+        _lib.check(lib.fpm_cg(A.data_ptr(), b.data_ptr(), mv.data_ptr(), T, N, L, bench.ITERS, ps, 0, x.data_ptr(),
+                              brk.data_ptr(), div.data_ptr(), st), "cg")
+
+    def fused():
+        _lib.check(lib.fpm_detect(H.data_ptr(), y.data_ptr(), bits.data_ptr(), T, M, N, bench.SIGMA2, 3, L,
+                                  bench.ITERS, ps, 0, 16, None, x.data_ptr(), brk.data_ptr(), div.data_ptr(), None,
+                                  cnt.data_ptr(), st), "detect")
+
+    if a.only in ("", "gram"):
+        ms = timeit(gram, a.reps)
+        out["gram"] = {"ms": ms, "det_s": T / ms * 1e3, "fp64_frac": fg * T / (ms / 1e3) / pk.value}
+    if a.only in ("", "cg"):
+        gram()
+        bj()
+        ms = timeit(cg, a.reps)
+        byts = 16 * N * N + 16 * N * (2 + L) + 8
+        out["cg"] = {"ms": ms, "det_s": T / ms * 1e3, "hbm_gbs": byts * T / (ms / 1e3) / 1e9,
+                     "hbm_frac": byts * T / (ms / 1e3) / 6554.9e9}
+    if a.only in ("", "detect"):
+        ms = timeit(fused, a.reps)
+        out["detect"] = {"ms": ms, "det_s": T / ms * 1e3, "fp64_frac": fg * T / (ms / 1e3) / pk.value}
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()
