@@ -130,6 +130,10 @@ int64_t fpm_launch_count(void);
  * second on the current device (synchronous; the fp64 roofline denominator). */
 int fpm_probe_fp64(int64_t iters, double* dp_ops_per_s);
 
+/* Diagnostic: device buffer (int64[16]) that subsequent fpm_detect launches
+ * fill with clock64() phase stamps from CTA 0 (NULL disables). */
+int fpm_debug_set_trace(int64_t* dev_buf);
+
 #ifdef __cplusplus
 }
 #endif

@@ -16,42 +16,62 @@
 //   frozen lanes never resume (so per-lane early exit is exact).
 //
 // Sequential accumulation order is part of the contract (linalg.py:65-68,
-// 94-95): every dot product is ONE dependent chain in one thread, every
-// matvec row is one chain; parallelism comes from rows and realizations.
+// 94-95).  Latency design: the product terms of every dot product are
+// formed in parallel by the row threads (each is an independent rounded
+// complex multiply), and only the left-to-right SUM runs as one dependent
+// chain in one thread per realization; matvec rows are chains in parallel.
+// Six CTA barriers per iteration.
 #pragma once
 #include "fpm_arith.cuh"
 
 namespace fpm {
 
-template <int MVK>
+template <int MVK, int IPK>
 struct CgSmem {
   typedef typename Ar<MVK>::C MC;
-  int R, N, L, nblk, ldA;
+  typedef typename Ar<IPK>::C IC;
+  int R, N, L, ldA;
   MC* At;          // R * N * ldA, transposed: entry (i,k) at k*ldA + i
   MC* pmv;         // R * N   p rounded to u_MV
+  IC *tphi, *trho, *tr1;  // R * N product terms of p^H w, r^H p, r^H z (or r^H r)
   double2* minv;   // R * N*L block inverses (block kb at kb*L*L, row-major Lk x Lk), on the u_W grid
   double2 *b, *x, *r, *p, *z, *w, *xn, *rn;  // R * N each
-  double2* sc;     // R * 8 : alpha, beta, phi, rho0, carry, rho1
+  double2* sc;     // R * 8 : 0 alpha, 1 beta, 3 rho0, 4 carry
   int* fl;         // R * 4 : live, nonfinite, breakdown_at, diverged_at
 };
 
-// Owner thread of dot product `which` (0/1) of slot g: prefer threads past
-// the matvec rows, one per warp, so the chains run in parallel.
-__device__ __forceinline__ int dot_owner(int g, int which, int R, int rows, int nthreads) {
+// Owner of the sequential sums of slot g: past the matvec rows when possible,
+// one warp apart so the R chains run in parallel.
+__device__ __forceinline__ int dot_owner(int g, int which, int rows, int nthreads) {
   int k = g * 2 + which;
   int cand = nthreads - 1 - 32 * k;
   if (cand >= rows && cand >= 0) return cand;
   return (nthreads - 1 - k) % nthreads;
 }
 
-// u^H v over n entries, products and sums at the IP format (dot_fp).
+// left-to-right sum t_0 + t_1 + ... (dot_fp's accumulation, linalg.py:94-95)
 template <int IPK>
-__device__ __forceinline__ double2 dot_ip(const double2* u, const double2* v, int n, const FmtP& f) {
+__device__ __forceinline__ double2 chain_sum(const typename Ar<IPK>::C* t, int n, const FmtP& f) {
   typedef Ar<IPK> A;
-  typename A::C s = A::mulc(A::rnd(u[0], f), A::rnd(v[0], f), f);
-  for (int k = 1; k < n; ++k) s = A::add(s, A::mulc(A::rnd(u[k], f), A::rnd(v[k], f), f), f);
+  typename A::C s = t[0];
+  int k = 1;
+  for (; k + 8 <= n; k += 8) {
+    typename A::C v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = t[k + j];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s = A::add(s, v[j], f);
+  }
+  for (; k < n; ++k) s = A::add(s, t[k], f);
   double2 d = A::wide(s);
   return assemble(d.x, d.y);
+}
+
+// conj(u) * v term at the IP format (inputs rounded into it, dot_fp)
+template <int IPK>
+__device__ __forceinline__ typename Ar<IPK>::C ip_term(double2 u, double2 v, const FmtP& f) {
+  typedef Ar<IPK> A;
+  return A::mulc(A::rnd(u, f), A::rnd(v, f), f);
 }
 
 // one row of the block-diagonal apply M r (solvers.py:222-225) at u_W
@@ -68,15 +88,41 @@ __device__ __forceinline__ double2 bj_row(const double2* minv, const double2* r,
   return assemble(s.x, s.y);
 }
 
+// w_i = sum_k A(i,k) p_k at u_MV (matvec_fp), A column-major in shared memory
+template <int MVK>
+__device__ __forceinline__ double2 mv_row(const typename Ar<MVK>::C* col, const typename Ar<MVK>::C* pv, int N,
+                                          int ldA, const FmtP& f) {
+  typedef Ar<MVK> A;
+  typename A::C s = A::mul(col[0], pv[0], f);
+  int k = 1;
+  for (; k + 8 <= N; k += 8) {
+    typename A::C t[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) t[j] = A::mul(col[(long)(k + j) * ldA], pv[k + j], f);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s = A::add(s, t[j], f);
+  }
+  for (; k < N; ++k) s = A::add(s, A::mul(col[(long)k * ldA], pv[k], f), f);
+  double2 d = A::wide(s);
+  return assemble(d.x, d.y);
+}
+
+// phase timestamps (diagnostic): thread 0 of CTA 0 writes clock64 values
+#define FPM_STAMP(tr, k)                                      \
+  do {                                                        \
+    if ((tr) && tid == 0) (tr)[(k)] = (long long)clock64();   \
+  } while (0)
+
 template <int WK, int MVK, int IPK>
-__device__ void cg_team(CgSmem<MVK>& S, int Rv, int iters, bool bj, bool textbook, const Prec& pr,
-                        int nthreads, int tid) {
+__device__ void cg_team(CgSmem<MVK, IPK>& S, int Rv, int iters, bool bj, bool textbook, const Prec& pr,
+                        int nthreads, int tid, long long* tr = nullptr) {
   typedef Ar<MVK> MV;
   const int N = S.N;
   const int RN = Rv * N;
   const FmtP& fw = pr.work;
   const FmtP& fm = pr.mv;
   const FmtP& fi = pr.ip;
+  const bool rho_fresh = bj && !textbook;  // as_written: rho0 = r^H p every sweep
 
   // ---- init (solvers.py:297-328) ----
   for (int q = tid; q < RN; q += nthreads) {
@@ -92,49 +138,50 @@ __device__ void cg_team(CgSmem<MVK>& S, int Rv, int iters, bool bj, bool textboo
   __syncthreads();
   for (int q = tid; q < RN; q += nthreads) {
     const int g = q / N, i = q - g * N;
-    double2 pv = bj ? bj_row<WK>(S.minv + (long)g * N * S.L, S.r + g * N, i, S.L, N, fw) : S.r[q];
+    const double2 rv = S.r[q];
+    const double2 pv = bj ? bj_row<WK>(S.minv + (long)g * N * S.L, S.r + g * N, i, S.L, N, fw) : rv;
     S.p[q] = pv;
     S.pmv[q] = MV::rnd(pv, fm);
+    S.tr1[q] = ip_term<IPK>(rv, (bj && textbook) ? pv : rv, fi);  // carry terms
+    if (rho_fresh) S.trho[q] = ip_term<IPK>(rv, pv, fi);
   }
   __syncthreads();
-  if (!bj || textbook) {
+  if (!rho_fresh) {
     for (int g = 0; g < Rv; ++g)
-      if (tid == dot_owner(g, 0, Rv, RN, nthreads))
-        S.sc[g * 8 + 4] = dot_ip<IPK>(S.r + g * N, bj ? S.p + g * N : S.r + g * N, N, fi);
+      if (tid == dot_owner(g, 0, RN, nthreads)) S.sc[g * 8 + 4] = chain_sum<IPK>(S.tr1 + g * N, N, fi);
   }
   __syncthreads();
 
   for (int it = 1; it <= iters; ++it) {
-    // ---- w = A p (u_MV), and for BJ as_written rho0 = r^H p ----
+    // ---- A: w = A p (u_MV) + phi terms;  rho0 = sum r^H p (BJ as_written) ----
     for (int q = tid; q < RN; q += nthreads) {
       const int g = q / N, i = q - g * N;
       if (!S.fl[g * 4]) continue;
-      const typename MV::C* col = S.At + (long)g * N * S.ldA + i;
-      const typename MV::C* pv = S.pmv + g * N;
-      typename MV::C s = MV::mul(col[0], pv[0], fm);
-      for (int k = 1; k < N; ++k) s = MV::add(s, MV::mul(col[(long)k * S.ldA], pv[k], fm), fm);
-      double2 d = MV::wide(s);
-      S.w[q] = assemble(d.x, d.y);
+      const double2 wv = mv_row<MVK>(S.At + (long)g * N * S.ldA + i, S.pmv + g * N, N, S.ldA, fm);
+      S.w[q] = wv;
+      S.tphi[q] = ip_term<IPK>(S.p[q], wv, fi);
     }
-    if (bj && !textbook) {
+    if (rho_fresh) {
       for (int g = 0; g < Rv; ++g)
-        if (tid == dot_owner(g, 1, Rv, RN, nthreads) && S.fl[g * 4])
-          S.sc[g * 8 + 3] = dot_ip<IPK>(S.r + g * N, S.p + g * N, N, fi);
+        if (tid == dot_owner(g, 1, RN, nthreads) && S.fl[g * 4])
+          S.sc[g * 8 + 3] = chain_sum<IPK>(S.trho + g * N, N, fi);
     }
     __syncthreads();
-    // ---- phi, flags, alpha ----
+    if (it == 1) FPM_STAMP(tr, 0);
+    // ---- B: phi, flags, alpha ----
     for (int g = 0; g < Rv; ++g) {
-      if (tid != dot_owner(g, 0, Rv, RN, nthreads) || !S.fl[g * 4]) continue;
-      double2 phi = dot_ip<IPK>(S.p + g * N, S.w + g * N, N, fi);
-      double2 rho0 = (bj && !textbook) ? S.sc[g * 8 + 3] : S.sc[g * 8 + 4];
+      if (tid != dot_owner(g, 0, RN, nthreads) || !S.fl[g * 4]) continue;
+      const double2 phi = chain_sum<IPK>(S.tphi + g * N, N, fi);
+      const double2 rho0 = rho_fresh ? S.sc[g * 8 + 3] : S.sc[g * 8 + 4];
       S.sc[g * 8 + 3] = rho0;
-      bool stall = (rho0.x == 0.0) && (rho0.y == 0.0);
+      const bool stall = (rho0.x == 0.0) && (rho0.y == 0.0);
       if (!stall && phi.x <= 0.0) S.fl[g * 4 + 2] = it;  // breakdown
       if (stall || phi.x <= 0.0) S.fl[g * 4] = 0;
       S.sc[g * 8 + 0] = wdiv<WK>(rho0, phi, fw);
     }
     __syncthreads();
-    // ---- x, r updates (u_W) + finiteness ----
+    if (it == 1) FPM_STAMP(tr, 1);
+    // ---- C: x, r updates (u_W) + finiteness ----
     for (int q = tid; q < RN; q += nthreads) {
       const int g = q / N;
       if (!S.fl[g * 4]) continue;
@@ -146,48 +193,55 @@ __device__ void cg_team(CgSmem<MVK>& S, int Rv, int iters, bool bj, bool textboo
       if (!(finite2(xn) && finite2(rn))) S.fl[g * 4 + 1] = 1;
     }
     __syncthreads();
-    for (int q = tid; q < RN; q += nthreads) {  // commit (same thread wrote xn/rn)
-      const int g = q / N;
-      if (S.fl[g * 4] && !S.fl[g * 4 + 1]) {
-        S.x[q] = S.xn[q];
-        S.r[q] = S.rn[q];
+    if (it == 1) FPM_STAMP(tr, 2);
+    // ---- D: commit; z = M r_new; rho1 terms ----
+    for (int q = tid; q < RN; q += nthreads) {
+      const int g = q / N, i = q - g * N;
+      if (!S.fl[g * 4] || S.fl[g * 4 + 1]) continue;
+      const double2 rn = S.rn[q];
+      S.x[q] = S.xn[q];
+      S.r[q] = rn;
+      if (bj) {
+        const double2 zv = bj_row<WK>(S.minv + (long)g * N * S.L, S.rn + g * N, i, S.L, N, fw);
+        S.z[q] = zv;
+        S.tr1[q] = ip_term<IPK>(rn, zv, fi);
+      } else {
+        S.tr1[q] = ip_term<IPK>(rn, rn, fi);
       }
     }
     __syncthreads();
-    if (bj) {
-      for (int q = tid; q < RN; q += nthreads) {
-        const int g = q / N, i = q - g * N;
-        if (S.fl[g * 4] && !S.fl[g * 4 + 1])
-          S.z[q] = bj_row<WK>(S.minv + (long)g * N * S.L, S.r + g * N, i, S.L, N, fw);
-      }
-      __syncthreads();
-    }
-    // ---- rho1, beta, flags ----
+    if (it == 1) FPM_STAMP(tr, 3);
+    // ---- E: rho1, beta, divergence flag ----
     for (int g = 0; g < Rv; ++g) {
-      if (tid != dot_owner(g, 0, Rv, RN, nthreads) || !S.fl[g * 4]) continue;
-      if (S.fl[g * 4 + 1]) {  // non-finite update: diverged, frozen
+      if (tid != dot_owner(g, 0, RN, nthreads) || !S.fl[g * 4]) continue;
+      if (S.fl[g * 4 + 1]) {  // non-finite update: diverged, frozen at the last finite iterate
         S.fl[g * 4 + 3] = it;
         S.fl[g * 4] = 0;
         continue;
       }
-      double2 rho1 = dot_ip<IPK>(S.r + g * N, bj ? S.z + g * N : S.r + g * N, N, fi);
+      const double2 rho1 = chain_sum<IPK>(S.tr1 + g * N, N, fi);
       S.sc[g * 8 + 1] = wdiv<WK>(rho1, S.sc[g * 8 + 3], fw);
       S.sc[g * 8 + 4] = rho1;
     }
     __syncthreads();
-    // ---- p = (z|r) + beta p ; pmv = rnd(p) ----
+    if (it == 1) FPM_STAMP(tr, 4);
+    // ---- F: p = (z|r) + beta p ; pmv = rnd(p) ; next rho0 terms ----
     int any = 0;
     for (int q = tid; q < RN; q += nthreads) {
       const int g = q / N;
       if (!S.fl[g * 4]) continue;
       any = 1;
-      double2 pn = axpy1<WK>(S.sc[g * 8 + 1], S.p[q], bj ? S.z[q] : S.r[q], fw);
+      const double2 pn = axpy1<WK>(S.sc[g * 8 + 1], S.p[q], bj ? S.z[q] : S.r[q], fw);
       S.p[q] = pn;
       S.pmv[q] = MV::rnd(pn, fm);
+      if (rho_fresh) S.trho[q] = ip_term<IPK>(S.r[q], pn, fi);
     }
-    if (!__syncthreads_or(any)) break;
+    const int more = __syncthreads_or(any);
+    if (it == 1) FPM_STAMP(tr, 5);
+    if (!more) break;
   }
   __syncthreads();
+  FPM_STAMP(tr, 6);
 }
 
 }  // namespace fpm

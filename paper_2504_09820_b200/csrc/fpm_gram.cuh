@@ -108,10 +108,17 @@ __device__ __forceinline__ void gram_issue(const double2* H, long t0, int Rv, co
 // final A entry (both triangles) and every b entry.
 //   emit.a(g, i, j, value)   value already in its final (reference) bits
 //   emit.b(g, n, value)
+// bars: full[0..S-1], empty[S..2S-1], y-barrier [2S]; full/y count 1,
+// empty count = warps per CTA.  Thread 0 is the (lagging) producer: before
+// consuming chunk c it refills the stage chunk c-1 used once every warp has
+// released it, so warps are never forced into lockstep.
 template <class Emit>
 __device__ void gram_run(const double2* __restrict__ H, const double2* __restrict__ y, long t0, int Rv,
-                         const GramGeom& G, double sigma2, double2* stages, double2* ys, uint64_t* full,
-                         uint64_t* ybar, int nthreads, int tid, Emit& emit) {
+                         const GramGeom& G, double sigma2, double2* stages, double2* ys, uint64_t* bars,
+                         int nthreads, int tid, Emit& emit) {
+  uint64_t* full = bars;
+  uint64_t* empty = bars + G.S;
+  uint64_t* ybar = bars + 2 * G.S;
   const int nchunks = (G.M + G.MC - 1) / G.MC;
   const long stage_elems = (long)G.R * G.MC * G.Np;
   if (tid == 0) {
@@ -143,6 +150,11 @@ __device__ void gram_run(const double2* __restrict__ H, const double2* __restric
   const int nb = G.nb;
   for (int c = 0; c < nchunks; ++c) {
     const int s = c % G.S;
+    if (tid == 0 && c >= 1 && c - 1 + G.S < nchunks) {
+      const int ps = (c - 1) % G.S;
+      mbar_wait(&empty[ps], (uint32_t)(((c - 1) / G.S) & 1));
+      gram_issue(H, t0, Rv, G, c - 1 + G.S, stages + ps * stage_elems, &full[ps]);
+    }
     mbar_wait(&full[s], (uint32_t)((c / G.S) & 1));
     const double2* sb = stages + s * stage_elems;
     const int m0 = c * G.MC;
@@ -201,9 +213,10 @@ __device__ void gram_run(const double2* __restrict__ H, const double2* __restric
         }
       }
     }
-    __syncthreads();  // stage s fully consumed
-    if (tid == 0 && c + G.S < nchunks) gram_issue(H, t0, Rv, G, c + G.S, stages + s * stage_elems, &full[s]);
+    __syncwarp();
+    if ((tid & 31) == 0) mbar_arrive(&empty[s]);  // this warp is done with stage s
   }
+  __syncthreads();  // every warp is past the last stage before the epilogue reuses it
 
   // ---- epilogue: final reference bits for both triangles ----
   if (active) {

@@ -23,6 +23,7 @@
 namespace fpm {
 
 static std::atomic<long long> g_launches{0};
+static long long* g_trace = nullptr;  // diagnostic phase timestamps (fpm_debug_set_trace)
 
 constexpr int kMaxN = 128;
 constexpr int kMaxL = 16;
@@ -157,13 +158,14 @@ struct DetectArgs {
   GramGeom G;
   int ldA;
   // dynamic shared memory offsets (bytes)
-  int off_ys, off_union, off_minv, off_scr, off_vec, off_pmv, off_sc, off_fl;
+  int off_ys, off_union, off_minv, off_scr, off_vec, off_pmv, off_tip, off_sc, off_fl;
   int smem_bytes;
+  long long* trace;  // nullable: [0] start [1] gram done [2] bj done [3..9] cg phases it=1 [10] cg done [11] end
 };
 
-template <int WK, int MVK>
+template <int WK, int MVK, int IPK>
 struct EmitSmem {
-  CgSmem<MVK>* S;
+  CgSmem<MVK, IPK>* S;
   const FmtP* fm;
   int bj;
   __device__ __forceinline__ void a(int g, int i, int j, double2 v) {
@@ -191,9 +193,10 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_kernel(const DetectArgs arg
   const int Rv = (int)min((long)G.R, args.T - t0);
   const int N = G.N;
 
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem);  // S full + 1 y
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem);  // S full, S empty, 1 y
   __shared__ unsigned long long cnt[FPM_NCOUNTERS];
-  CgSmem<MVK> S;
+  typedef typename Ar<IPK>::C IC;
+  CgSmem<MVK, IPK> S;
   S.R = G.R;
   S.N = N;
   S.L = args.bj ? args.L : 1;
@@ -211,24 +214,34 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_kernel(const DetectArgs arg
   S.xn = vec + 6 * RN;
   S.rn = vec + 7 * RN;
   S.pmv = reinterpret_cast<MC*>(smem + args.off_pmv);
+  S.tphi = reinterpret_cast<IC*>(smem + args.off_tip);
+  S.trho = S.tphi + RN;
+  S.tr1 = S.trho + RN;
   S.sc = reinterpret_cast<double2*>(smem + args.off_sc);
   S.fl = reinterpret_cast<int*>(smem + args.off_fl);
 
   if (tid == 0) {
-    for (int s = 0; s <= G.S; ++s) mbar_init(&bars[s], 1);
+    for (int s = 0; s < G.S; ++s) {
+      mbar_init(&bars[s], 1);
+      mbar_init(&bars[G.S + s], nthreads / 32);
+    }
+    mbar_init(&bars[2 * G.S], 1);
     fence_mbar_init();
   }
   if (tid < FPM_NCOUNTERS) cnt[tid] = 0ULL;
   for (int g = tid; g < G.R; g += nthreads) S.fl[g * 4] = g < Rv ? 1 : 0;
+  long long* tr = (args.trace && blockIdx.x == 0) ? args.trace : nullptr;
+  FPM_STAMP(tr, 0);
   __syncthreads();
 
   // 1) Gram + matched filter straight into shared memory
-  EmitSmem<WK, MVK> em;
+  EmitSmem<WK, MVK, IPK> em;
   em.S = &S;
   em.fm = &args.pr.mv;
   em.bj = args.bj && !args.minv_in;
   gram_run(args.H, args.y, t0, Rv, G, args.sigma2, reinterpret_cast<double2*>(smem + args.off_union),
-           reinterpret_cast<double2*>(smem + args.off_ys), bars, &bars[G.S], nthreads, tid, em);
+           reinterpret_cast<double2*>(smem + args.off_ys), bars, nthreads, tid, em);
+  FPM_STAMP(tr, 1);
 
   // 2) block-Jacobi inverses (on-chip fp64 Cholesky, or injected)
   if (args.bj) {
@@ -257,8 +270,10 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_kernel(const DetectArgs arg
     __syncthreads();
   }
 
+  FPM_STAMP(tr, 2);
   // 3) CG in shared memory
-  cg_team<WK, MVK, IPK>(S, Rv, args.iters, args.bj != 0, args.textbook != 0, args.pr, nthreads, tid);
+  cg_team<WK, MVK, IPK>(S, Rv, args.iters, args.bj != 0, args.textbook != 0, args.pr, nthreads, tid,
+                        tr ? tr + 3 : nullptr);
 
   // 4) slicer + counters + write-back
   const int bps = 2 * args.sl.bpa;
@@ -290,6 +305,7 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_kernel(const DetectArgs arg
   }
   if (tid == 0) atomicAdd(&cnt[FPM_CNT_TRIALS], (unsigned long long)Rv);
   block_add_counters(cnt, args.counters, tid, nthreads);
+  FPM_STAMP(tr, 11);
 }
 
 // ---------------------------------------------------------------------------
@@ -325,7 +341,11 @@ __global__ void __launch_bounds__(512, 1) fpm_gram_kernel(const GramArgs args) {
   const int Rv = (int)min((long)G.R, args.T - t0);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
   if (tid == 0) {
-    for (int s = 0; s <= G.S; ++s) mbar_init(&bars[s], 1);
+    for (int s = 0; s < G.S; ++s) {
+      mbar_init(&bars[s], 1);
+      mbar_init(&bars[G.S + s], nthreads / 32);
+    }
+    mbar_init(&bars[2 * G.S], 1);
     fence_mbar_init();
   }
   __syncthreads();
@@ -335,7 +355,7 @@ __global__ void __launch_bounds__(512, 1) fpm_gram_kernel(const GramArgs args) {
   em.t0 = t0;
   em.N = G.N;
   gram_run(args.H, args.y, t0, Rv, G, args.sigma2, reinterpret_cast<double2*>(smem + args.off_union),
-           reinterpret_cast<double2*>(smem + args.off_ys), bars, &bars[G.S], nthreads, tid, em);
+           reinterpret_cast<double2*>(smem + args.off_ys), bars, nthreads, tid, em);
 }
 
 // ---------------------------------------------------------------------------
@@ -381,18 +401,19 @@ struct CgArgs {
   double2* x;
   int* brk;
   int* div;
-  int off_minv, off_vec, off_pmv, off_sc, off_fl;
+  int off_minv, off_vec, off_pmv, off_tip, off_sc, off_fl;
 };
 
 template <int WK, int MVK, int IPK>
 __global__ void __launch_bounds__(256) fpm_cg_kernel(const CgArgs args) {
   extern __shared__ __align__(128) unsigned char smem[];
   typedef typename Ar<MVK>::C MC;
+  typedef typename Ar<IPK>::C IC;
   const int tid = threadIdx.x, nthreads = blockDim.x;
   const long t0 = (long)blockIdx.x * args.R;
   const int Rv = (int)min((long)args.R, args.T - t0);
   const int N = args.N;
-  CgSmem<MVK> S;
+  CgSmem<MVK, IPK> S;
   S.R = args.R;
   S.N = N;
   S.L = args.bj ? args.L : 1;
@@ -410,6 +431,9 @@ __global__ void __launch_bounds__(256) fpm_cg_kernel(const CgArgs args) {
   S.xn = vec + 6 * RN;
   S.rn = vec + 7 * RN;
   S.pmv = reinterpret_cast<MC*>(smem + args.off_pmv);
+  S.tphi = reinterpret_cast<IC*>(smem + args.off_tip);
+  S.trho = S.tphi + RN;
+  S.tr1 = S.trho + RN;
   S.sc = reinterpret_cast<double2*>(smem + args.off_sc);
   S.fl = reinterpret_cast<int*>(smem + args.off_fl);
 
@@ -598,7 +622,7 @@ static int gram_threads(const GramGeom& G) {
 }
 
 // Plan the fused kernel for (M, N, L, kinds); returns false if it cannot fit.
-static bool plan_detect(int M, int N, int L, int bj, int mvk, DetectArgs& a, int& threads) {
+static bool plan_detect(int M, int N, int L, int bj, int mvk, int ipk, DetectArgs& a, int& threads) {
   const int Np = (N + 7) / 8 * 8;
   int R = std::max(1, 256 / Np);
   const int limit = max_smem_optin();
@@ -608,7 +632,7 @@ static bool plan_detect(int M, int N, int L, int bj, int mvk, DetectArgs& a, int
     threads = gram_threads(G);
     if (threads > 512) continue;
     const int ldA = N + 1;
-    size_t off = 64;  // mbarriers
+    size_t off = 128;  // mbarriers (2S+1)
     a.off_ys = (int)off;
     off = align_up(off + (size_t)R * M * 16, 128);
     a.off_union = (int)off;
@@ -624,6 +648,8 @@ static bool plan_detect(int M, int N, int L, int bj, int mvk, DetectArgs& a, int
     off = align_up(off + (size_t)8 * R * N * 16, 128);
     a.off_pmv = (int)off;
     off = align_up(off + (size_t)R * N * mv_bytes(mvk), 128);
+    a.off_tip = (int)off;
+    off = align_up(off + (size_t)3 * R * N * mv_bytes(ipk), 128);
     a.off_sc = (int)off;
     off = align_up(off + (size_t)R * 8 * 16, 128);
     a.off_fl = (int)off;
@@ -639,7 +665,7 @@ static bool plan_detect(int M, int N, int L, int bj, int mvk, DetectArgs& a, int
   return false;
 }
 
-static bool plan_cg(int N, int L, int bj, int mvk, CgArgs& a, int& smem) {
+static bool plan_cg(int N, int L, int bj, int mvk, int ipk, CgArgs& a, int& smem) {
   const int limit = std::min(max_smem_optin(), 110 * 1024);  // aim for >= 2 CTAs / SM
   int R = std::max(1, 256 / N);
   for (; R >= 1; R = (R > 1 ? R / 2 : 0)) {
@@ -652,6 +678,8 @@ static bool plan_cg(int N, int L, int bj, int mvk, CgArgs& a, int& smem) {
     off = align_up(off + (size_t)8 * R * N * 16, 128);
     a.off_pmv = (int)off;
     off = align_up(off + (size_t)R * N * mv_bytes(mvk), 128);
+    a.off_tip = (int)off;
+    off = align_up(off + (size_t)3 * R * N * mv_bytes(ipk), 128);
     a.off_sc = (int)off;
     off = align_up(off + (size_t)R * 8 * 16, 128);
     a.off_fl = (int)off;
@@ -748,6 +776,11 @@ int fpm_limits(int32_t* max_n, int32_t* max_l, int32_t* max_m) {
 
 int64_t fpm_launch_count(void) { return (int64_t)g_launches.load(); }
 
+int fpm_debug_set_trace(int64_t* dev_buf) {
+  g_trace = reinterpret_cast<long long*>(dev_buf);
+  return FPM_OK;
+}
+
 int fpm_probe_fp64(int64_t iters, double* dp_ops_per_s) {
   if (iters < 1 || !dp_ops_per_s) return FPM_EINVAL;
   int dev = 0, sms = 148;
@@ -793,8 +826,8 @@ int fpm_gram(const double* H, const double* y, int64_t T, int32_t M, int32_t N, 
   for (; R >= 1; R = R > 1 ? R / 2 : 0) {
     gram_geom(R, M, N, a.G);
     threads = gram_threads(a.G);
-    a.off_ys = 64;
-    a.off_union = (int)align_up(64 + (size_t)R * M * 16, 128);
+    a.off_ys = 128;
+    a.off_union = (int)align_up(128 + (size_t)R * M * 16, 128);
     smem = a.off_union + (size_t)a.G.S * R * a.G.MC * a.G.Np * 16;
     if (threads <= 512 && (long)smem <= max_smem_optin()) break;
     if (R == 1) return FPM_EUNSUPPORTED;
@@ -874,7 +907,7 @@ int fpm_cg(const double* A, const double* b, const double* Minv, int64_t T, int3
   a.brk = breakdown_at;
   a.div = diverged_at;
   int smem = 0;
-  if (!plan_cg(N, a.L, bj, k.mv, a, smem)) return FPM_EUNSUPPORTED;
+  if (!plan_cg(N, a.L, bj, k.mv, k.ip, a, smem)) return FPM_EUNSUPPORTED;
   return launch_cg(k, a, smem, (cudaStream_t)stream);
 }
 
@@ -928,8 +961,9 @@ static int detect_args(const double* H, const double* y, const uint8_t* tx_bits,
   a.rx = rx;
   a.counters = reinterpret_cast<unsigned long long*>(counters);
   a.sl = make_slicer(qam);
+  a.trace = g_trace;
   k = pick_kinds(*pp);
-  if (!plan_detect(M, N, a.L, bj, k.mv, a, threads)) return FPM_EUNSUPPORTED;
+  if (!plan_detect(M, N, a.L, bj, k.mv, k.ip, a, threads)) return FPM_EUNSUPPORTED;
   return FPM_OK;
 }
 

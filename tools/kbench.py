@@ -47,6 +47,7 @@ def main():
     ap.add_argument("--M", type=int, default=bench.M)
     ap.add_argument("--N", type=int, default=bench.N)
     ap.add_argument("--L", type=int, default=bench.L)
+    ap.add_argument("--trace", action="store_true")
     a = ap.parse_args()
     bench.M, bench.N, bench.L = a.M, a.N, a.L
     M, N, L, T = a.M, a.N, a.L, a.T
@@ -95,6 +96,23 @@ def main():
         byts = 16 * N * N + 16 * N * (2 + L) + 8
         out["cg"] = {"ms": ms, "det_s": T / ms * 1e3, "hbm_gbs": byts * T / (ms / 1e3) / 1e9,
                      "hbm_frac": byts * T / (ms / 1e3) / 6554.9e9}
+    if a.trace:
+        tr = torch.zeros(16, dtype=torch.int64, device=dev)
+        lib.fpm_debug_set_trace(tr.data_ptr())
+        fused()
+        torch.cuda.synchronize()
+        lib.fpm_debug_set_trace(None)
+        t = tr.cpu().tolist()
+        names = ["start", "gram", "bj", "A:matvec", "B:phi/alpha", "C:axpy", "D:commit/z", "E:rho1/beta",
+                 "F:p", "cg_rest(it>=2)", "-", "slice+writeback"]
+        prev = t[0]
+        out["trace_cycles"] = {}
+        for i, nm in enumerate(names):
+            if i == 0 or nm == "-" or t[i] == 0:
+                continue
+            out["trace_cycles"][nm] = t[i] - prev
+            prev = t[i]
+        out["trace_cycles"]["total"] = t[11] - t[0]
     if a.only in ("", "detect"):
         ms = timeit(fused, a.reps)
         out["detect"] = {"ms": ms, "det_s": T / ms * 1e3, "fp64_frac": fg * T / (ms / 1e3) / pk.value}
