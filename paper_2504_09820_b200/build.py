@@ -1,47 +1,73 @@
 """Build libfpmimo_b200.so in-tree with nvcc for sm_100a.
 
-    python -m paper_2504_09820_b200.build
+    python -m paper_2504_09820_b200.build [--force]
 
-Flags: -fmad=false (no FMA contraction: the reference's arithmetic is
-separately rounded), no -use_fast_math / -ftz (subnormals are part of the
-contract), -lineinfo for ncu source views.
+Each format kind's kernels are a separate translation unit
+(csrc/fpm_inst_<kind>.cu) compiled in parallel, then linked with the host
+unit (csrc/fpm_host.cu).  Flags: -fmad=false (no FMA contraction: the
+reference's arithmetic is separately rounded), no -use_fast_math / -ftz
+(subnormals are part of the contract), -lineinfo for ncu source views.
 """
 
 from __future__ import annotations
 
+import concurrent.futures as cf
+import glob
 import os
 import subprocess
 import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SRC = os.path.join(HERE, "csrc", "fpm_kernels.cu")
-DEPS = [os.path.join(HERE, "csrc", f) for f in os.listdir(os.path.join(HERE, "csrc"))] + [
-    os.path.join(os.path.dirname(HERE), "include", "fpmimo_b200.h")]
+CSRC = os.path.join(HERE, "csrc")
+OBJ = os.path.join(HERE, "_obj")
 OUT = os.path.join(HERE, "libfpmimo_b200.so")
+HEADER = os.path.join(os.path.dirname(HERE), "include", "fpmimo_b200.h")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-fmad=false", "-std=c++17",
-         "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v"]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+FLAGS = ARCH + ["-O3", "-lineinfo", "-fmad=false", "-std=c++17", "-Xcompiler", "-fPIC"]
+
+
+def _units():
+    return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
+
+
+def _headers():
+    return sorted(glob.glob(os.path.join(CSRC, "*.cuh"))) + [HEADER]
 
 
 def needs_build() -> bool:
     if not os.path.exists(OUT):
         return True
     t = os.path.getmtime(OUT)
-    return any(os.path.getmtime(d) > t for d in DEPS)
+    return any(os.path.getmtime(d) > t for d in _units() + _headers())
+
+
+def _compile(src: str, verbose: bool) -> tuple[str, str]:
+    obj = os.path.join(OBJ, os.path.basename(src)[:-3] + ".o")
+    cmd = [NVCC, *FLAGS, "-c", src, "-o", obj] + (["-Xptxas", "-v"] if verbose else [])
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"nvcc failed on {src}:\n{r.stdout}{r.stderr}")
+    return obj, r.stderr
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
-    if force or needs_build():
-        cmd = [NVCC, *FLAGS, "-o", OUT + ".tmp", SRC]
-        r = subprocess.run(cmd, capture_output=True, text=True)
-        if r.returncode != 0:
-            sys.stderr.write(r.stdout + r.stderr)
-            raise RuntimeError("nvcc failed building libfpmimo_b200.so")
-        if verbose:
-            sys.stderr.write(r.stderr)
-        os.replace(OUT + ".tmp", OUT)
+    if not (force or needs_build()):
+        return OUT
+    os.makedirs(OBJ, exist_ok=True)
+    units = _units()
+    with cf.ThreadPoolExecutor(max_workers=min(len(units), os.cpu_count() or 4)) as ex:
+        results = list(ex.map(lambda s: _compile(s, verbose), units))
+    if verbose:
+        for _, log in results:
+            sys.stderr.write(log)
+    cmd = [NVCC, *ARCH, "-shared", "-o", OUT + ".tmp"] + [o for o, _ in results]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"link failed:\n{r.stdout}{r.stderr}")
+    os.replace(OUT + ".tmp", OUT)
     return OUT
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

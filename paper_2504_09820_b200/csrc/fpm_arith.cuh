@@ -55,7 +55,7 @@ __device__ __forceinline__ double pow2_scale(double v, int q) {
   return __dmul_rn(__dmul_rn(v, s1), s2);
 }
 
-__device__ __forceinline__ double gen_round(double x, const FmtP& f) {
+static __device__ __noinline__ double gen_round(double x, const FmtP& f) {
   if (f.native) return x;
   unsigned long long b = (unsigned long long)__double_as_longlong(x);
   unsigned long long a = b & 0x7FFFFFFFFFFFFFFFULL;
@@ -119,10 +119,24 @@ __device__ __forceinline__ double2 cdiv(double2 n, double2 d) {
 //   add(a, b)         _cadd
 //   wide(c)           exact binary64 value
 // ------------------------------------------------------------------------
+// half2 / bfloat162 lanes: .x = real (low 16 bits), .y = imag (high 16 bits)
+__device__ __forceinline__ unsigned h2u(__half2 h) { return *reinterpret_cast<unsigned*>(&h); }
+__device__ __forceinline__ __half2 u2h(unsigned u) { return *reinterpret_cast<__half2*>(&u); }
+__device__ __forceinline__ unsigned b2u(__nv_bfloat162 h) { return *reinterpret_cast<unsigned*>(&h); }
+__device__ __forceinline__ __nv_bfloat162 u2b(unsigned u) { return *reinterpret_cast<__nv_bfloat162*>(&u); }
+
 template <int K> struct Ar;
 
+// Extra per-format members used by the matvec / dot kernels:
+//   P, prep(v)   "prepared" right operand of a matvec product (see F16)
+//   mulp(a, p)   == mul(a, v) bit for bit
+//   asmc(c)      the reference's `re + 1j*im` assembly applied in-format
 template <> struct Ar<FK_F64> {
   typedef double2 C;
+  typedef double2 P;
+  static __device__ __forceinline__ P prep(C v) { return v; }
+  static __device__ __forceinline__ C mulp(C a, P v, const FmtP& f) { return mul(a, v, f); }
+  static __device__ __forceinline__ C asmc(C c) { return assemble(c.x, c.y); }
   static __device__ __forceinline__ C rnd(double2 v, const FmtP&) { return v; }
   static __device__ __forceinline__ C mul(C a, C b, const FmtP&) {
     return make_double2(__dsub_rn(__dmul_rn(a.x, b.x), __dmul_rn(a.y, b.y)),
@@ -139,6 +153,10 @@ template <> struct Ar<FK_F64> {
 
 template <> struct Ar<FK_GEN> {
   typedef double2 C;
+  typedef double2 P;
+  static __device__ __forceinline__ P prep(C v) { return v; }
+  static __device__ __forceinline__ C mulp(C a, P v, const FmtP& f) { return mul(a, v, f); }
+  static __device__ __forceinline__ C asmc(C c) { return assemble(c.x, c.y); }
   static __device__ __forceinline__ C rnd(double2 v, const FmtP& f) {
     return make_double2(gen_round(v.x, f), gen_round(v.y, f));
   }
@@ -158,6 +176,14 @@ template <> struct Ar<FK_GEN> {
 
 template <> struct Ar<FK_F32> {
   typedef float2 C;
+  typedef float2 P;
+  static __device__ __forceinline__ P prep(C v) { return v; }
+  static __device__ __forceinline__ C mulp(C a, P v, const FmtP& f) { return mul(a, v, f); }
+  static __device__ __forceinline__ C asmc(C c) {
+    // (re + (0*im - 0), 0 + (0 + im)) in binary32 (exact: same rules as binary64)
+    float t = __fsub_rn(__fmul_rn(0.0f, c.y), 0.0f);
+    return make_float2(__fadd_rn(c.x, t), __fadd_rn(0.0f, __fadd_rn(0.0f, c.y)));
+  }
   static __device__ __forceinline__ C rnd(double2 v, const FmtP&) {
     return make_float2(__double2float_rn(v.x), __double2float_rn(v.y));
   }
@@ -174,14 +200,31 @@ template <> struct Ar<FK_F32> {
   static __device__ __forceinline__ double2 wide(C c) { return make_double2((double)c.x, (double)c.y); }
 };
 
-// half2 / bfloat162 lanes: .x = real (low 16 bits), .y = imag (high 16 bits)
-__device__ __forceinline__ unsigned h2u(__half2 h) { return *reinterpret_cast<unsigned*>(&h); }
-__device__ __forceinline__ __half2 u2h(unsigned u) { return *reinterpret_cast<__half2*>(&u); }
-__device__ __forceinline__ unsigned b2u(__nv_bfloat162 h) { return *reinterpret_cast<unsigned*>(&h); }
-__device__ __forceinline__ __nv_bfloat162 u2b(unsigned u) { return *reinterpret_cast<__nv_bfloat162*>(&u); }
 
 template <> struct Ar<FK_F16> {
   typedef __half2 C;
+  // P = (v, rot(v)) with rot(v) = (-vi, vr): a*v = lo(a)*v + hi(a)*rot(v)
+  // lane-wise: (ar*vr + ai*(-vi), ar*vi + ai*vr); fl(x*(-y)) = -fl(x*y), so
+  // this equals _cmul's fl(fl(ar vr) - fl(ai vi)), fl(fl(ar vi) + fl(ai vr)).
+  struct P {
+    __half2 v1, v2;
+  };
+  static __device__ __forceinline__ P prep(C v) {
+    P p;
+    p.v1 = v;
+    p.v2 = u2h(h2u(__lowhigh2highlow(v)) ^ 0x00008000u);
+    return p;
+  }
+  static __device__ __forceinline__ C mulp(C a, P p, const FmtP&) {
+    return __hadd2_rn(__hmul2_rn(__low2half2(a), p.v1), __hmul2_rn(__high2half2(a), p.v2));
+  }
+  static __device__ __forceinline__ C asmc(C c) {
+    unsigned u = h2u(c), re = u & 0xFFFFu, im = u >> 16;
+    if ((im & 0x7C00u) == 0x7C00u) re = 0x7E00u;           // non-finite imag -> NaN real
+    else if (re == 0x8000u && !(im & 0x8000u)) re = 0u;    // -0 + (+0) = +0
+    if (im == 0x8000u) im = 0u;                            // 0 + -0 = +0
+    return u2h(re | (im << 16));
+  }
   static __device__ __forceinline__ C rnd(double2 v, const FmtP&) {
     // cvt.rn.f16.f64: a single rounding (never via fp32)
     return __halves2half2(__double2half(v.x), __double2half(v.y));
@@ -203,6 +246,25 @@ template <> struct Ar<FK_F16> {
 
 template <> struct Ar<FK_BF16> {
   typedef __nv_bfloat162 C;
+  struct P {
+    __nv_bfloat162 v1, v2;
+  };
+  static __device__ __forceinline__ P prep(C v) {
+    P p;
+    p.v1 = v;
+    p.v2 = u2b(b2u(__lowhigh2highlow(v)) ^ 0x00008000u);
+    return p;
+  }
+  static __device__ __forceinline__ C mulp(C a, P p, const FmtP&) {
+    return __hadd2_rn(__hmul2_rn(__low2bfloat162(a), p.v1), __hmul2_rn(__high2bfloat162(a), p.v2));
+  }
+  static __device__ __forceinline__ C asmc(C c) {
+    unsigned u = b2u(c), re = u & 0xFFFFu, im = u >> 16;
+    if ((im & 0x7F80u) == 0x7F80u) re = 0x7FC0u;
+    else if (re == 0x8000u && !(im & 0x8000u)) re = 0u;
+    if (im == 0x8000u) im = 0u;
+    return u2b(re | (im << 16));
+  }
   static __device__ __forceinline__ C rnd(double2 v, const FmtP&) {
     return __halves2bfloat162(__double2bfloat16(v.x), __double2bfloat16(v.y));  // cvt.rn.bf16.f64
   }
@@ -228,9 +290,9 @@ __device__ __forceinline__ double2 work_round_c(double2 q, const FmtP& w) {
   return assemble(gen_round(q.x, w), gen_round(q.y, w));
 }
 
-// _wdiv (solvers.py:256-259)
+// _wdiv (solvers.py:256-259); noinline: one shared copy (see fpm_cg.cuh)
 template <int WK>
-__device__ __forceinline__ double2 wdiv(double2 num, double2 den, const FmtP& w) {
+__device__ __noinline__ double2 wdiv(double2 num, double2 den, const FmtP& w) {
   return work_round_c<WK>(cdiv(num, den), w);
 }
 

@@ -16,45 +16,54 @@
 //   frozen lanes never resume (so per-lane early exit is exact).
 //
 // Sequential accumulation order is part of the contract (linalg.py:65-68,
-// 94-95).  Latency design: the product terms of every dot product are
-// formed in parallel by the row threads (each is an independent rounded
-// complex multiply), and only the left-to-right SUM runs as one dependent
-// chain in one thread per realization; matvec rows are chains in parallel.
-// Six CTA barriers per iteration.
+// 94-95).  Latency design: the product terms of every dot product are formed
+// in parallel by the row threads (each an independent rounded complex
+// multiply) and only the left-to-right SUM runs as one dependent chain in one
+// "owner" thread per realization; matvec rows are chains in parallel.  Six
+// CTA barriers per sweep.  The matvec and inner-product formats are the same
+// kind K (the host only builds native kernels for u_MV == u_IP; any other
+// pair runs the generic emulation kind, with separate runtime parameters).
+//
+// I-cache: each step runs once per sweep on a few warps, so latency is
+// dominated by instruction fetch unless the code is small and shared; the
+// heavy helpers are __noinline__ (one hot copy) and thread roles are
+// computed once.
 #pragma once
 #include "fpm_arith.cuh"
 
 namespace fpm {
 
-template <int MVK, int IPK>
+template <int K>
 struct CgSmem {
-  typedef typename Ar<MVK>::C MC;
-  typedef typename Ar<IPK>::C IC;
+  typedef typename Ar<K>::C C;
+  typedef typename Ar<K>::P P;
   int R, N, L, ldA;
-  MC* At;          // R * N * ldA, transposed: entry (i,k) at k*ldA + i
-  MC* pmv;         // R * N   p rounded to u_MV
-  IC *tphi, *trho, *tr1;  // R * N product terms of p^H w, r^H p, r^H z (or r^H r)
-  double2* minv;   // R * N*L block inverses (block kb at kb*L*L, row-major Lk x Lk), on the u_W grid
-  double2 *b, *x, *r, *p, *z, *w, *xn, *rn;  // R * N each
-  double2* sc;     // R * 8 : 0 alpha, 1 beta, 3 rho0, 4 carry
-  int* fl;         // R * 4 : live, nonfinite, breakdown_at, diverged_at
+  C* At;                  // R * N * ldA, transposed: entry (i,k) at k*ldA + i, on the u_MV grid
+  P* pmv;                 // R * N   p rounded to u_MV, prepared for the matvec
+  C *tphi, *trho, *tr1;   // R * N   product terms of p^H w, r^H p, r^H z (or r^H r), u_IP
+  C* rip;                 // R * N   r rounded to u_IP
+  double2* minv;          // R * N*L block inverses: block kb at kb*L*L, column-major Lk x Lk, u_W grid
+  double2 *b, *x, *r, *p, *z, *w, *xn, *rn;  // R * N each (u_W values, binary64 carriers)
+  double2* sc;            // R * 8 : 0 alpha, 1 beta, 3 rho0, 4 carry
+  int* fl;                // R * 4 : live, nonfinite, breakdown_at, diverged_at
 };
 
-// Owner of the sequential sums of slot g: past the matvec rows when possible,
-// one warp apart so the R chains run in parallel.
+// Owner of the sequential sums of slot g (which = 0: phi/rho1/carry,
+// 1: as_written rho0): past the matvec rows when possible, one warp apart.
 __device__ __forceinline__ int dot_owner(int g, int which, int rows, int nthreads) {
-  int k = g * 2 + which;
-  int cand = nthreads - 1 - 32 * k;
+  const int k = g * 2 + which;
+  const int cand = nthreads - 1 - 32 * k;
   if (cand >= rows && cand >= 0) return cand;
   return (nthreads - 1 - k) % nthreads;
 }
 
 // left-to-right sum t_0 + t_1 + ... (dot_fp's accumulation, linalg.py:94-95)
-template <int IPK>
-__device__ __forceinline__ double2 chain_sum(const typename Ar<IPK>::C* t, int n, const FmtP& f) {
-  typedef Ar<IPK> A;
+template <int K>
+__device__ __noinline__ double2 chain_sum(const typename Ar<K>::C* t, int n, const FmtP& f) {
+  typedef Ar<K> A;
   typename A::C s = t[0];
   int k = 1;
+#pragma unroll 1
   for (; k + 8 <= n; k += 8) {
     typename A::C v[8];
 #pragma unroll
@@ -62,73 +71,91 @@ __device__ __forceinline__ double2 chain_sum(const typename Ar<IPK>::C* t, int n
 #pragma unroll
     for (int j = 0; j < 8; ++j) s = A::add(s, v[j], f);
   }
+#pragma unroll 1
   for (; k < n; ++k) s = A::add(s, t[k], f);
-  double2 d = A::wide(s);
-  return assemble(d.x, d.y);
+  return A::wide(A::asmc(s));
 }
 
-// conj(u) * v term at the IP format (inputs rounded into it, dot_fp)
-template <int IPK>
-__device__ __forceinline__ typename Ar<IPK>::C ip_term(double2 u, double2 v, const FmtP& f) {
-  typedef Ar<IPK> A;
-  return A::mulc(A::rnd(u, f), A::rnd(v, f), f);
-}
-
-// one row of the block-diagonal apply M r (solvers.py:222-225) at u_W
-template <int WK>
-__device__ __forceinline__ double2 bj_row(const double2* minv, const double2* r, int j, int L, int N,
-                                          const FmtP& w) {
-  typedef Ar<WK> A;
-  const int kb = j / L, jl = j - kb * L;
-  const int s0 = kb * L;
-  const int Lk = min(L, N - s0);
-  const double2* M = minv + kb * L * L + jl * Lk;
-  double2 s = A::mul(M[0], A::rnd(r[s0], w), w);
-  for (int l = 1; l < Lk; ++l) s = A::add(s, A::mul(M[l], A::rnd(r[s0 + l], w), w), w);
-  return assemble(s.x, s.y);
-}
-
-// w_i = sum_k A(i,k) p_k at u_MV (matvec_fp), A column-major in shared memory
-template <int MVK>
-__device__ __forceinline__ double2 mv_row(const typename Ar<MVK>::C* col, const typename Ar<MVK>::C* pv, int N,
-                                          int ldA, const FmtP& f) {
-  typedef Ar<MVK> A;
-  typename A::C s = A::mul(col[0], pv[0], f);
+// w_i = sum_k A(i,k) p_k at u_MV (matvec_fp), A column-major in shared memory;
+// returned assembled (`sr + 1j*si`) in-format
+template <int K>
+__device__ __noinline__ typename Ar<K>::C mv_row(const typename Ar<K>::C* col, const typename Ar<K>::P* pv, int N,
+                                               int ldA, const FmtP& f) {
+  typedef Ar<K> A;
+  typename A::C s = A::mulp(col[0], pv[0], f);
   int k = 1;
+#pragma unroll 1
   for (; k + 8 <= N; k += 8) {
     typename A::C t[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) t[j] = A::mul(col[(long)(k + j) * ldA], pv[k + j], f);
+    for (int j = 0; j < 8; ++j) t[j] = A::mulp(col[(k + j) * ldA], pv[k + j], f);
 #pragma unroll
     for (int j = 0; j < 8; ++j) s = A::add(s, t[j], f);
   }
-  for (; k < N; ++k) s = A::add(s, A::mul(col[(long)k * ldA], pv[k], f), f);
-  double2 d = A::wide(s);
-  return assemble(d.x, d.y);
+#pragma unroll 1
+  for (; k < N; ++k) s = A::add(s, A::mulp(col[k * ldA], pv[k], f), f);
+  return A::asmc(s);
+}
+
+// one row of the block-diagonal apply M r (solvers.py:222-225) at u_W
+template <int WK, int LB>
+__device__ __noinline__ double2 bj_row(const double2* minv, const double2* r, int j, int L_rt, int N, const FmtP& w) {
+  typedef Ar<WK> A;
+  const int L = LB > 0 ? LB : L_rt;
+  const int kb = j / L, jl = j - kb * L;
+  const int s0 = kb * L;
+  const int Lk = LB > 0 ? LB : min(L, N - s0);
+  const double2* M = minv + kb * L * L + jl;  // column-major block
+  double2 s = A::mul(M[0], A::rnd(r[s0], w), w);
+#pragma unroll
+  for (int l = 1; l < Lk; ++l) s = A::add(s, A::mul(M[l * Lk], A::rnd(r[s0 + l], w), w), w);
+  return assemble(s.x, s.y);
 }
 
 // phase timestamps (diagnostic): thread 0 of CTA 0 writes clock64 values
-#define FPM_STAMP(tr, k)                                      \
-  do {                                                        \
-    if ((tr) && tid == 0) (tr)[(k)] = (long long)clock64();   \
+// (a volatile shared-memory read first forces the deferred-blocking barrier
+// to actually release before the clock is sampled)
+#define FPM_STAMP(tr, k)                                                      \
+  do {                                                                        \
+    if ((tr) && tid == 0) {                                                   \
+      __shared__ int _fpm_dummy;                                              \
+      int _v = *(volatile int*)&_fpm_dummy;                                   \
+      (tr)[(k)] = (long long)clock64() + (_v == 0x7fffffff ? 1 : 0);          \
+    }                                                                         \
   } while (0)
 
-template <int WK, int MVK, int IPK>
-__device__ void cg_team(CgSmem<MVK, IPK>& S, int Rv, int iters, bool bj, bool textbook, const Prec& pr,
-                        int nthreads, int tid, long long* tr = nullptr) {
-  typedef Ar<MVK> MV;
+template <int WK, int K, int LB>
+__device__ void cg_team(CgSmem<K>& S, int Rv, int iters, bool bj, bool textbook, const Prec& pr, int nthreads,
+                        int tid, long long* tr = nullptr) {
+  typedef Ar<K> A;
+  typedef typename A::C C;
   const int N = S.N;
   const int RN = Rv * N;
   const FmtP& fw = pr.work;
   const FmtP& fm = pr.mv;
   const FmtP& fi = pr.ip;
   const bool rho_fresh = bj && !textbook;  // as_written: rho0 = r^H p every sweep
+  // roles, once
+  const int nrow = RN > tid ? (RN - tid + nthreads - 1) / nthreads : 0;
+  int og = -1, ow = 0;
+#pragma unroll 1
+  for (int g = 0; g < Rv; ++g) {
+    if (dot_owner(g, 0, RN, nthreads) == tid) og = g, ow = 0;
+    if (dot_owner(g, 1, RN, nthreads) == tid) og = g, ow = 1;
+  }
+  // u_IP value of a binary64 (work) value / of a value already on the u_MV grid
+  // (native kinds: u_IP == u_MV, so the matvec's rounding of p is reused)
+  auto ipr = [&](double2 v) -> C { return A::rnd(v, fi); };
+  auto mv_to_ip = [&](C v) -> C { return K == FK_GEN ? A::rnd(A::wide(v), fi) : v; };
 
   // ---- init (solvers.py:297-328) ----
-  for (int q = tid; q < RN; q += nthreads) {
+#pragma unroll 1
+  for (int k = 0; k < nrow; ++k) {
+    const int q = tid + k * nthreads;
     S.x[q] = make_double2(0.0, 0.0);
     S.r[q] = S.b[q];
   }
+#pragma unroll 1
   for (int g = tid; g < Rv; g += nthreads) {
     S.fl[g * 4 + 1] = 0;
     S.fl[g * 4 + 2] = -1;
@@ -136,42 +163,45 @@ __device__ void cg_team(CgSmem<MVK, IPK>& S, int Rv, int iters, bool bj, bool te
     // fl[g*4+0] (live) is set by the caller (0 if setup failed)
   }
   __syncthreads();
-  for (int q = tid; q < RN; q += nthreads) {
+#pragma unroll 1
+  for (int k = 0; k < nrow; ++k) {
+    const int q = tid + k * nthreads;
     const int g = q / N, i = q - g * N;
     const double2 rv = S.r[q];
-    const double2 pv = bj ? bj_row<WK>(S.minv + (long)g * N * S.L, S.r + g * N, i, S.L, N, fw) : rv;
+    const double2 pv = bj ? bj_row<WK, LB>(S.minv + g * N * S.L, S.r + g * N, i, S.L, N, fw) : rv;
     S.p[q] = pv;
-    S.pmv[q] = MV::rnd(pv, fm);
-    S.tr1[q] = ip_term<IPK>(rv, (bj && textbook) ? pv : rv, fi);  // carry terms
-    if (rho_fresh) S.trho[q] = ip_term<IPK>(rv, pv, fi);
+    const C pm = A::rnd(pv, fm);
+    S.pmv[q] = A::prep(pm);
+    const C ri = ipr(rv);
+    S.rip[q] = ri;
+    const C pi = K == FK_GEN ? ipr(pv) : pm;
+    S.tr1[q] = A::mulc(ri, (bj && textbook) ? pi : ri, fi);  // carry terms
+    if (rho_fresh) S.trho[q] = A::mulc(ri, pi, fi);
   }
   __syncthreads();
-  if (!rho_fresh) {
-    for (int g = 0; g < Rv; ++g)
-      if (tid == dot_owner(g, 0, RN, nthreads)) S.sc[g * 8 + 4] = chain_sum<IPK>(S.tr1 + g * N, N, fi);
-  }
+  if (!rho_fresh && og >= 0 && ow == 0) S.sc[og * 8 + 4] = chain_sum<K>(S.tr1 + og * N, N, fi);
   __syncthreads();
 
+#pragma unroll 1
   for (int it = 1; it <= iters; ++it) {
     // ---- A: w = A p (u_MV) + phi terms;  rho0 = sum r^H p (BJ as_written) ----
-    for (int q = tid; q < RN; q += nthreads) {
+#pragma unroll 1
+    for (int k = 0; k < nrow; ++k) {
+      const int q = tid + k * nthreads;
       const int g = q / N, i = q - g * N;
       if (!S.fl[g * 4]) continue;
-      const double2 wv = mv_row<MVK>(S.At + (long)g * N * S.ldA + i, S.pmv + g * N, N, S.ldA, fm);
-      S.w[q] = wv;
-      S.tphi[q] = ip_term<IPK>(S.p[q], wv, fi);
+      const C wc = mv_row<K>(S.At + g * N * S.ldA + i, S.pmv + g * N, N, S.ldA, fm);
+      S.w[q] = A::wide(wc);
+      const C pi = K == FK_GEN ? ipr(S.p[q]) : A::rnd(S.p[q], fm);
+      S.tphi[q] = A::mulc(pi, mv_to_ip(wc), fi);
     }
-    if (rho_fresh) {
-      for (int g = 0; g < Rv; ++g)
-        if (tid == dot_owner(g, 1, RN, nthreads) && S.fl[g * 4])
-          S.sc[g * 8 + 3] = chain_sum<IPK>(S.trho + g * N, N, fi);
-    }
+    if (rho_fresh && og >= 0 && ow == 1 && S.fl[og * 4]) S.sc[og * 8 + 3] = chain_sum<K>(S.trho + og * N, N, fi);
     __syncthreads();
     if (it == 1) FPM_STAMP(tr, 0);
     // ---- B: phi, flags, alpha ----
-    for (int g = 0; g < Rv; ++g) {
-      if (tid != dot_owner(g, 0, RN, nthreads) || !S.fl[g * 4]) continue;
-      const double2 phi = chain_sum<IPK>(S.tphi + g * N, N, fi);
+    if (og >= 0 && ow == 0 && S.fl[og * 4]) {
+      const int g = og;
+      const double2 phi = chain_sum<K>(S.tphi + g * N, N, fi);
       const double2 rho0 = rho_fresh ? S.sc[g * 8 + 3] : S.sc[g * 8 + 4];
       S.sc[g * 8 + 3] = rho0;
       const bool stall = (rho0.x == 0.0) && (rho0.y == 0.0);
@@ -182,7 +212,9 @@ __device__ void cg_team(CgSmem<MVK, IPK>& S, int Rv, int iters, bool bj, bool te
     __syncthreads();
     if (it == 1) FPM_STAMP(tr, 1);
     // ---- C: x, r updates (u_W) + finiteness ----
-    for (int q = tid; q < RN; q += nthreads) {
+#pragma unroll 1
+    for (int k = 0; k < nrow; ++k) {
+      const int q = tid + k * nthreads;
       const int g = q / N;
       if (!S.fl[g * 4]) continue;
       const double2 al = S.sc[g * 8 + 0];
@@ -195,46 +227,53 @@ __device__ void cg_team(CgSmem<MVK, IPK>& S, int Rv, int iters, bool bj, bool te
     __syncthreads();
     if (it == 1) FPM_STAMP(tr, 2);
     // ---- D: commit; z = M r_new; rho1 terms ----
-    for (int q = tid; q < RN; q += nthreads) {
+#pragma unroll 1
+    for (int k = 0; k < nrow; ++k) {
+      const int q = tid + k * nthreads;
       const int g = q / N, i = q - g * N;
       if (!S.fl[g * 4] || S.fl[g * 4 + 1]) continue;
       const double2 rn = S.rn[q];
       S.x[q] = S.xn[q];
       S.r[q] = rn;
+      const C ri = ipr(rn);
+      S.rip[q] = ri;
       if (bj) {
-        const double2 zv = bj_row<WK>(S.minv + (long)g * N * S.L, S.rn + g * N, i, S.L, N, fw);
+        const double2 zv = bj_row<WK, LB>(S.minv + g * N * S.L, S.rn + g * N, i, S.L, N, fw);
         S.z[q] = zv;
-        S.tr1[q] = ip_term<IPK>(rn, zv, fi);
+        S.tr1[q] = A::mulc(ri, ipr(zv), fi);
       } else {
-        S.tr1[q] = ip_term<IPK>(rn, rn, fi);
+        S.tr1[q] = A::mulc(ri, ri, fi);
       }
     }
     __syncthreads();
     if (it == 1) FPM_STAMP(tr, 3);
     // ---- E: rho1, beta, divergence flag ----
-    for (int g = 0; g < Rv; ++g) {
-      if (tid != dot_owner(g, 0, RN, nthreads) || !S.fl[g * 4]) continue;
+    if (og >= 0 && ow == 0 && S.fl[og * 4]) {
+      const int g = og;
       if (S.fl[g * 4 + 1]) {  // non-finite update: diverged, frozen at the last finite iterate
         S.fl[g * 4 + 3] = it;
         S.fl[g * 4] = 0;
-        continue;
+      } else {
+        const double2 rho1 = chain_sum<K>(S.tr1 + g * N, N, fi);
+        S.sc[g * 8 + 1] = wdiv<WK>(rho1, S.sc[g * 8 + 3], fw);
+        S.sc[g * 8 + 4] = rho1;
       }
-      const double2 rho1 = chain_sum<IPK>(S.tr1 + g * N, N, fi);
-      S.sc[g * 8 + 1] = wdiv<WK>(rho1, S.sc[g * 8 + 3], fw);
-      S.sc[g * 8 + 4] = rho1;
     }
     __syncthreads();
     if (it == 1) FPM_STAMP(tr, 4);
     // ---- F: p = (z|r) + beta p ; pmv = rnd(p) ; next rho0 terms ----
     int any = 0;
-    for (int q = tid; q < RN; q += nthreads) {
+#pragma unroll 1
+    for (int k = 0; k < nrow; ++k) {
+      const int q = tid + k * nthreads;
       const int g = q / N;
       if (!S.fl[g * 4]) continue;
       any = 1;
       const double2 pn = axpy1<WK>(S.sc[g * 8 + 1], S.p[q], bj ? S.z[q] : S.r[q], fw);
       S.p[q] = pn;
-      S.pmv[q] = MV::rnd(pn, fm);
-      if (rho_fresh) S.trho[q] = ip_term<IPK>(S.r[q], pn, fi);
+      const C pm = A::rnd(pn, fm);
+      S.pmv[q] = A::prep(pm);
+      if (rho_fresh) S.trho[q] = A::mulc(S.rip[q], K == FK_GEN ? ipr(pn) : pm, fi);
     }
     const int more = __syncthreads_or(any);
     if (it == 1) FPM_STAMP(tr, 5);

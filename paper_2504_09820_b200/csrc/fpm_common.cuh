@@ -1,0 +1,71 @@
+// Host/device shared argument blocks and the per-kind launcher interface.
+// Each format kind's kernels live in their own translation unit
+// (fpm_inst_<kind>.cu, compiled in parallel); fpm_host.cu plans and dispatches.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "fpm_arith.cuh"
+#include "fpm_gram.cuh"
+
+namespace fpm {
+
+struct Slicer {
+  double th[7];
+  int nth;  // 3 (16-QAM) or 7 (64-QAM)
+  int bpa;  // bits per axis
+};
+
+struct DetectArgs {
+  const double2* H;
+  const double2* y;
+  const uint8_t* tx;
+  long T;
+  double sigma2;
+  int L, iters, bj, textbook;
+  Prec pr;
+  const double2* minv_in;
+  double2* x;
+  int* brk;
+  int* div;
+  uint8_t* rx;
+  unsigned long long* counters;
+  Slicer sl;
+  GramGeom G;
+  int ldA;
+  // dynamic shared memory offsets (bytes)
+  int off_ys, off_union, off_minv, off_scr, off_scr2, off_vec, off_pmv, off_tip, off_sc, off_fl;
+  int smem_bytes;
+  long long* trace;  // nullable: phase clock stamps of CTA 0 (diagnostic)
+};
+
+struct CgArgs {
+  const double2* A;
+  const double2* b;
+  const double2* minv;
+  long T;
+  int N, L, iters, bj, textbook, R, ldA;
+  Prec pr;
+  double2* x;
+  int* brk;
+  int* div;
+  int off_minv, off_vec, off_pmv, off_tip, off_sc, off_fl;
+};
+
+// Launchers (return FPM_* codes).  nb / lb: compile-time specialisation
+// requested by the planner (0 = generic); a launcher falls back to its generic
+// instance when it has no matching specialisation.
+#define FPM_DECLARE_KIND(name)                                                                 \
+  int launch_detect_##name(const DetectArgs& a, int threads, int nb, int lb, cudaStream_t st); \
+  int launch_cg_##name(const CgArgs& a, int smem, int lb, cudaStream_t st);
+FPM_DECLARE_KIND(f64)
+FPM_DECLARE_KIND(f32)
+FPM_DECLARE_KIND(f16)
+FPM_DECLARE_KIND(bf16)
+FPM_DECLARE_KIND(gen)    // W = fp64, MV/IP generic emulation
+FPM_DECLARE_KIND(gen_w)  // everything generic (W != fp64)
+#undef FPM_DECLARE_KIND
+
+void count_launch();
+
+}  // namespace fpm

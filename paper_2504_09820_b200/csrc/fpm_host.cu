@@ -1,10 +1,6 @@
-// Kernels and C ABI of libfpmimo_b200.so (see include/fpmimo_b200.h).
-//
-//   fpm_detect_kernel  fused Gram/MF -> BJ setup -> (BJ-)CG -> slicer/counter
-//   fpm_gram_kernel    Gram/MF to global A, b
-//   fpm_bj_kernel      block-Jacobi Hermitian inverses from global A
-//   fpm_cg_kernel      (BJ-)CG from global A, b, Minv
-//   fpm_slice_kernel   slicer + error counters
+// Host side of libfpmimo_b200.so (C ABI: include/fpmimo_b200.h): planning,
+// dispatch to the per-kind kernel units (fpm_inst_<kind>.cu), the standalone
+// Gram / block-Jacobi / slicer kernels, the host-buffer pipeline.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -15,10 +11,7 @@
 #include <cstring>
 
 #include "../../include/fpmimo_b200.h"
-#include "fpm_arith.cuh"
-#include "fpm_cg.cuh"
-#include "fpm_gram.cuh"
-#include "fpm_ptx.cuh"
+#include "fpm_detect.cuh"
 
 namespace fpm {
 
@@ -29,284 +22,7 @@ constexpr int kMaxN = 128;
 constexpr int kMaxL = 16;
 constexpr int kMaxM = 4096;
 
-struct Slicer {
-  double th[7];
-  int nth;  // 3 (16-QAM) or 7 (64-QAM)
-  int bpa;  // bits per axis
-};
-
-// ---------------------------------------------------------------------------
-// Hermitian-PD block inverse via Cholesky (fp64).  The reference inverts with
-// LAPACK zgesv (solvers.py:250-251) after a Cholesky PD check
-// (solvers.py:246-249) and symmetrizes (solvers.py:252); the bits of a
-// LAPACK inverse are not portable, so parity for this piece is a tolerance
-// (or Minv is injected).  B: Lk x Lk row-major (full Hermitian) -> inverse,
-// in place; C: scratch Lk x Lk.
-// ---------------------------------------------------------------------------
-__device__ bool hpd_inverse(double2* B, double2* C, int Lk) {
-  for (int j = 0; j < Lk; ++j) {
-    double d = B[j * Lk + j].x;
-    for (int k = 0; k < j; ++k) {
-      double2 c = C[j * Lk + k];
-      d = d - (c.x * c.x + c.y * c.y);
-    }
-    if (!(d > 0.0)) return false;
-    double cjj = sqrt(d);
-    C[j * Lk + j] = make_double2(cjj, 0.0);
-    for (int i = j + 1; i < Lk; ++i) {
-      double2 s = B[i * Lk + j];
-      for (int k = 0; k < j; ++k) {
-        double2 a = C[i * Lk + k], b = C[j * Lk + k];  // s -= a * conj(b)
-        s.x -= a.x * b.x + a.y * b.y;
-        s.y -= a.y * b.x - a.x * b.y;
-      }
-      C[i * Lk + j] = make_double2(s.x / cjj, s.y / cjj);
-    }
-  }
-  // Linv (lower) into B
-  for (int i = 0; i < Lk; ++i) {
-    const double cii = C[i * Lk + i].x;
-    for (int j = 0; j < i; ++j) {
-      double2 s = make_double2(0.0, 0.0);
-      for (int k = j; k < i; ++k) {
-        double2 a = C[i * Lk + k], b = B[k * Lk + j];
-        s.x += a.x * b.x - a.y * b.y;
-        s.y += a.x * b.y + a.y * b.x;
-      }
-      B[i * Lk + j] = make_double2(-s.x / cii, -s.y / cii);
-    }
-    B[i * Lk + i] = make_double2(1.0 / cii, 0.0);
-  }
-  // Minv = Linv^H Linv (upper incl. diagonal) into C
-  for (int i = 0; i < Lk; ++i)
-    for (int j = i; j < Lk; ++j) {
-      double2 s = make_double2(0.0, 0.0);
-      for (int k = j; k < Lk; ++k) {
-        double2 a = B[k * Lk + i], b = B[k * Lk + j];  // conj(a) * b
-        s.x += a.x * b.x + a.y * b.y;
-        s.y += a.x * b.y - a.y * b.x;
-      }
-      C[i * Lk + j] = s;
-    }
-  for (int i = 0; i < Lk; ++i)
-    for (int j = i; j < Lk; ++j) {
-      double2 v = C[i * Lk + j];
-      if (i == j) {
-        B[i * Lk + i] = make_double2(v.x, 0.0);
-      } else {
-        B[i * Lk + j] = v;
-        B[j * Lk + i] = make_double2(v.x, -v.y);
-      }
-    }
-  return true;
-}
-
-// Level index = #thresholds strictly below v (digitize right=True; NaN -> 0,
-// detect.py:70-75), then the per-axis Gray label (detect.py:50).
-__device__ __forceinline__ int level_index(double v, const Slicer& sl) {
-  int idx = 0;
-#pragma unroll
-  for (int k = 0; k < 7; ++k)
-    if (k < sl.nth && v > sl.th[k]) ++idx;
-  return idx;
-}
-
-// Slices x[q] and compares with tx; returns (bit errors) and sets *sym_err.
-__device__ __forceinline__ int slice_one(double2 x, const uint8_t* tx, uint8_t* rx, const Slicer& sl,
-                                         int* sym_err) {
-  int gi = level_index(x.x, sl), gq = level_index(x.y, sl);
-  gi ^= gi >> 1;
-  gq ^= gq >> 1;
-  int errs = 0;
-  for (int k = 0; k < sl.bpa; ++k) {
-    uint8_t bi = (uint8_t)((gi >> (sl.bpa - 1 - k)) & 1);
-    uint8_t bq = (uint8_t)((gq >> (sl.bpa - 1 - k)) & 1);
-    if (rx) {
-      rx[k] = bi;
-      rx[sl.bpa + k] = bq;
-    }
-    if (tx) errs += (tx[k] != bi) + (tx[sl.bpa + k] != bq);
-  }
-  *sym_err = errs > 0;
-  return errs;
-}
-
-__device__ __forceinline__ void block_add_counters(unsigned long long* cnt_smem, unsigned long long* cnt_g,
-                                                   int tid, int nthreads) {
-  __syncthreads();
-  if (tid < FPM_NCOUNTERS && cnt_smem[tid]) atomicAdd(&cnt_g[tid], cnt_smem[tid]);
-}
-
-// ---------------------------------------------------------------------------
-// Fused detector
-// ---------------------------------------------------------------------------
-struct DetectArgs {
-  const double2* H;
-  const double2* y;
-  const uint8_t* tx;
-  long T;
-  double sigma2;
-  int L, iters, bj, textbook;
-  Prec pr;
-  const double2* minv_in;
-  double2* x;
-  int* brk;
-  int* div;
-  uint8_t* rx;
-  unsigned long long* counters;
-  Slicer sl;
-  GramGeom G;
-  int ldA;
-  // dynamic shared memory offsets (bytes)
-  int off_ys, off_union, off_minv, off_scr, off_vec, off_pmv, off_tip, off_sc, off_fl;
-  int smem_bytes;
-  long long* trace;  // nullable: [0] start [1] gram done [2] bj done [3..9] cg phases it=1 [10] cg done [11] end
-};
-
-template <int WK, int MVK, int IPK>
-struct EmitSmem {
-  CgSmem<MVK, IPK>* S;
-  const FmtP* fm;
-  int bj;
-  __device__ __forceinline__ void a(int g, int i, int j, double2 v) {
-    const int N = S->N;
-    S->At[(long)g * N * S->ldA + (long)j * S->ldA + i] = Ar<MVK>::rnd(v, *fm);
-    if (bj) {
-      const int L = S->L;
-      const int kb = i / L;
-      if (kb == j / L) {
-        const int Lk = min(L, N - kb * L);
-        S->minv[(long)g * N * L + kb * L * L + (i - kb * L) * Lk + (j - kb * L)] = v;
-      }
-    }
-  }
-  __device__ __forceinline__ void b(int g, int n, double2 v) { S->b[g * S->N + n] = v; }
-};
-
-template <int WK, int MVK, int IPK>
-__global__ void __launch_bounds__(512, 1) fpm_detect_kernel(const DetectArgs args) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  typedef typename Ar<MVK>::C MC;
-  const int tid = threadIdx.x, nthreads = blockDim.x;
-  const GramGeom& G = args.G;
-  const long t0 = (long)blockIdx.x * G.R;
-  const int Rv = (int)min((long)G.R, args.T - t0);
-  const int N = G.N;
-
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem);  // S full, S empty, 1 y
-  __shared__ unsigned long long cnt[FPM_NCOUNTERS];
-  typedef typename Ar<IPK>::C IC;
-  CgSmem<MVK, IPK> S;
-  S.R = G.R;
-  S.N = N;
-  S.L = args.bj ? args.L : 1;
-  S.ldA = args.ldA;
-  S.At = reinterpret_cast<MC*>(smem + args.off_union);
-  S.minv = reinterpret_cast<double2*>(smem + args.off_minv);
-  double2* vec = reinterpret_cast<double2*>(smem + args.off_vec);
-  const long RN = (long)G.R * N;
-  S.b = vec;
-  S.x = vec + RN;
-  S.r = vec + 2 * RN;
-  S.p = vec + 3 * RN;
-  S.z = vec + 4 * RN;
-  S.w = vec + 5 * RN;
-  S.xn = vec + 6 * RN;
-  S.rn = vec + 7 * RN;
-  S.pmv = reinterpret_cast<MC*>(smem + args.off_pmv);
-  S.tphi = reinterpret_cast<IC*>(smem + args.off_tip);
-  S.trho = S.tphi + RN;
-  S.tr1 = S.trho + RN;
-  S.sc = reinterpret_cast<double2*>(smem + args.off_sc);
-  S.fl = reinterpret_cast<int*>(smem + args.off_fl);
-
-  if (tid == 0) {
-    for (int s = 0; s < G.S; ++s) {
-      mbar_init(&bars[s], 1);
-      mbar_init(&bars[G.S + s], nthreads / 32);
-    }
-    mbar_init(&bars[2 * G.S], 1);
-    fence_mbar_init();
-  }
-  if (tid < FPM_NCOUNTERS) cnt[tid] = 0ULL;
-  for (int g = tid; g < G.R; g += nthreads) S.fl[g * 4] = g < Rv ? 1 : 0;
-  long long* tr = (args.trace && blockIdx.x == 0) ? args.trace : nullptr;
-  FPM_STAMP(tr, 0);
-  __syncthreads();
-
-  // 1) Gram + matched filter straight into shared memory
-  EmitSmem<WK, MVK, IPK> em;
-  em.S = &S;
-  em.fm = &args.pr.mv;
-  em.bj = args.bj && !args.minv_in;
-  gram_run(args.H, args.y, t0, Rv, G, args.sigma2, reinterpret_cast<double2*>(smem + args.off_union),
-           reinterpret_cast<double2*>(smem + args.off_ys), bars, nthreads, tid, em);
-  FPM_STAMP(tr, 1);
-
-  // 2) block-Jacobi inverses (on-chip fp64 Cholesky, or injected)
-  if (args.bj) {
-    const int L = args.L;
-    const int nblk = (N + L - 1) / L;
-    if (args.minv_in) {
-      for (long q = tid; q < (long)Rv * N * L; q += nthreads) {
-        const int g = (int)(q / ((long)N * L));
-        const long e = q - (long)g * N * L;
-        S.minv[q] = Ar<WK>::rnd(args.minv_in[(t0 + g) * (long)N * L + e], args.pr.work);
-      }
-    } else {
-      double2* scr = reinterpret_cast<double2*>(smem + args.off_scr);
-      for (int q = tid; q < Rv * nblk; q += nthreads) {
-        const int g = q / nblk, kb = q - g * nblk;
-        const int Lk = min(L, N - kb * L);
-        double2* B = S.minv + (long)g * N * L + kb * L * L;
-        if (!hpd_inverse(B, scr + (long)g * N * L + kb * L * L, Lk)) {
-          atomicExch(&S.fl[g * 4], 0);
-          atomicAdd(&cnt[FPM_CNT_NONPD], 1ULL);
-        } else if (WK != FK_F64) {
-          for (int e = 0; e < Lk * Lk; ++e) B[e] = Ar<WK>::rnd(B[e], args.pr.work);
-        }
-      }
-    }
-    __syncthreads();
-  }
-
-  FPM_STAMP(tr, 2);
-  // 3) CG in shared memory
-  cg_team<WK, MVK, IPK>(S, Rv, args.iters, args.bj != 0, args.textbook != 0, args.pr, nthreads, tid,
-                        tr ? tr + 3 : nullptr);
-
-  // 4) slicer + counters + write-back
-  const int bps = 2 * args.sl.bpa;
-  unsigned long long be = 0, se = 0;
-  for (int q = tid; q < Rv * N; q += nthreads) {
-    const int g = q / N, n = q - g * N;
-    const long gq = (t0 + g) * (long)N + n;
-    const double2 xv = S.x[q];
-    args.x[gq] = xv;
-    int sym;
-    be += slice_one(xv, args.tx ? args.tx + gq * bps : nullptr, args.rx ? args.rx + gq * bps : nullptr,
-                    args.sl, &sym);
-    se += sym;
-  }
-  for (int off = 16; off; off >>= 1) {
-    be += __shfl_xor_sync(0xffffffffu, be, off);
-    se += __shfl_xor_sync(0xffffffffu, se, off);
-  }
-  if ((tid & 31) == 0) {
-    if (be) atomicAdd(&cnt[FPM_CNT_BIT_ERRORS], be);
-    if (se) atomicAdd(&cnt[FPM_CNT_SYMBOL_ERRORS], se);
-  }
-  for (int g = tid; g < Rv; g += nthreads) {
-    const int bk = S.fl[g * 4 + 2], dv = S.fl[g * 4 + 3];
-    args.brk[t0 + g] = bk;
-    args.div[t0 + g] = dv;
-    if (dv >= 0) atomicAdd(&cnt[FPM_CNT_DIVERGED], 1ULL);
-    if (bk >= 0) atomicAdd(&cnt[FPM_CNT_BREAKDOWN], 1ULL);
-  }
-  if (tid == 0) atomicAdd(&cnt[FPM_CNT_TRIALS], (unsigned long long)Rv);
-  block_add_counters(cnt, args.counters, tid, nthreads);
-  FPM_STAMP(tr, 11);
-}
+void count_launch() { g_launches++; }
 
 // ---------------------------------------------------------------------------
 // Standalone Gram
@@ -316,10 +32,21 @@ struct EmitGlobal {
   double2* bout;
   long t0;
   int N;
-  __device__ __forceinline__ void a(int g, int i, int j, double2 v) {
-    Aout[((t0 + g) * (long)N + i) * N + j] = v;
+  double sigma2;
+  __device__ __forceinline__ void job(const GramJob& jb, const double2 (&acc)[16], int nb) {
+    double2* A = Aout + (t0 + jb.g) * (long)N * N;
+    const int n = N;
+    gram_entries(
+        jb, acc, nb, N, sigma2,
+        [&](int i, int j, double2 vij, double2 vji) {
+          A[i * n + j] = vij;
+          A[j * n + i] = vji;
+        },
+        [&](int i, double2 vii) { A[i * n + i] = vii; });
   }
-  __device__ __forceinline__ void b(int g, int n, double2 v) { bout[(t0 + g) * (long)N + n] = v; }
+  __device__ __forceinline__ void b(int g, int n, int part, double v) {
+    reinterpret_cast<double*>(bout + (t0 + g) * (long)N + n)[part] = v;
+  }
 };
 
 struct GramArgs {
@@ -354,8 +81,9 @@ __global__ void __launch_bounds__(512, 1) fpm_gram_kernel(const GramArgs args) {
   em.bout = args.b;
   em.t0 = t0;
   em.N = G.N;
-  gram_run(args.H, args.y, t0, Rv, G, args.sigma2, reinterpret_cast<double2*>(smem + args.off_union),
-           reinterpret_cast<double2*>(smem + args.off_ys), bars, nthreads, tid, em);
+  em.sigma2 = args.sigma2;
+  gram_run<0>(args.H, args.y, t0, Rv, G, reinterpret_cast<double2*>(smem + args.off_union),
+              reinterpret_cast<double2*>(smem + args.off_ys), bars, nthreads, tid, em);
 }
 
 // ---------------------------------------------------------------------------
@@ -366,17 +94,20 @@ __global__ void fpm_bj_kernel(const double2* __restrict__ A, long T, int N, int 
   extern __shared__ __align__(128) unsigned char smem[];
   const int nblk = (N + L - 1) / L;
   const long q = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  double2* B = reinterpret_cast<double2*>(smem) + (long)threadIdx.x * 2 * L * L;
-  double2* C = B + L * L;
+  const int nt = blockDim.x;
+  double2* B = reinterpret_cast<double2*>(smem) + threadIdx.x;  // interleaved across threads
+  double2* C = B + (long)nt * L * L;
+  double2* O = reinterpret_cast<double2*>(smem) + (long)2 * nt * L * L + (long)threadIdx.x * L * L;
   if (q >= T * nblk) return;
   const long t = q / nblk;
   const int kb = (int)(q - t * nblk);
   const int s0 = kb * L, Lk = min(L, N - s0);
   for (int i = 0; i < Lk; ++i)
-    for (int j = 0; j < Lk; ++j) B[i * Lk + j] = A[(t * N + s0 + i) * (long)N + s0 + j];
-  bool ok = hpd_inverse(B, C, Lk);
+    for (int j = 0; j < Lk; ++j) B[(i * Lk + j) * nt] = A[(t * N + s0 + i) * (long)N + s0 + j];
+  bool ok = hpd_inverse<0>(B, nt, C, nt, O, Lk);
   double2* out = Minv + t * (long)N * L + (long)kb * L * L;
-  for (int e = 0; e < Lk * Lk; ++e) out[e] = B[e];
+  for (int i = 0; i < Lk; ++i)
+    for (int j = 0; j < Lk; ++j) out[i * Lk + j] = O[j * Lk + i];  // row-major in global
   if (!ok) {
     atomicAdd(nonpd, 1u);
     if (bad_block) atomicMin(&bad_block[t], s0);
@@ -386,77 +117,6 @@ __global__ void fpm_bj_kernel(const double2* __restrict__ A, long T, int N, int 
 __global__ void fpm_bad_fix_kernel(int* bad_block, long T) {
   const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
   if (t < T && bad_block[t] == 0x7f7f7f7f) bad_block[t] = -1;
-}
-
-// ---------------------------------------------------------------------------
-// Standalone CG from global A / b / Minv
-// ---------------------------------------------------------------------------
-struct CgArgs {
-  const double2* A;
-  const double2* b;
-  const double2* minv;
-  long T;
-  int N, L, iters, bj, textbook, R, ldA;
-  Prec pr;
-  double2* x;
-  int* brk;
-  int* div;
-  int off_minv, off_vec, off_pmv, off_tip, off_sc, off_fl;
-};
-
-template <int WK, int MVK, int IPK>
-__global__ void __launch_bounds__(256) fpm_cg_kernel(const CgArgs args) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  typedef typename Ar<MVK>::C MC;
-  typedef typename Ar<IPK>::C IC;
-  const int tid = threadIdx.x, nthreads = blockDim.x;
-  const long t0 = (long)blockIdx.x * args.R;
-  const int Rv = (int)min((long)args.R, args.T - t0);
-  const int N = args.N;
-  CgSmem<MVK, IPK> S;
-  S.R = args.R;
-  S.N = N;
-  S.L = args.bj ? args.L : 1;
-  S.ldA = args.ldA;
-  S.At = reinterpret_cast<MC*>(smem);
-  S.minv = reinterpret_cast<double2*>(smem + args.off_minv);
-  double2* vec = reinterpret_cast<double2*>(smem + args.off_vec);
-  const long RN = (long)args.R * N;
-  S.b = vec;
-  S.x = vec + RN;
-  S.r = vec + 2 * RN;
-  S.p = vec + 3 * RN;
-  S.z = vec + 4 * RN;
-  S.w = vec + 5 * RN;
-  S.xn = vec + 6 * RN;
-  S.rn = vec + 7 * RN;
-  S.pmv = reinterpret_cast<MC*>(smem + args.off_pmv);
-  S.tphi = reinterpret_cast<IC*>(smem + args.off_tip);
-  S.trho = S.tphi + RN;
-  S.tr1 = S.trho + RN;
-  S.sc = reinterpret_cast<double2*>(smem + args.off_sc);
-  S.fl = reinterpret_cast<int*>(smem + args.off_fl);
-
-  // A (row-major, global) -> At (transposed, u_MV), coalesced along k
-  const long NN = (long)N * N;
-  for (long q = tid; q < (long)Rv * NN; q += nthreads) {
-    const int g = (int)(q / NN);
-    const long e = q - g * NN;
-    const int i = (int)(e / N), k = (int)(e - (long)i * N);
-    S.At[(long)g * N * S.ldA + (long)k * S.ldA + i] = Ar<MVK>::rnd(args.A[(t0 + g) * NN + e], args.pr.mv);
-  }
-  for (long q = tid; q < (long)Rv * N; q += nthreads) S.b[q] = args.b[t0 * N + q];
-  if (args.bj)
-    for (long q = tid; q < (long)Rv * N * args.L; q += nthreads)
-      S.minv[q] = Ar<WK>::rnd(args.minv[t0 * (long)N * args.L + q], args.pr.work);
-  for (int g = tid; g < args.R; g += nthreads) S.fl[g * 4] = g < Rv ? 1 : 0;
-  __syncthreads();
-  cg_team<WK, MVK, IPK>(S, Rv, args.iters, args.bj != 0, args.textbook != 0, args.pr, nthreads, tid);
-  for (long q = tid; q < (long)Rv * N; q += nthreads) args.x[t0 * N + q] = S.x[q];
-  for (int g = tid; g < Rv; g += nthreads) {
-    args.brk[t0 + g] = S.fl[g * 4 + 2];
-    args.div[t0 + g] = S.fl[g * 4 + 3];
-  }
 }
 
 // ---------------------------------------------------------------------------
@@ -579,6 +239,15 @@ static Slicer make_slicer(int qam) {
   return s;
 }
 
+static int p_bytes(int kind) {  // prepared matvec operand (Ar<K>::P)
+  switch (kind) {
+    case FK_F32:
+    case FK_F16:
+    case FK_BF16: return 8;
+    default: return 16;
+  }
+}
+
 static int mv_bytes(int kind) {
   switch (kind) {
     case FK_F32: return 8;
@@ -604,15 +273,20 @@ static int max_smem_optin() {
 }
 
 // Gram geometry for a given R: fills G and the union/ys sizes.
-static void gram_geom(int R, int M, int N, GramGeom& G) {
+static int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return (v && *v) ? std::atoi(v) : dflt;
+}
+
+static void gram_geom(int R, int M, int N, GramGeom& G, int stage_kb = 24) {
   G.R = R;
   G.M = M;
   G.N = N;
   G.Np = (N + 7) / 8 * 8;
   G.nb = G.Np / 4;
-  G.S = 3;
+  G.S = env_int("FPM_STAGES", 3);
   const long row_bytes = (long)R * G.Np * 16;
-  int mc = (int)std::max(1L, (long)(24 * 1024) / row_bytes);
+  int mc = (int)std::max(1L, (long)(stage_kb * 1024) / row_bytes);
   G.MC = std::min(mc, M);
 }
 
@@ -624,11 +298,13 @@ static int gram_threads(const GramGeom& G) {
 // Plan the fused kernel for (M, N, L, kinds); returns false if it cannot fit.
 static bool plan_detect(int M, int N, int L, int bj, int mvk, int ipk, DetectArgs& a, int& threads) {
   const int Np = (N + 7) / 8 * 8;
-  int R = std::max(1, 256 / Np);
-  const int limit = max_smem_optin();
+  // R realization slots per CTA; FPM_R / FPM_CTAS_PER_SM / FPM_STAGE_KB are tuning overrides
+  int R = env_int("FPM_R", std::max(1, 256 / Np));
+  const int per_sm = env_int("FPM_CTAS_PER_SM", 1);
+  const int limit = max_smem_optin() / per_sm - (per_sm > 1 ? 1024 : 0);
   for (; R >= 1; R = (R > 1 ? R / 2 : 0)) {
     GramGeom G;
-    gram_geom(R, M, N, G);
+    gram_geom(R, M, N, G, env_int("FPM_STAGE_KB", 24));
     threads = gram_threads(G);
     if (threads > 512) continue;
     const int ldA = N + 1;
@@ -644,17 +320,19 @@ static bool plan_detect(int M, int N, int L, int bj, int mvk, int ipk, DetectArg
     off = align_up(off + (bj ? (size_t)R * N * Lb * 16 : 0), 128);
     a.off_scr = (int)off;
     off = align_up(off + (bj ? (size_t)R * N * Lb * 16 : 0), 128);
+    a.off_scr2 = (int)off;
+    off = align_up(off + (bj ? (size_t)R * N * Lb * 16 : 0), 128);
     a.off_vec = (int)off;
     off = align_up(off + (size_t)8 * R * N * 16, 128);
     a.off_pmv = (int)off;
-    off = align_up(off + (size_t)R * N * mv_bytes(mvk), 128);
+    off = align_up(off + (size_t)R * N * p_bytes(mvk), 128);
     a.off_tip = (int)off;
-    off = align_up(off + (size_t)3 * R * N * mv_bytes(ipk), 128);
+    off = align_up(off + (size_t)4 * R * N * mv_bytes(ipk), 128);
     a.off_sc = (int)off;
     off = align_up(off + (size_t)R * 8 * 16, 128);
     a.off_fl = (int)off;
     off = align_up(off + (size_t)R * 4 * 4, 128);
-    if ((long)off + 1024 <= limit) {
+    if ((long)off + 1024 <= limit || (R == 1 && (long)off + 1024 <= max_smem_optin())) {
       a.G = G;
       a.ldA = ldA;
       a.smem_bytes = (int)off;
@@ -677,9 +355,9 @@ static bool plan_cg(int N, int L, int bj, int mvk, int ipk, CgArgs& a, int& smem
     a.off_vec = (int)off;
     off = align_up(off + (size_t)8 * R * N * 16, 128);
     a.off_pmv = (int)off;
-    off = align_up(off + (size_t)R * N * mv_bytes(mvk), 128);
+    off = align_up(off + (size_t)R * N * p_bytes(mvk), 128);
     a.off_tip = (int)off;
-    off = align_up(off + (size_t)3 * R * N * mv_bytes(ipk), 128);
+    off = align_up(off + (size_t)4 * R * N * mv_bytes(ipk), 128);
     a.off_sc = (int)off;
     off = align_up(off + (size_t)R * 8 * 16, 128);
     a.off_fl = (int)off;
@@ -695,47 +373,38 @@ static bool plan_cg(int N, int L, int bj, int mvk, int ipk, CgArgs& a, int& smem
   return false;
 }
 
-template <int WK, int MVK, int IPK>
-static int launch_detect_t(const DetectArgs& a, int threads, cudaStream_t st) {
-  auto k = fpm_detect_kernel<WK, MVK, IPK>;
-  if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, a.smem_bytes) != cudaSuccess)
-    return FPM_ECUDA;
-  const long grid = (a.T + a.G.R - 1) / a.G.R;
-  k<<<(unsigned)grid, threads, a.smem_bytes, st>>>(a);
-  g_launches++;
-  return cudaGetLastError() == cudaSuccess ? FPM_OK : FPM_ECUDA;
+// Specialisations the per-kind units provide (nb = N/4, lb = L): see
+// fpm_inst_<kind>.cu.  Anything else runs the kind's generic instance.
+static void pick_spec(int N, int L, int bj, int& nb, int& lb) {
+  nb = (N % 8 == 0) ? N / 4 : 0;
+  lb = bj ? L : 0;
+  if (bj && nb && (nb % L)) nb = 0;
 }
 
 static int launch_detect(const Kinds& k, const DetectArgs& a, int threads, cudaStream_t st) {
-  if (k.w == FK_GEN) return launch_detect_t<FK_GEN, FK_GEN, FK_GEN>(a, threads, st);
+  int nb, lb;
+  pick_spec(a.G.N, a.L, a.bj, nb, lb);
+  if (a.G.N != a.G.Np) nb = 0;
+  if (std::getenv("FPM_NO_SPEC")) nb = lb = 0;
+  if (k.w == FK_GEN) return launch_detect_gen_w(a, threads, 0, 0, st);
   switch (k.mv) {
-    case FK_F64: return launch_detect_t<FK_F64, FK_F64, FK_F64>(a, threads, st);
-    case FK_F32: return launch_detect_t<FK_F64, FK_F32, FK_F32>(a, threads, st);
-    case FK_F16: return launch_detect_t<FK_F64, FK_F16, FK_F16>(a, threads, st);
-    case FK_BF16: return launch_detect_t<FK_F64, FK_BF16, FK_BF16>(a, threads, st);
-    default: return launch_detect_t<FK_F64, FK_GEN, FK_GEN>(a, threads, st);
+    case FK_F64: return launch_detect_f64(a, threads, nb, lb, st);
+    case FK_F32: return launch_detect_f32(a, threads, nb, lb, st);
+    case FK_F16: return launch_detect_f16(a, threads, nb, lb, st);
+    case FK_BF16: return launch_detect_bf16(a, threads, nb, lb, st);
+    default: return launch_detect_gen(a, threads, 0, 0, st);
   }
 }
 
-template <int WK, int MVK, int IPK>
-static int launch_cg_t(const CgArgs& a, int smem, cudaStream_t st) {
-  auto k = fpm_cg_kernel<WK, MVK, IPK>;
-  if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
-    return FPM_ECUDA;
-  const long grid = (a.T + a.R - 1) / a.R;
-  k<<<(unsigned)grid, 256, smem, st>>>(a);
-  g_launches++;
-  return cudaGetLastError() == cudaSuccess ? FPM_OK : FPM_ECUDA;
-}
-
 static int launch_cg(const Kinds& k, const CgArgs& a, int smem, cudaStream_t st) {
-  if (k.w == FK_GEN) return launch_cg_t<FK_GEN, FK_GEN, FK_GEN>(a, smem, st);
+  const int lb = (a.bj && a.N % a.L == 0 && !std::getenv("FPM_NO_SPEC")) ? a.L : 0;
+  if (k.w == FK_GEN) return launch_cg_gen_w(a, smem, 0, st);
   switch (k.mv) {
-    case FK_F64: return launch_cg_t<FK_F64, FK_F64, FK_F64>(a, smem, st);
-    case FK_F32: return launch_cg_t<FK_F64, FK_F32, FK_F32>(a, smem, st);
-    case FK_F16: return launch_cg_t<FK_F64, FK_F16, FK_F16>(a, smem, st);
-    case FK_BF16: return launch_cg_t<FK_F64, FK_BF16, FK_BF16>(a, smem, st);
-    default: return launch_cg_t<FK_F64, FK_GEN, FK_GEN>(a, smem, st);
+    case FK_F64: return launch_cg_f64(a, smem, lb, st);
+    case FK_F32: return launch_cg_f32(a, smem, lb, st);
+    case FK_F16: return launch_cg_f16(a, smem, lb, st);
+    case FK_BF16: return launch_cg_bf16(a, smem, lb, st);
+    default: return launch_cg_gen(a, smem, 0, st);
   }
 }
 
@@ -856,7 +525,7 @@ int fpm_bj_setup(const double* A, int64_t T, int32_t N, int32_t L, int32_t allow
     cudaMemsetAsync(bad_block, 0x7f, sizeof(int32_t) * T, st);
   }
   const int nblk = (N + L - 1) / L;
-  const int per = 2 * L * L * 16;
+  const int per = 3 * L * L * 16;
   int tpb = std::max(1, std::min(128, (48 * 1024) / per));
   const long work = T * nblk;
   const long grid = (work + tpb - 1) / tpb;

@@ -1,0 +1,11 @@
+// fp64 work, bfloat16 matvec / inner products.  Specialisation: c2-p7 (N=32, plain).
+#include "fpm_detect.cuh"
+namespace fpm {
+int launch_detect_bf16(const DetectArgs& a, int threads, int nb, int lb, cudaStream_t st) {
+  if (nb == 8 && lb == 0) return launch_detect_t<FK_F64, FK_BF16, 8, 0>(a, threads, st);
+  return launch_detect_t<FK_F64, FK_BF16, 0, 0>(a, threads, st);
+}
+int launch_cg_bf16(const CgArgs& a, int smem, int lb, cudaStream_t st) {
+  return launch_cg_t<FK_F64, FK_BF16, 0>(a, smem, st);
+}
+}  // namespace fpm

@@ -97,22 +97,28 @@ def main():
         out["cg"] = {"ms": ms, "det_s": T / ms * 1e3, "hbm_gbs": byts * T / (ms / 1e3) / 1e9,
                      "hbm_frac": byts * T / (ms / 1e3) / 6554.9e9}
     if a.trace:
-        tr = torch.zeros(16, dtype=torch.int64, device=dev)
+        tr = torch.zeros(64, dtype=torch.int64, device=dev)
         lib.fpm_debug_set_trace(tr.data_ptr())
         fused()
         torch.cuda.synchronize()
         lib.fpm_debug_set_trace(None)
         t = tr.cpu().tolist()
-        names = ["start", "gram", "bj", "A:matvec", "B:phi/alpha", "C:axpy", "D:commit/z", "E:rho1/beta",
-                 "F:p", "cg_rest(it>=2)", "-", "slice+writeback"]
+        names = {1: "gram", 2: "bj", 3: "A:init+matvec", 4: "B:phi/alpha", 5: "C:axpy", 6: "D:commit/z",
+                 7: "E:rho1/beta", 8: "F:p", 9: "cg_rest(it>=2)", 10: "cg_tail", 15: "slice+writeback"}
         prev = t[0]
         out["trace_cycles"] = {}
-        for i, nm in enumerate(names):
-            if i == 0 or nm == "-" or t[i] == 0:
+        for i in sorted(names):
+            if t[i] == 0:
                 continue
-            out["trace_cycles"][nm] = t[i] - prev
+            out["trace_cycles"][names[i]] = t[i] - prev
             prev = t[i]
-        out["trace_cycles"]["total"] = t[11] - t[0]
+        out["trace_cycles"]["total"] = t[15] - t[0]
+        out["trace_cycles"]["gram.mainloop"] = t[16] - t[0]
+        out["trace_cycles"]["gram.epilogue"] = t[1] - t[16]
+        out["trace_cycles"]["gram.producer_empty_wait"] = t[16 + 5]
+        out["trace_cycles"]["gram.w0_full_wait"] = t[16 + 6]
+        out["trace_cycles"]["gram.w1_full_wait"] = t[16 + 7]
+        out["trace_cycles"]["gram.warp_finish"] = [t[16 + 8 + w] - t[0] for w in range(16)]
     if a.only in ("", "detect"):
         ms = timeit(fused, a.reps)
         out["detect"] = {"ms": ms, "det_s": T / ms * 1e3, "fp64_frac": fg * T / (ms / 1e3) / pk.value}
