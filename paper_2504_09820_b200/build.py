@@ -24,7 +24,8 @@ OUT = os.path.join(HERE, "libfpmimo_b200.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "fpmimo_b200.h")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ARCH + ["-O3", "-lineinfo", "-fmad=false", "-std=c++17", "-Xcompiler", "-fPIC"]
+FLAGS = ARCH + ["-O3", "-lineinfo", "-fmad=false", "-std=c++17", "-Xcompiler", "-fPIC"] + \
+    os.environ.get("FPM_NVCC_EXTRA", "").split()
 
 
 def _units():

@@ -20,7 +20,7 @@
 // in parallel by the row threads (each an independent rounded complex
 // multiply) and only the left-to-right SUM runs as one dependent chain in one
 // "owner" thread per realization; matvec rows are chains in parallel.  Six
-// CTA barriers per sweep.  The matvec and inner-product formats are the same
+// group barriers per sweep.  The matvec and inner-product formats are the same
 // kind K (the host only builds native kernels for u_MV == u_IP; any other
 // pair runs the generic emulation kind, with separate runtime parameters).
 //
@@ -124,9 +124,39 @@ __device__ __noinline__ double2 bj_row(const double2* minv, const double2* r, in
     }                                                                         \
   } while (0)
 
-template <int WK, int K, int LB>
-__device__ void cg_team(CgSmem<K>& S, int Rv, int iters, bool bj, bool textbook, const Prec& pr, int nthreads,
-                        int tid, long long* tr = nullptr) {
+
+// Group barriers: the whole CTA, or a named hardware barrier over `count`
+// threads (warp-specialised kernel; ids 1..15, count a multiple of 32).
+struct CtaBar {
+  __device__ __forceinline__ void sync() { __syncthreads(); }
+  __device__ __forceinline__ int any(int v) { return __syncthreads_or(v); }
+};
+struct NamedBar {
+  int id, count;
+  __device__ __forceinline__ void sync() { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory"); }
+  __device__ __forceinline__ int any(int v) {
+    int out;
+    asm volatile(
+        "{\n\t.reg .pred p, q;\n\t"
+        "setp.ne.s32 p, %1, 0;\n\t"
+        "bar.red.or.pred q, %2, %3, p;\n\t"
+        "selp.s32 %0, 1, 0, q;\n}"
+        : "=r"(out)
+        : "r"(v), "r"(id), "r"(count)
+        : "memory");
+    return out;
+  }
+};
+
+// Group-level CG: the nthreads threads of one synchronisation group (the
+// whole CTA, or a named-barrier warp group in the warp-specialised kernel)
+// advance all Rv resident realizations in lockstep.  Rows are spread over
+// the group; each realization's sequential sums run in an "owner" thread,
+// placed past the row threads when the group has spare lanes.  bar.sync()
+// is the group barrier, bar.any(v) a barrier that ORs v over the group.
+template <int WK, int K, int LB, class Bar>
+__device__ void cg_group(CgSmem<K>& S, int Rv, int iters, bool bj, bool textbook, const Prec& pr, int nthreads,
+                         int tid, Bar& bar, long long* tr = nullptr) {
   typedef Ar<K> A;
   typedef typename A::C C;
   const int N = S.N;
@@ -162,7 +192,7 @@ __device__ void cg_team(CgSmem<K>& S, int Rv, int iters, bool bj, bool textbook,
     S.fl[g * 4 + 3] = -1;
     // fl[g*4+0] (live) is set by the caller (0 if setup failed)
   }
-  __syncthreads();
+  bar.sync();
 #pragma unroll 1
   for (int k = 0; k < nrow; ++k) {
     const int q = tid + k * nthreads;
@@ -178,9 +208,9 @@ __device__ void cg_team(CgSmem<K>& S, int Rv, int iters, bool bj, bool textbook,
     S.tr1[q] = A::mulc(ri, (bj && textbook) ? pi : ri, fi);  // carry terms
     if (rho_fresh) S.trho[q] = A::mulc(ri, pi, fi);
   }
-  __syncthreads();
+  bar.sync();
   if (!rho_fresh && og >= 0 && ow == 0) S.sc[og * 8 + 4] = chain_sum<K>(S.tr1 + og * N, N, fi);
-  __syncthreads();
+  bar.sync();
 
 #pragma unroll 1
   for (int it = 1; it <= iters; ++it) {
@@ -196,8 +226,7 @@ __device__ void cg_team(CgSmem<K>& S, int Rv, int iters, bool bj, bool textbook,
       S.tphi[q] = A::mulc(pi, mv_to_ip(wc), fi);
     }
     if (rho_fresh && og >= 0 && ow == 1 && S.fl[og * 4]) S.sc[og * 8 + 3] = chain_sum<K>(S.trho + og * N, N, fi);
-    __syncthreads();
-    if (it == 1) FPM_STAMP(tr, 0);
+    bar.sync();
     // ---- B: phi, flags, alpha ----
     if (og >= 0 && ow == 0 && S.fl[og * 4]) {
       const int g = og;
@@ -209,8 +238,7 @@ __device__ void cg_team(CgSmem<K>& S, int Rv, int iters, bool bj, bool textbook,
       if (stall || phi.x <= 0.0) S.fl[g * 4] = 0;
       S.sc[g * 8 + 0] = wdiv<WK>(rho0, phi, fw);
     }
-    __syncthreads();
-    if (it == 1) FPM_STAMP(tr, 1);
+    bar.sync();
     // ---- C: x, r updates (u_W) + finiteness ----
 #pragma unroll 1
     for (int k = 0; k < nrow; ++k) {
@@ -224,8 +252,7 @@ __device__ void cg_team(CgSmem<K>& S, int Rv, int iters, bool bj, bool textbook,
       S.rn[q] = rn;
       if (!(finite2(xn) && finite2(rn))) S.fl[g * 4 + 1] = 1;
     }
-    __syncthreads();
-    if (it == 1) FPM_STAMP(tr, 2);
+    bar.sync();
     // ---- D: commit; z = M r_new; rho1 terms ----
 #pragma unroll 1
     for (int k = 0; k < nrow; ++k) {
@@ -245,8 +272,7 @@ __device__ void cg_team(CgSmem<K>& S, int Rv, int iters, bool bj, bool textbook,
         S.tr1[q] = A::mulc(ri, ri, fi);
       }
     }
-    __syncthreads();
-    if (it == 1) FPM_STAMP(tr, 3);
+    bar.sync();
     // ---- E: rho1, beta, divergence flag ----
     if (og >= 0 && ow == 0 && S.fl[og * 4]) {
       const int g = og;
@@ -259,8 +285,7 @@ __device__ void cg_team(CgSmem<K>& S, int Rv, int iters, bool bj, bool textbook,
         S.sc[g * 8 + 4] = rho1;
       }
     }
-    __syncthreads();
-    if (it == 1) FPM_STAMP(tr, 4);
+    bar.sync();
     // ---- F: p = (z|r) + beta p ; pmv = rnd(p) ; next rho0 terms ----
     int any = 0;
 #pragma unroll 1
@@ -275,12 +300,10 @@ __device__ void cg_team(CgSmem<K>& S, int Rv, int iters, bool bj, bool textbook,
       S.pmv[q] = A::prep(pm);
       if (rho_fresh) S.trho[q] = A::mulc(S.rip[q], K == FK_GEN ? ipr(pn) : pm, fi);
     }
-    const int more = __syncthreads_or(any);
-    if (it == 1) FPM_STAMP(tr, 5);
+    const int more = bar.any(any);
     if (!more) break;
   }
-  __syncthreads();
-  FPM_STAMP(tr, 6);
+  bar.sync();
 }
 
 }  // namespace fpm

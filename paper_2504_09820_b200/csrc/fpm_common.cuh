@@ -23,6 +23,7 @@ struct DetectArgs {
   long T;
   double sigma2;
   int L, iters, bj, textbook;
+  int tl;  // CG team lanes per realization
   Prec pr;
   const double2* minv_in;
   double2* x;
@@ -37,7 +38,12 @@ struct DetectArgs {
   int off_ys, off_union, off_minv, off_scr, off_scr2, off_vec, off_pmv, off_tip, off_sc, off_fl;
   int smem_bytes;
   long long* trace;  // nullable: phase clock stamps of CTA 0 (diagnostic)
+  // warp-specialised persistent kernel: Gram / CG thread counts, slots base
+  int ws_gt, ws_ct, off_slot, off_bsm;
+  int debug;  // diagnostic bits (FPM_DEBUG): 1 = WS kernel skips the CG side
 };
+
+struct WsLayout;  // fpm_detect_ws.cuh
 
 struct CgArgs {
   const double2* A;
@@ -45,6 +51,7 @@ struct CgArgs {
   const double2* minv;
   long T;
   int N, L, iters, bj, textbook, R, ldA;
+  int tl;  // CG team lanes per realization
   Prec pr;
   double2* x;
   int* brk;
@@ -57,6 +64,8 @@ struct CgArgs {
 // instance when it has no matching specialisation.
 #define FPM_DECLARE_KIND(name)                                                                 \
   int launch_detect_##name(const DetectArgs& a, int threads, int nb, int lb, cudaStream_t st); \
+  int launch_detect_ws_##name(const DetectArgs& a, const WsLayout& sl, int grid, int nb, int lb, \
+                              cudaStream_t st);                                                \
   int launch_cg_##name(const CgArgs& a, int smem, int lb, cudaStream_t st);
 FPM_DECLARE_KIND(f64)
 FPM_DECLARE_KIND(f32)

@@ -207,8 +207,11 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_kernel(const DetectArgs arg
   FPM_STAMP(tr, 2);
 
   // 3) CG in shared memory
-  cg_team<WK, K, LB>(S, Rv, args.iters, args.bj != 0, args.textbook != 0, args.pr, nthreads, tid,
-                     tr ? tr + 3 : nullptr);
+  {
+    CtaBar bar;
+    cg_group<WK, K, LB>(S, Rv, args.iters, args.bj != 0, args.textbook != 0, args.pr, nthreads, tid, bar,
+                        tr ? tr + 3 : nullptr);
+  }
   FPM_STAMP(tr, 10);
 
   // 4) slicer + counters + write-back
@@ -308,7 +311,10 @@ __global__ void __launch_bounds__(256) fpm_cg_kernel(const CgArgs args) {
 #pragma unroll 1
   for (int g = tid; g < args.R; g += nthreads) S.fl[g * 4] = g < Rv ? 1 : 0;
   __syncthreads();
-  cg_team<WK, K, LB>(S, Rv, args.iters, args.bj != 0, args.textbook != 0, args.pr, nthreads, tid);
+  {
+    CtaBar bar;
+    cg_group<WK, K, LB>(S, Rv, args.iters, args.bj != 0, args.textbook != 0, args.pr, nthreads, tid, bar);
+  }
 #pragma unroll 1
   for (int q = tid; q < Rv * N; q += nthreads) args.x[t0 * N + q] = S.x[q];
 #pragma unroll 1

@@ -1,0 +1,413 @@
+// Warp-specialised persistent detector kernel (the fast path).
+//
+//   threads [0, gt)        "Gram" warps: accumulate the bit-exact Gram/MF of
+//                          realization group j+1 from the TMA ring ...
+//   threads [gt, gt+32)    producer warp: keeps the H / y TMA ring full
+//   threads [gt+32, ...)   ... while the "CG" warps solve group j: block
+//                          inverses, (BJ-)CG, slicing, counters, write-back.
+//
+// The hand-off is a double-buffered shared-memory slot (A at u_MV, b, fp64
+// diagonal blocks) guarded by two mbarrier pairs (slot full / slot empty), so
+// the latency-bound CG of one group never stalls the FP64 pipe: the Gram
+// warps only wait for a slot when the CG side is more than one group behind.
+// The H ring runs continuously across groups (the producer prefetches the
+// next group's first chunks and its y vector while the current group ends).
+// Each CTA owns groups blockIdx.x, blockIdx.x + gridDim.x, ...  Named
+// hardware barriers: 1 = Gram group, 2 = CG group.
+#pragma once
+#include "fpm_detect.cuh"
+
+namespace fpm {
+
+struct WsLayout {  // byte offsets inside one hand-off slot
+  int at, b, d, bytes;
+};
+
+template <int WK, int K, int NB, int LB>
+__global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const DetectArgs args, const WsLayout sl) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  typedef typename Ar<K>::C C;
+  typedef typename Ar<K>::P P;
+  const int tid = threadIdx.x;
+  const GramGeom& G = args.G;
+  const int R = G.R;
+  const int N = NB > 0 ? 4 * NB : G.N;
+  const int Np = NB > 0 ? 4 * NB : G.Np;
+  const int nb = NB > 0 ? NB : G.nb;
+  const int gt = args.ws_gt, ct = args.ws_ct;
+  const long ngroups = (args.T + R - 1) / R;
+  const int my_groups = blockIdx.x < ngroups ? (int)((ngroups - blockIdx.x + gridDim.x - 1) / gridDim.x) : 0;
+  const int nch = (G.M + G.MC - 1) / G.MC;
+  const int L = args.bj ? (LB > 0 ? LB : args.L) : 1;
+  const int nblk = args.bj ? (N + L - 1) / L : 1;
+  const int ldA = NB > 0 ? N + 1 : args.ldA;
+
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty = full + G.S;
+  uint64_t* ybar = full + 2 * G.S;   // [2]
+  uint64_t* sfull = ybar + 2;        // [2]
+  uint64_t* sempty = sfull + 2;      // [2]
+  double2* stages = reinterpret_cast<double2*>(smem + args.off_union);
+  double2* ysb = reinterpret_cast<double2*>(smem + args.off_ys);  // [2][R*M]
+  unsigned char* slots = smem + args.off_slot;
+  __shared__ unsigned long long cnt[FPM_NCOUNTERS];
+  // diagnostic timeline of CTA 0, groups 0..7: [j*8 + 0] gram loop start,
+  // 1 gram loop end, 2 slot acquired, 3 hand-off done, 4 cg start, 5 cg end
+  long long* tr = (args.trace && blockIdx.x == 0) ? args.trace : nullptr;
+
+  if (tid == 0) {
+    for (int s = 0; s < G.S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], gt / 32);
+    }
+    for (int k = 0; k < 2; ++k) {
+      mbar_init(&ybar[k], 1);
+      mbar_init(&sfull[k], 1);
+      mbar_init(&sempty[k], 1);
+    }
+    fence_mbar_init();
+  }
+  if (tid < FPM_NCOUNTERS) cnt[tid] = 0ULL;
+  __syncthreads();
+
+  const int stage_elems = R * G.MC * Np;
+  const long total = (long)my_groups * nch;
+  if (tid >= gt && tid < gt + 32) {
+    // ========================= producer warp ==========================
+    if (tid == gt) {
+      // issue global chunk gc (group gc/nch, local chunk gc%nch) into its stage
+      auto issue = [&](long gc) {
+        const int jj = (int)(gc / nch), c = (int)(gc - (long)jj * nch);
+        const long t0 = ((long)blockIdx.x + (long)jj * gridDim.x) * R;
+        const int Rv = (int)min((long)R, args.T - t0);
+        if (c == 0) {  // this group's y rides with its first chunk
+          double2* yd = ysb + (jj & 1) * R * G.M;
+          mbar_expect_tx(&ybar[jj & 1], (uint32_t)Rv * (uint32_t)G.M * 16u);
+          for (int g = 0; g < Rv; ++g)
+            bulk_g2s(yd + g * G.M, args.y + (t0 + g) * (long)G.M, G.M * 16u, &ybar[jj & 1]);
+        }
+        const int s = (int)(gc % G.S);
+        gram_issue(args.H, t0, Rv, G, c, stages + s * stage_elems, &full[s]);
+      };
+      fence_proxy_async();
+#pragma unroll 1
+      for (long gc = 0; gc < total; ++gc) {
+        if (gc >= G.S) mbar_wait(&empty[gc % G.S], (uint32_t)(((gc - G.S) / G.S) & 1));
+        if (gc >= 2 * nch && gc % nch == 0) {
+          // the y buffer of group jj was last read by group jj-2: wait until
+          // that group's Gram is done (its hand-off has been published)
+          const int jj = (int)(gc / nch);
+          mbar_wait(&sfull[jj & 1], (uint32_t)(((jj - 2) >> 1) & 1));
+        }
+        issue(gc);
+      }
+    }
+  } else if (tid < gt) {
+    // =========================== Gram warps ===========================
+    NamedBar gbar{1, gt};
+    const GramJob job = gram_job(tid, R, nb);
+    const int joff = job.g * G.MC * Np;
+    // matched-filter chain accumulators live in shared memory between chunks
+    // (one binary64 per chain), so no chain state occupies registers across
+    // the tile loop
+    double* bsm = reinterpret_cast<double*>(smem + args.off_bsm);
+    // N = 64: 2*R*N chains == gt threads, so each thread carries exactly one
+    // chain inside the tile loop (latency hidden by the tile math)
+    constexpr bool kChainInLoop = (NB == 16);
+    const int cq_g = tid / (2 * N), cq_e = tid - cq_g * 2 * N;
+    const int cq_part = cq_e / N, cq_n = cq_e - cq_part * N;
+    const int cq_hoff = cq_g * G.MC * Np + cq_n, cq_yoff = cq_g * G.M;
+
+#pragma unroll 1
+    for (int j = 0; j < my_groups; ++j) {
+      const long t0 = ((long)blockIdx.x + (long)j * gridDim.x) * R;
+      const int Rv = (int)min((long)R, args.T - t0);
+      const int slot = j & 1;
+      const bool active = job.g >= 0 && job.g < Rv;
+      const int nchain = 2 * Rv * N;
+      const bool chain_ok = kChainInLoop && tid < nchain;
+      double ca = 0.0;
+      double2 acc[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) acc[k] = make_double2(0.0, 0.0);
+      if (!kChainInLoop) {
+#pragma unroll 1
+        for (int q = tid; q < nchain; q += gt) bsm[q] = 0.0;
+      }
+      const double2* ys = ysb + slot * R * G.M;
+      mbar_wait(&ybar[slot], (uint32_t)((j >> 1) & 1));
+      if (tr && tid == 0 && j < 8) tr[j * 8 + 0] = clock64();
+
+#pragma unroll 1
+      for (int c = 0; c < nch; ++c) {
+        const long gc = (long)j * nch + c;
+        const int s = (int)(gc % G.S);
+        mbar_wait(&full[s], (uint32_t)((gc / G.S) & 1));
+        const double2* sb = stages + s * stage_elems;
+        const int m0 = c * G.MC;
+        const int rows = min(G.MC, G.M - m0);
+        const double2* pa = sb + joff + job.a;
+        const double2* pc = sb + joff + job.c;
+        if (active && !job.half) {
+FPM_ROW_UNROLL
+          for (int mm = 0; mm < rows; ++mm) {
+            double2 hi[4], hj[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) hi[u] = pa[mm * Np + nb * u];
+#pragma unroll
+            for (int v = 0; v < 4; ++v) hj[v] = pc[mm * Np + nb * v];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+              for (int v = 0; v < 4; ++v) cmac_conj(acc[u * 4 + v], hi[u], hj[v]);
+            if (chain_ok) {
+              const double2 h = sb[cq_hoff + mm * Np];
+              const double2 yv = ys[cq_yoff + m0 + mm];
+              const double y1 = cq_part ? yv.y : yv.x, y2 = cq_part ? -yv.x : yv.y;
+              ca = __dadd_rn(ca, __dadd_rn(__dmul_rn(h.x, y1), __dmul_rn(h.y, y2)));
+            }
+          }
+        } else if (active) {
+          const double2* py = sb + joff + job.y + nb * job.yo;
+FPM_ROW_UNROLL
+          for (int mm = 0; mm < rows; ++mm) {
+            {
+              double2 hx[4];
+#pragma unroll
+              for (int u = 0; u < 4; ++u) hx[u] = pa[mm * Np + nb * u];
+              int p = 0;
+#pragma unroll
+              for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int v = u + 1; v < 4; ++v) cmac_conj(acc[p++], hx[u], hx[v]);
+              acc[14].x = __dadd_rn(acc[14].x, sqmag(hx[0]));
+              acc[14].y = __dadd_rn(acc[14].y, sqmag(hx[1]));
+              acc[15].x = __dadd_rn(acc[15].x, sqmag(hx[2]));
+              acc[15].y = __dadd_rn(acc[15].y, sqmag(hx[3]));
+            }
+            double2 hy[2], hz[4];
+#pragma unroll
+            for (int w = 0; w < 2; ++w) hy[w] = py[mm * Np + nb * w];
+#pragma unroll
+            for (int v = 0; v < 4; ++v) hz[v] = pc[mm * Np + nb * v];
+#pragma unroll
+            for (int w = 0; w < 2; ++w)
+#pragma unroll
+              for (int v = 0; v < 4; ++v) cmac_conj(acc[6 + w * 4 + v], hy[w], hz[v]);
+            if (chain_ok) {
+              const double2 h = sb[cq_hoff + mm * Np];
+              const double2 yv = ys[cq_yoff + m0 + mm];
+              const double y1 = cq_part ? yv.y : yv.x, y2 = cq_part ? -yv.x : yv.y;
+              ca = __dadd_rn(ca, __dadd_rn(__dmul_rn(h.x, y1), __dmul_rn(h.y, y2)));
+            }
+          }
+        } else if (chain_ok) {  // idle job slot (partial group) that still owns a chain
+#pragma unroll 1
+          for (int mm = 0; mm < rows; ++mm) {
+            const double2 h = sb[cq_hoff + mm * Np];
+            const double2 yv = ys[cq_yoff + m0 + mm];
+            const double y1 = cq_part ? yv.y : yv.x, y2 = cq_part ? -yv.x : yv.y;
+            ca = __dadd_rn(ca, __dadd_rn(__dmul_rn(h.x, y1), __dmul_rn(h.y, y2)));
+          }
+        }
+        // matched-filter chains (split re / im, exact): chain q -> slot g,
+        // entry n, part (0 re / 1 im); accumulators round-trip through smem
+        if (!kChainInLoop && !(args.debug & 2)) {
+#pragma unroll 1
+          for (int q = tid; q < nchain; q += gt) {
+            const int g = q / (2 * N), e = q - g * 2 * N;
+            const int part = e / N, n = e - part * N;
+            const double2* hcol = sb + g * G.MC * Np + n;
+            const double2* yy = ys + g * G.M + m0;
+            double a = bsm[q];
+#pragma unroll 1
+            for (int mm = 0; mm < rows; ++mm) {
+              const double2 h = hcol[mm * Np];
+              const double2 yv = yy[mm];
+              const double y1 = part ? yv.y : yv.x, y2 = part ? -yv.x : yv.y;
+              a = __dadd_rn(a, __dadd_rn(__dmul_rn(h.x, y1), __dmul_rn(h.y, y2)));
+            }
+            bsm[q] = a;
+          }
+        }
+        __syncwarp();
+        if ((tid & 31) == 0) mbar_arrive(&empty[s]);
+      }
+
+      // ---- hand-off: wait until the CG side has released this slot ----
+      if (tr && tid == 0 && j < 8) tr[j * 8 + 1] = clock64();
+      if (tr && (tid & 31) == 0 && j == 2) tr[72 + tid / 32] = clock64();
+      if (j >= 2) mbar_wait(&sempty[slot], (uint32_t)(((j >> 1) - 1) & 1));
+      if (tr && tid == 0 && j < 8) tr[j * 8 + 2] = clock64();
+      unsigned char* sp = slots + slot * sl.bytes;
+      C* At = reinterpret_cast<C*>(sp + sl.at);
+      double2* bS = reinterpret_cast<double2*>(sp + sl.b);
+      double2* dS = reinterpret_cast<double2*>(sp + sl.d);
+      const int nbt = R * nblk;
+      const bool onchip = args.bj && !args.minv_in;
+      if (active) {
+        C* Ag = At + job.g * N * ldA;
+        double2* dg = dS + job.g * nblk;
+        gram_entries(
+            job, acc, nb, N, args.sigma2,
+            [&](int i, int jx, double2 vij, double2 vji) {
+              Ag[jx * ldA + i] = Ar<K>::rnd(vij, args.pr.mv);
+              Ag[i * ldA + jx] = Ar<K>::rnd(vji, args.pr.mv);
+              if (onchip) {
+                const int kb = i / L;
+                if (kb == jx / L) {
+                  const int il = i - kb * L, jl = jx - kb * L;
+                  dg[(il * L + jl) * nbt + kb] = vij;
+                  dg[(jl * L + il) * nbt + kb] = vji;
+                }
+              }
+            },
+            [&](int i, double2 vii) {
+              Ag[i * ldA + i] = Ar<K>::rnd(vii, args.pr.mv);
+              if (onchip) {
+                const int kb = i / L, il = i - kb * L;
+                dg[(il * L + il) * nbt + kb] = vii;
+              }
+            });
+      }
+      if (kChainInLoop) {
+        if (chain_ok) reinterpret_cast<double*>(bS + cq_g * N + cq_n)[cq_part] = ca;
+      } else {
+#pragma unroll 1
+        for (int q = tid; q < nchain; q += gt) {
+          const int g = q / (2 * N), e = q - g * 2 * N;
+          const int part = e / N;
+          reinterpret_cast<double*>(bS + g * N + (e - part * N))[part] = bsm[q];
+        }
+      }
+      gbar.sync();
+      if (tid == 0) mbar_arrive(&sfull[slot]);
+      if (tr && tid == 0 && j < 8) tr[j * 8 + 3] = clock64();
+    }
+  } else {
+    // ============================ CG warps ============================
+    const int lt = tid - gt - 32;
+    NamedBar cbar{2, ct};
+    CgSmem<K> S;
+    S.R = R;
+    S.N = N;
+    S.L = L;
+    S.ldA = ldA;
+    S.minv = reinterpret_cast<double2*>(smem + args.off_minv);
+    double2* vec = reinterpret_cast<double2*>(smem + args.off_vec);
+    const int RN = R * N;
+    S.x = vec + RN;
+    S.r = vec + 2 * RN;
+    S.p = vec + 3 * RN;
+    S.z = vec + 4 * RN;
+    S.w = vec + 5 * RN;
+    S.xn = vec + 6 * RN;
+    S.rn = vec + 7 * RN;
+    S.pmv = reinterpret_cast<P*>(smem + args.off_pmv);
+    S.tphi = reinterpret_cast<C*>(smem + args.off_tip);
+    S.trho = S.tphi + RN;
+    S.tr1 = S.trho + RN;
+    S.rip = S.tr1 + RN;
+    S.sc = reinterpret_cast<double2*>(smem + args.off_sc);
+    S.fl = reinterpret_cast<int*>(smem + args.off_fl);
+    double2* scr2 = reinterpret_cast<double2*>(smem + args.off_scr2);
+    const int bps = 2 * args.sl.bpa;
+    unsigned long long be = 0, se = 0;
+#pragma unroll 1
+    for (int j = 0; j < my_groups; ++j) {
+      const long t0 = ((long)blockIdx.x + (long)j * gridDim.x) * R;
+      const int Rv = (int)min((long)R, args.T - t0);
+      const int slot = j & 1;
+      unsigned char* sp = slots + slot * sl.bytes;
+      S.At = reinterpret_cast<C*>(sp + sl.at);
+      S.b = reinterpret_cast<double2*>(sp + sl.b);
+      double2* dS = reinterpret_cast<double2*>(sp + sl.d);
+      mbar_wait(&sfull[slot], (uint32_t)((j >> 1) & 1));
+      if (tr && lt == 0 && j < 8) tr[j * 8 + 4] = clock64();
+#pragma unroll 1
+      for (int g = lt; g < R; g += ct) S.fl[g * 4] = g < Rv ? 1 : 0;
+      cbar.sync();
+      // block-Jacobi inverses (on-chip fp64 Cholesky, or injected)
+      if (args.bj) {
+        if (args.minv_in) {
+#pragma unroll 1
+          for (int q = lt; q < Rv * N * L; q += ct) {
+            const int g = q / (N * L);
+            const int e = q - g * N * L;
+            const int kb = e / (L * L), o = e - kb * L * L;
+            const int Lk = min(L, N - kb * L);
+            if (o >= Lk * Lk) continue;
+            const int i = o / Lk, jj = o - i * Lk;
+            S.minv[g * N * L + kb * L * L + jj * Lk + i] =
+                Ar<WK>::rnd(args.minv_in[(t0 + g) * (long)N * L + e], args.pr.work);
+          }
+        } else {
+          const int nbt = R * nblk;
+#pragma unroll 1
+          for (int q = lt; q < Rv * nblk; q += ct) {
+            const int g = q / nblk, kb = q - g * nblk;
+            const int Lk = min(L, N - kb * L);
+            double2* out = S.minv + g * N * L + kb * L * L;
+            const bool ok = (LB > 0) ? hpd_inverse<LB>(dS + q, nbt, scr2 + q, nbt, out, Lk)
+                                     : hpd_inverse<0>(dS + q, nbt, scr2 + q, nbt, out, Lk);
+            if (!ok) {
+              atomicExch(&S.fl[g * 4], 0);
+              atomicAdd(&cnt[FPM_CNT_NONPD], 1ULL);
+            } else if (WK != FK_F64) {
+              for (int e = 0; e < Lk * Lk; ++e) out[e] = Ar<WK>::rnd(out[e], args.pr.work);
+            }
+          }
+        }
+        cbar.sync();
+      }
+      if (!(args.debug & 1)) cg_group<WK, K, LB>(S, Rv, args.iters, args.bj != 0, args.textbook != 0, args.pr, ct, lt, cbar);
+      // slot no longer needed (A, b, diagonal blocks consumed)
+      if (lt == 0) mbar_arrive(&sempty[slot]);
+      if (tr && lt == 0 && j < 8) tr[j * 8 + 5] = clock64();
+      // slicer + counters + write-back
+#pragma unroll 1
+      for (int q = lt; q < Rv * N; q += ct) {
+        const long gq = t0 * N + q;
+        const double2 xv = S.x[q];
+        args.x[gq] = xv;
+        int sym;
+        be += slice_one(xv, args.tx ? args.tx + gq * bps : nullptr, args.rx ? args.rx + gq * bps : nullptr,
+                        args.sl, &sym);
+        se += sym;
+      }
+#pragma unroll 1
+      for (int g = lt; g < Rv; g += ct) {
+        const int bk = S.fl[g * 4 + 2], dv = S.fl[g * 4 + 3];
+        args.brk[t0 + g] = bk;
+        args.div[t0 + g] = dv;
+        if (dv >= 0) atomicAdd(&cnt[FPM_CNT_DIVERGED], 1ULL);
+        if (bk >= 0) atomicAdd(&cnt[FPM_CNT_BREAKDOWN], 1ULL);
+      }
+      if (lt == 0) atomicAdd(&cnt[FPM_CNT_TRIALS], (unsigned long long)Rv);
+      cbar.sync();  // x / flags read before the next group overwrites them
+    }
+#pragma unroll
+    for (int off = 16; off; off >>= 1) {
+      be += __shfl_xor_sync(0xffffffffu, be, off);
+      se += __shfl_xor_sync(0xffffffffu, se, off);
+    }
+    if ((lt & 31) == 0) {
+      if (be) atomicAdd(&cnt[FPM_CNT_BIT_ERRORS], be);
+      if (se) atomicAdd(&cnt[FPM_CNT_SYMBOL_ERRORS], se);
+    }
+  }
+  __syncthreads();
+  if (tid < FPM_NCOUNTERS && cnt[tid]) atomicAdd(&args.counters[tid], cnt[tid]);
+}
+
+template <int WK, int K, int NB, int LB>
+int launch_detect_ws_t(const DetectArgs& a, const WsLayout& sl, int grid, cudaStream_t st) {
+  auto k = fpm_detect_ws_kernel<WK, K, NB, LB>;
+  if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, a.smem_bytes) != cudaSuccess)
+    return FPM_ECUDA;
+  k<<<(unsigned)grid, a.ws_gt + 32 + a.ws_ct, a.smem_bytes, st>>>(a, sl);
+  count_launch();
+  return cudaGetLastError() == cudaSuccess ? FPM_OK : FPM_ECUDA;
+}
+
+}  // namespace fpm

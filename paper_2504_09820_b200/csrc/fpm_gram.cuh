@@ -30,9 +30,12 @@
 #include "fpm_arith.cuh"
 #include "fpm_ptx.cuh"
 
-#ifndef FPM_ROW_UNROLL
-#define FPM_ROW_UNROLL _Pragma("unroll 1")
+#ifndef FPM_ROW_UNROLL_N
+#define FPM_ROW_UNROLL_N 1
 #endif
+#define FPM_PRAGMA_(x) _Pragma(#x)
+#define FPM_UNROLL_(n) FPM_PRAGMA_(unroll n)
+#define FPM_ROW_UNROLL FPM_UNROLL_(FPM_ROW_UNROLL_N)
 
 namespace fpm {
 

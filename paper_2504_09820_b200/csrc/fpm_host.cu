@@ -11,7 +11,7 @@
 #include <cstring>
 
 #include "../../include/fpmimo_b200.h"
-#include "fpm_detect.cuh"
+#include "fpm_detect_ws.cuh"
 
 namespace fpm {
 
@@ -375,6 +375,90 @@ static bool plan_cg(int N, int L, int bj, int mvk, int ipk, CgArgs& a, int& smem
 
 // Specialisations the per-kind units provide (nb = N/4, lb = L): see
 // fpm_inst_<kind>.cu.  Anything else runs the kind's generic instance.
+static int sm_count() {
+  static int v = -1;
+  if (v < 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+  }
+  return v;
+}
+
+// Warp-specialised persistent kernel geometry (fpm_detect_ws.cuh): R realizations
+// per group with uniform Gram warps, gt Gram threads + ct CG threads <= 512.
+static bool plan_detect_ws(int M, int N, int L, int bj, int mvk, int ipk, DetectArgs& a, WsLayout& sl, int& grid) {
+  if (std::getenv("FPM_NO_WS")) return false;
+  const int Np = (N + 7) / 8 * 8, nb = Np / 4, Cc = nb * (nb / 2 - 1);
+  const int limit = max_smem_optin();
+  int best = -1;
+  for (int R = 64; R >= 1; R /= 2) {
+    const int gt = R * nb * nb / 2;
+    const int ct = (R * N + 31) / 32 * 32 + 32;
+    if (gt > 384 || gt + ct > 512 || gt < 32) continue;
+    if ((R * Cc) % 32 || (R * nb) % 32) continue;
+    if (env_int("FPM_R", 0) && env_int("FPM_R", 0) != R) continue;
+    best = R;
+    break;
+  }
+  if (best < 0) return false;
+  const int R = best;
+  const int Lb = bj ? L : 1;
+  for (int stage_kb = env_int("FPM_STAGE_KB", 24); stage_kb >= 4; stage_kb /= 2) {
+    GramGeom G;
+    gram_geom(R, M, N, G, stage_kb);
+    G.S = std::max(3, G.S);  // the producer refills two chunks behind
+    const int ldA = N + 1;
+    size_t off = 128;  // mbarriers
+    a.off_union = (int)off;  // H stage ring
+    off = align_up(off + (size_t)G.S * R * G.MC * G.Np * 16, 128);
+    a.off_ys = (int)off;
+    off = align_up(off + (size_t)2 * R * M * 16, 128);
+    sl.at = 0;
+    sl.b = (int)align_up((size_t)R * N * ldA * mv_bytes(mvk), 128);
+    sl.d = (int)align_up(sl.b + (size_t)R * N * 16, 128);
+    sl.bytes = (int)align_up(sl.d + (bj ? (size_t)R * N * Lb * 16 : 0), 128);
+    a.off_slot = (int)off;
+    off = align_up(off + (size_t)2 * sl.bytes, 128);
+    a.off_bsm = (int)off;  // matched-filter chain accumulators
+    off = align_up(off + (size_t)2 * R * N * 8, 128);
+    a.off_minv = (int)off;
+    off = align_up(off + (bj ? (size_t)R * N * Lb * 16 : 0), 128);
+    a.off_scr2 = (int)off;
+    off = align_up(off + (bj ? (size_t)R * N * Lb * 16 : 0), 128);
+    a.off_vec = (int)off;
+    off = align_up(off + (size_t)8 * R * N * 16, 128);
+    a.off_pmv = (int)off;
+    off = align_up(off + (size_t)R * N * p_bytes(mvk), 128);
+    a.off_tip = (int)off;
+    off = align_up(off + (size_t)4 * R * N * mv_bytes(ipk), 128);
+    a.off_sc = (int)off;
+    off = align_up(off + (size_t)R * 8 * 16, 128);
+    a.off_fl = (int)off;
+    off = align_up(off + (size_t)R * 4 * 4, 128);
+    if ((long)off + 1024 <= limit) {
+      a.G = G;
+      a.ldA = ldA;
+      a.smem_bytes = (int)off;
+      a.ws_gt = R * nb * nb / 2;
+      a.ws_ct = (R * N + 31) / 32 * 32 + 32;
+      const long ngroups = (a.T + R - 1) / R;
+      grid = (int)std::min<long>(ngroups, (long)sm_count() * env_int("FPM_CTAS_PER_SM", 1));
+      return true;
+    }
+  }
+  return false;
+}
+
+// CG team width: TL lanes per realization (power of two), <= 8 rows per lane.
+static int pick_tl(int N) {
+  int tl = env_int("FPM_TL", 16);
+  while (tl < 32 && (N + tl - 1) / tl > 8) tl *= 2;
+  int p2 = 1;
+  while (p2 < N && p2 < 32) p2 *= 2;
+  return std::max(1, std::min(tl, p2));
+}
+
 static void pick_spec(int N, int L, int bj, int& nb, int& lb) {
   nb = (N % 8 == 0) ? N / 4 : 0;
   lb = bj ? L : 0;
@@ -393,6 +477,21 @@ static int launch_detect(const Kinds& k, const DetectArgs& a, int threads, cudaS
     case FK_F16: return launch_detect_f16(a, threads, nb, lb, st);
     case FK_BF16: return launch_detect_bf16(a, threads, nb, lb, st);
     default: return launch_detect_gen(a, threads, 0, 0, st);
+  }
+}
+
+static int launch_detect_ws(const Kinds& k, const DetectArgs& a, const WsLayout& sl, int grid, cudaStream_t st) {
+  int nb, lb;
+  pick_spec(a.G.N, a.L, a.bj, nb, lb);
+  if (a.G.N != a.G.Np) nb = 0;
+  if (std::getenv("FPM_NO_SPEC")) nb = lb = 0;
+  if (k.w == FK_GEN) return launch_detect_ws_gen_w(a, sl, grid, 0, 0, st);
+  switch (k.mv) {
+    case FK_F64: return launch_detect_ws_f64(a, sl, grid, nb, lb, st);
+    case FK_F32: return launch_detect_ws_f32(a, sl, grid, nb, lb, st);
+    case FK_F16: return launch_detect_ws_f16(a, sl, grid, nb, lb, st);
+    case FK_BF16: return launch_detect_ws_bf16(a, sl, grid, nb, lb, st);
+    default: return launch_detect_ws_gen(a, sl, grid, 0, 0, st);
   }
 }
 
@@ -575,6 +674,7 @@ int fpm_cg(const double* A, const double* b, const double* Minv, int64_t T, int3
   a.x = reinterpret_cast<double2*>(x);
   a.brk = breakdown_at;
   a.div = diverged_at;
+  a.tl = pick_tl(N);
   int smem = 0;
   if (!plan_cg(N, a.L, bj, k.mv, k.ip, a, smem)) return FPM_EUNSUPPORTED;
   return launch_cg(k, a, smem, (cudaStream_t)stream);
@@ -597,7 +697,8 @@ int fpm_slice_count(const double* x, const uint8_t* tx_bits, int64_t T, int32_t 
 static int detect_args(const double* H, const double* y, const uint8_t* tx_bits, int64_t T, int32_t M, int32_t N,
                        double sigma2, int32_t algorithm, int32_t L, int32_t iters, const fpm_precision* prec,
                        int32_t rho_update, int32_t qam, const double* Minv_in, double* x, int32_t* brk,
-                       int32_t* div, uint8_t* rx, int64_t* counters, DetectArgs& a, Kinds& k, int& threads) {
+                       int32_t* div, uint8_t* rx, int64_t* counters, DetectArgs& a, Kinds& k, int& threads,
+                       bool& ws, WsLayout& sl, int& grid) {
   if (T < 0 || M < 1 || N < 1) return FPM_EINVAL;
   if (iters < 1) return FPM_EINVAL;
   if (rho_update != FPM_RHO_AS_WRITTEN && rho_update != FPM_RHO_TEXTBOOK) return FPM_EINVAL;
@@ -631,7 +732,15 @@ static int detect_args(const double* H, const double* y, const uint8_t* tx_bits,
   a.counters = reinterpret_cast<unsigned long long*>(counters);
   a.sl = make_slicer(qam);
   a.trace = g_trace;
+  a.tl = pick_tl(N);
+  a.debug = env_int("FPM_DEBUG", 0);
   k = pick_kinds(*pp);
+  DetectArgs aw = a;
+  ws = plan_detect_ws(M, N, a.L, bj, k.mv, k.ip, aw, sl, grid);
+  if (ws) {
+    a = aw;
+    return FPM_OK;
+  }
   if (!plan_detect(M, N, a.L, bj, k.mv, k.ip, a, threads)) return FPM_EUNSUPPORTED;
   return FPM_OK;
 }
@@ -643,11 +752,14 @@ int fpm_detect(const double* H, const double* y, const uint8_t* tx_bits, int64_t
   if (!H || !y || !x || !breakdown_at || !diverged_at || !counters) return FPM_EINVAL;
   DetectArgs a;
   Kinds k;
-  int threads = 0;
+  int threads = 0, grid = 0;
+  bool ws = false;
+  WsLayout sl;
   int rc = detect_args(H, y, tx_bits, T, M, N, sigma2, algorithm, L, iters, prec, rho_update, qam, Minv_in, x,
-                       breakdown_at, diverged_at, rx_bits, counters, a, k, threads);
+                       breakdown_at, diverged_at, rx_bits, counters, a, k, threads, ws, sl, grid);
   if (rc) return rc;
   if (T == 0) return FPM_OK;
+  if (ws) return launch_detect_ws(k, a, sl, grid, (cudaStream_t)stream);
   return launch_detect(k, a, threads, (cudaStream_t)stream);
 }
 
@@ -658,9 +770,11 @@ int fpm_detect_host(const double* H, const double* y, const uint8_t* tx_bits, in
   if (!H || !y || !x || !breakdown_at || !diverged_at || !counters) return FPM_EINVAL;
   DetectArgs a;
   Kinds k;
-  int threads = 0;
+  int threads = 0, grid0 = 0;
+  bool ws = false;
+  WsLayout sl;
   int rc = detect_args(H, y, tx_bits, T, M, N, sigma2, algorithm, L, iters, prec, rho_update, qam, Minv_in, x,
-                       breakdown_at, diverged_at, rx_bits, counters, a, k, threads);
+                       breakdown_at, diverged_at, rx_bits, counters, a, k, threads, ws, sl, grid0);
   if (rc) return rc;
   if (T == 0) return FPM_OK;
   const int bps = qam == 64 ? 6 : 4;
@@ -716,7 +830,12 @@ int fpm_detect_host(const double* H, const double* y, const uint8_t* tx_bits, in
     b.div = ddv;
     b.rx = rx_bits ? drx : nullptr;
     b.counters = reinterpret_cast<unsigned long long*>(dcnt + s * FPM_NCOUNTERS);
-    rc = launch_detect(k, b, threads, st[s]);
+    if (ws) {
+      const int grid = (int)std::min<long>((n + a.G.R - 1) / a.G.R, (long)sm_count() * env_int("FPM_CTAS_PER_SM", 1));
+      rc = launch_detect_ws(k, b, sl, grid, st[s]);
+    } else {
+      rc = launch_detect(k, b, threads, st[s]);
+    }
     if (rc) break;
     cudaMemcpyAsync(x + c0 * (int64_t)N * 2, dx, (size_t)n * N * 16, cudaMemcpyDeviceToHost, st[s]);
     cudaMemcpyAsync(breakdown_at + c0, dbk, (size_t)n * 4, cudaMemcpyDeviceToHost, st[s]);

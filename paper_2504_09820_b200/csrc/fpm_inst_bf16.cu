@@ -1,5 +1,5 @@
 // fp64 work, bfloat16 matvec / inner products.  Specialisation: c2-p7 (N=32, plain).
-#include "fpm_detect.cuh"
+#include "fpm_detect_ws.cuh"
 namespace fpm {
 int launch_detect_bf16(const DetectArgs& a, int threads, int nb, int lb, cudaStream_t st) {
   if (nb == 8 && lb == 0) return launch_detect_t<FK_F64, FK_BF16, 8, 0>(a, threads, st);
@@ -7,5 +7,9 @@ int launch_detect_bf16(const DetectArgs& a, int threads, int nb, int lb, cudaStr
 }
 int launch_cg_bf16(const CgArgs& a, int smem, int lb, cudaStream_t st) {
   return launch_cg_t<FK_F64, FK_BF16, 0>(a, smem, st);
+}
+int launch_detect_ws_bf16(const DetectArgs& a, const WsLayout& sl, int grid, int nb, int lb, cudaStream_t st) {
+  if (nb == 8 && lb == 0) return launch_detect_ws_t<FK_F64, FK_BF16, 8, 0>(a, sl, grid, st);
+  return launch_detect_ws_t<FK_F64, FK_BF16, 0, 0>(a, sl, grid, st);
 }
 }  // namespace fpm

@@ -1,6 +1,6 @@
 // Generic emulation of any (sig, exp) format: fp64 work with generic
 // matvec/inner formats, and everything generic (work coarser than fp64).
-#include "fpm_detect.cuh"
+#include "fpm_detect_ws.cuh"
 namespace fpm {
 int launch_detect_gen(const DetectArgs& a, int threads, int nb, int lb, cudaStream_t st) {
   return launch_detect_t<FK_F64, FK_GEN, 0, 0>(a, threads, st);
@@ -13,5 +13,11 @@ int launch_detect_gen_w(const DetectArgs& a, int threads, int nb, int lb, cudaSt
 }
 int launch_cg_gen_w(const CgArgs& a, int smem, int lb, cudaStream_t st) {
   return launch_cg_t<FK_GEN, FK_GEN, 0>(a, smem, st);
+}
+int launch_detect_ws_gen(const DetectArgs& a, const WsLayout& sl, int grid, int nb, int lb, cudaStream_t st) {
+  return launch_detect_ws_t<FK_F64, FK_GEN, 0, 0>(a, sl, grid, st);
+}
+int launch_detect_ws_gen_w(const DetectArgs& a, const WsLayout& sl, int grid, int nb, int lb, cudaStream_t st) {
+  return launch_detect_ws_t<FK_GEN, FK_GEN, 0, 0>(a, sl, grid, st);
 }
 }  // namespace fpm

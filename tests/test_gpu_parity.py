@@ -241,3 +241,29 @@ def test_large_batch_properties():
     H, y, bits = _gpu_batch(T, 128, 16, 2)
     res = detect(DetectorSpec("cg", iters=16), H, y, 1e-30, bits)
     assert res.counters["bit_errors"] == 0
+
+
+def test_persistent_kernel_multi_group_and_partial_group():
+    """The warp-specialised persistent kernel loops over several realization
+    groups per CTA (148 CTAs) and ends with a partial group: bit-exact vs the
+    oracle with injected block inverses, and the fallback kernel agrees."""
+    import fpm_oracle as O
+    from paper_2504_09820_b200.detect import DetectorSpec, detect
+    T = 148 * 2 * 3 + 1
+    H, y, bits, s2 = _oracle_inputs(128, 64, 0.5, 15.0, T)
+    det = DetectorSpec("fp_bj_cg", iters=8, L=4, matvec="fp16", inner="fp16")
+    A, b = O.gram_mf_einsum(H, y, s2)
+    mats = O.bj_inverses(A, 4)
+    ref = O.cg_batch(A, b, 8, O.FP64, O.FP16, O.FP16, mats)
+    res = detect(det, H, y, s2, bits, minv=mats, want_bits=True)
+    assert bits_equal(res.x, ref.x)
+    ob = O.demod16(ref.x)
+    np.testing.assert_array_equal(res.bits, ob)
+    assert res.counters["bit_errors"] == int(O.bit_errors(ob, bits).sum())
+    assert res.counters["trials"] == T
+    os.environ["FPM_NO_WS"] = "1"
+    try:
+        res2 = detect(det, H, y, s2, bits, minv=mats)
+    finally:
+        del os.environ["FPM_NO_WS"]
+    assert bits_equal(res2.x, ref.x)

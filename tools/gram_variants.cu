@@ -176,25 +176,19 @@ int main() {
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  const int reps = 200, blocks = 148 * 4;
-  auto rep = [&](const char* nm, double ops_per_thread_row, int bpsm) {
+  const int reps = 200;
+  cudaFuncSetAttribute(v1, cudaFuncAttributeMaxDynamicSharedMemorySize, 150 * 1024);
+  for (int thr : {128, 256, 384, 512}) {
+    const int blocks = 148 * 4 * 512 / thr;
+    v1<<<blocks, thr, 150 * 1024>>>(d, reps);  // 150 KB dynamic smem: one CTA per SM
+    cudaEventRecord(e0);
+    v1<<<blocks, thr, 150 * 1024>>>(d, reps);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
     float ms;
     cudaEventElapsedTime(&ms, e0, e1);
-    double ops = (double)blocks * 512 * reps * ROWS * ops_per_thread_row;
-    printf("%-34s %8.3f ms  %6.2f TFLOP/s (non-fused DP ops)\n", nm, ms, ops / (ms * 1e-3) / 1e12);
-  };
-#define T(nm, launch, opr)   \
-  launch;                    \
-  cudaEventRecord(e0);       \
-  launch;                    \
-  cudaEventRecord(e1);       \
-  cudaEventSynchronize(e1);  \
-  rep(nm, opr, 1);
-  T("v0 runtime nb, 8 operands", (v0<<<blocks, 512>>>(d, reps, 16)), 128.0);
-  T("v1 compile-time NB", (v1<<<blocks, 512>>>(d, reps)), 128.0);
-  T("v2 products-first groups", (v2<<<blocks, 512>>>(d, reps)), 128.0);
-  T("v3 next-row prefetch", (v3<<<blocks, 512>>>(d, reps)), 128.0);
-  T("v4 4x2 tiles, 2 CTA/SM", (v4<<<blocks * 2, 512>>>(d, reps)), 64.0);
-  printf("%s\n", cudaGetErrorString(cudaGetLastError()));
+    double ops = (double)blocks * thr * reps * ROWS * 128.0;
+    printf("v1 %3d threads/CTA (1 CTA/SM resident): %6.2f TFLOP/s\n", thr, ops / (ms * 1e-3) / 1e12);
+  }
   return 0;
 }

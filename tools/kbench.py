@@ -48,6 +48,7 @@ def main():
     ap.add_argument("--N", type=int, default=bench.N)
     ap.add_argument("--L", type=int, default=bench.L)
     ap.add_argument("--trace", action="store_true")
+    ap.add_argument("--wstrace", action="store_true")
     a = ap.parse_args()
     bench.M, bench.N, bench.L = a.M, a.N, a.L
     M, N, L, T = a.M, a.N, a.L, a.T
@@ -96,6 +97,19 @@ def main():
         byts = 16 * N * N + 16 * N * (2 + L) + 8
         out["cg"] = {"ms": ms, "det_s": T / ms * 1e3, "hbm_gbs": byts * T / (ms / 1e3) / 1e9,
                      "hbm_frac": byts * T / (ms / 1e3) / 6554.9e9}
+    if a.wstrace:
+        tr = torch.zeros(96, dtype=torch.int64, device=dev)
+        lib.fpm_debug_set_trace(tr.data_ptr())
+        fused()
+        torch.cuda.synchronize()
+        lib.fpm_debug_set_trace(None)
+        t = tr.cpu().tolist()
+        t0 = t[0]
+        out["ws_timeline"] = [{"gram_start": t[j*8]-t0, "gram_loop": t[j*8+1]-t[j*8], "slot_wait": t[j*8+2]-t[j*8+1],
+                               "handoff": t[j*8+3]-t[j*8+2], "cg_start": t[j*8+4]-t0, "cg_bj_cg": t[j*8+5]-t[j*8+4],
+                               "w0_empty_wait": t[j*8+6], "w0_full_wait": t[j*8+7], "w1_full_wait": t[64+j]}
+                              for j in range(8)]
+        out["ws_warp_loopend_g2"] = [t[72 + w] - t[2*8+0] for w in range(12)]
     if a.trace:
         tr = torch.zeros(64, dtype=torch.int64, device=dev)
         lib.fpm_debug_set_trace(tr.data_ptr())
