@@ -47,6 +47,19 @@ def f_gram():
     return 4 * M * N * (N + 1) + 8 * M * N
 
 
+def ncu_traffic(units):
+    """dram__bytes_read.sum + dram__bytes_write.sum of the fused kernel from
+    the committed `ncu --set full` capture (profiles/), scaled per launch."""
+    p = os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")
+    try:
+        d = json.load(open(p))
+    except (OSError, ValueError):
+        return None
+    per = (d["dram_bytes_read"] + d["dram_bytes_write"]) / d["realizations_per_launch"]
+    return {"bytes": int(per * units), "source": f"profiles/{os.path.basename(p)}: {per:.0f} B/realization "
+                                                  f"measured at {d['realizations_per_launch']}/launch x {units}"}
+
+
 def io_bytes():
     """HBM bytes per detection: H, y read, x_hat written +
     tx bits read (4N uint8)."""
@@ -265,6 +278,8 @@ def run_ours(args):
         _lib.check(lib.fpm_probe_fp64(200000, ctypes.byref(out)), "probe")
         peak_dp = out.value
     ach_dp = f_gram() * min(pool, T) / (kernel_ms / 1e3)
+    kname = lib.fpm_last_kernel().decode()
+    traffic = ncu_traffic(min(pool, T))
 
     # e2e: host (pinned) buffers through the C-ABI host pipeline, copies in the timed region
     e2e = None
@@ -315,8 +330,10 @@ def run_ours(args):
             "ber": counters["bit_errors"] / max(1, counters["trials"] * 4 * N),
             "roofline": {"bound": "fp64", "achieved": round(ach_dp / 1e12, 3),
                          "peak": round(peak_dp / 1e12, 3) if peak_dp else None, "unit": "TFLOP/s",
-                         "frac": round(ach_dp / peak_dp, 4) if peak_dp else None, "traffic": None,
-                         "kernel": "fpm_detect_kernel", "kernel_ms": round(kernel_ms, 3),
+                         "frac": round(ach_dp / peak_dp, 4) if peak_dp else None,
+                         "traffic": traffic["bytes"] if traffic else None,
+                         "traffic_source": traffic["source"] if traffic else None,
+                         "kernel": kname, "kernel_ms": round(kernel_ms, 3),
                          "work_per_unit": f"F_gram = 4MN(N+1)+8MN = {f_gram()} non-fused fp64 ops/detection",
                          "peak_source": "fpm_probe_fp64 (measured non-fused DMUL/DADD rate, this GPU)",
                          "hbm": {"achieved_gbs": round(io_bytes() * min(pool, T) / (kernel_ms / 1e3) / 1e9, 1),

@@ -126,6 +126,11 @@ int fpm_detect_host(const double* H, const double* y, const uint8_t* tx_bits, in
  * entry points), for launch accounting in benchmarks. */
 int64_t fpm_launch_count(void);
 
+/* Name and specialisation of the last fused detector kernel this library
+ * launched ("" before the first fpm_detect / fpm_detect_host call); for
+ * benchmark / profile reports.  Not thread-safe across host threads. */
+const char* fpm_last_kernel(void);
+
 /* Diagnostic: measured rate of non-fused fp64 DMUL/DADD operations per
  * second on the current device (synchronous; the fp64 roofline denominator). */
 int fpm_probe_fp64(int64_t iters, double* dp_ops_per_s);

@@ -22,7 +22,7 @@ NCOUNTERS = 8
 
 # every symbol include/fpmimo_b200.h declares
 EXPORTS = ("fpm_version", "fpm_strerror", "fpm_limits", "fpm_gram", "fpm_bj_setup", "fpm_cg",
-           "fpm_slice_count", "fpm_detect", "fpm_detect_host", "fpm_launch_count", "fpm_probe_fp64",
+           "fpm_slice_count", "fpm_detect", "fpm_detect_host", "fpm_launch_count", "fpm_last_kernel", "fpm_probe_fp64",
            "fpm_debug_set_trace")
 
 
@@ -53,6 +53,7 @@ _SIGS = {
     "fpm_detect_host": (ctypes.c_int, [_P, _P, _P, _I64, _I32, _I32, _D, _I32, _I32, _I32,
                                        ctypes.POINTER(Precision), _I32, _I32, _P, _P, _P, _P, _P, _P, _I64]),
     "fpm_launch_count": (ctypes.c_int64, []),
+    "fpm_last_kernel": (ctypes.c_char_p, []),
     "fpm_probe_fp64": (ctypes.c_int, [_I64, ctypes.POINTER(ctypes.c_double)]),
     "fpm_debug_set_trace": (ctypes.c_int, [_P]),
 }

@@ -7,6 +7,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -465,11 +466,29 @@ static void pick_spec(int N, int L, int bj, int& nb, int& lb) {
   if (bj && nb && (nb % L)) nb = 0;
 }
 
+static char g_last_kernel[96] = "";
+
+static const char* kind_name(int k) {
+  switch (k) {
+    case FK_F64: return "f64";
+    case FK_F32: return "f32";
+    case FK_F16: return "f16";
+    case FK_BF16: return "bf16";
+    default: return "gen";
+  }
+}
+
+static void note_kernel(const char* base, const Kinds& k, int nb, int lb) {
+  std::snprintf(g_last_kernel, sizeof(g_last_kernel), "%s<w=%s,mv=%s,nb=%d,L=%d>", base, kind_name(k.w),
+                kind_name(k.mv), nb, lb);
+}
+
 static int launch_detect(const Kinds& k, const DetectArgs& a, int threads, cudaStream_t st) {
   int nb, lb;
   pick_spec(a.G.N, a.L, a.bj, nb, lb);
   if (a.G.N != a.G.Np) nb = 0;
   if (std::getenv("FPM_NO_SPEC")) nb = lb = 0;
+  note_kernel("fpm_detect_kernel", k, nb, lb);
   if (k.w == FK_GEN) return launch_detect_gen_w(a, threads, 0, 0, st);
   switch (k.mv) {
     case FK_F64: return launch_detect_f64(a, threads, nb, lb, st);
@@ -485,6 +504,7 @@ static int launch_detect_ws(const Kinds& k, const DetectArgs& a, const WsLayout&
   pick_spec(a.G.N, a.L, a.bj, nb, lb);
   if (a.G.N != a.G.Np) nb = 0;
   if (std::getenv("FPM_NO_SPEC")) nb = lb = 0;
+  note_kernel("fpm_detect_ws_kernel", k, nb, lb);
   if (k.w == FK_GEN) return launch_detect_ws_gen_w(a, sl, grid, 0, 0, st);
   switch (k.mv) {
     case FK_F64: return launch_detect_ws_f64(a, sl, grid, nb, lb, st);
@@ -543,6 +563,8 @@ int fpm_limits(int32_t* max_n, int32_t* max_l, int32_t* max_m) {
 }
 
 int64_t fpm_launch_count(void) { return (int64_t)g_launches.load(); }
+
+const char* fpm_last_kernel(void) { return g_last_kernel; }
 
 int fpm_debug_set_trace(int64_t* dev_buf) {
   g_trace = reinterpret_cast<long long*>(dev_buf);
