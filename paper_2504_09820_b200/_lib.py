@@ -12,7 +12,7 @@ import os
 from .errors import ContractViolation
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfpmimo_b200.so")
+LIB_PATH = os.environ.get("FPM_LIB") or os.path.join(_HERE, "libfpmimo_b200.so")  # FPM_LIB: dev variants
 
 FPM_OK, FPM_EINVAL, FPM_ENOTPD, FPM_ECUDA, FPM_EUNSUPPORTED = range(5)
 FPM_RHO = {"as_written": 0, "textbook": 1}

@@ -19,8 +19,10 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-OBJ = os.path.join(HERE, "_obj")
-OUT = os.path.join(HERE, "libfpmimo_b200.so")
+# FPM_BUILD_OUT / FPM_BUILD_OBJ: alternate output (development variants built
+# with different FPM_NVCC_EXTRA macros, loaded through FPM_LIB)
+OBJ = os.environ.get("FPM_BUILD_OBJ", os.path.join(HERE, "_obj"))
+OUT = os.environ.get("FPM_BUILD_OUT", os.path.join(HERE, "libfpmimo_b200.so"))
 HEADER = os.path.join(os.path.dirname(HERE), "include", "fpmimo_b200.h")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -25,6 +25,14 @@
 
 namespace fpm {
 
+// Row pitch (elements) of the u_MV matrix in shared memory: the smallest
+// ldA >= N whose row is an odd number of 16-byte units, so rows start
+// 16-byte aligned (LDS.128) and 8 consecutive rows fall on 8 distinct
+// bank quads (conflict-free quarter-warp phases).
+__host__ __device__ constexpr int lda_for(int N, int csize) {
+  return (((N * csize + 15) / 16) | 1) * 16 / csize;
+}
+
 enum FmtKind : int { FK_F64 = 0, FK_F32 = 1, FK_F16 = 2, FK_BF16 = 3, FK_GEN = 4 };
 
 // Runtime description of a format (generic path); mirrors FloatFormat.

@@ -38,7 +38,7 @@ struct CgSmem {
   typedef typename Ar<K>::C C;
   typedef typename Ar<K>::P P;
   int R, N, L, ldA;
-  C* At;                  // R * N * ldA, transposed: entry (i,k) at k*ldA + i, on the u_MV grid
+  C* At;                  // R * N * ldA, row-major: entry (i,k) at i*ldA + k (ldA = lda_for), u_MV grid
   P* pmv;                 // R * N   p rounded to u_MV, prepared for the matvec
   C *tphi, *trho, *tr1;   // R * N   product terms of p^H w, r^H p, r^H z (or r^H r), u_IP
   C* rip;                 // R * N   r rounded to u_IP
@@ -57,43 +57,132 @@ __device__ __forceinline__ int dot_owner(int g, int which, int rows, int nthread
   return (nthreads - 1 - k) % nthreads;
 }
 
-// left-to-right sum t_0 + t_1 + ... (dot_fp's accumulation, linalg.py:94-95)
+// 16-byte shared-memory vector loads of consecutive elements: V16<T>::n
+// elements per LDS.128 (16-byte aligned source).
+template <class T> struct V16;
+template <> struct V16<__half2> {
+  static constexpr int n = 4;
+  static __device__ __forceinline__ void ld(const __half2* p, __half2* d) {
+    const uint4 u = *reinterpret_cast<const uint4*>(p);
+    d[0] = u2h(u.x); d[1] = u2h(u.y); d[2] = u2h(u.z); d[3] = u2h(u.w);
+  }
+};
+template <> struct V16<__nv_bfloat162> {
+  static constexpr int n = 4;
+  static __device__ __forceinline__ void ld(const __nv_bfloat162* p, __nv_bfloat162* d) {
+    const uint4 u = *reinterpret_cast<const uint4*>(p);
+    d[0] = u2b(u.x); d[1] = u2b(u.y); d[2] = u2b(u.z); d[3] = u2b(u.w);
+  }
+};
+template <> struct V16<Ar<FK_F16>::P> {
+  static constexpr int n = 2;
+  static __device__ __forceinline__ void ld(const Ar<FK_F16>::P* p, Ar<FK_F16>::P* d) {
+    const uint4 u = *reinterpret_cast<const uint4*>(p);
+    d[0].v1 = u2h(u.x); d[0].v2 = u2h(u.y); d[1].v1 = u2h(u.z); d[1].v2 = u2h(u.w);
+  }
+};
+template <> struct V16<Ar<FK_BF16>::P> {
+  static constexpr int n = 2;
+  static __device__ __forceinline__ void ld(const Ar<FK_BF16>::P* p, Ar<FK_BF16>::P* d) {
+    const uint4 u = *reinterpret_cast<const uint4*>(p);
+    d[0].v1 = u2b(u.x); d[0].v2 = u2b(u.y); d[1].v1 = u2b(u.z); d[1].v2 = u2b(u.w);
+  }
+};
+template <> struct V16<float2> {
+  static constexpr int n = 2;
+  static __device__ __forceinline__ void ld(const float2* p, float2* d) {
+    const float4 u = *reinterpret_cast<const float4*>(p);
+    d[0] = make_float2(u.x, u.y); d[1] = make_float2(u.z, u.w);
+  }
+};
+template <> struct V16<double2> {
+  static constexpr int n = 1;
+  static __device__ __forceinline__ void ld(const double2* p, double2* d) { d[0] = *p; }
+};
+
+template <int B, class T>
+__device__ __forceinline__ void ld_blk(const T* p, T (&d)[B]) {
+  constexpr int n = V16<T>::n;
+  static_assert(B % n == 0, "block must be whole 16-byte vectors");
+#pragma unroll
+  for (int i = 0; i < B / n; ++i) V16<T>::ld(p + i * n, d + i * n);
+}
+
+__device__ __forceinline__ bool al16(const void* a, const void* b = nullptr) {
+  return ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) & 15) == 0;
+}
+
+// left-to-right sum t_0 + t_1 + ... (dot_fp's accumulation, linalg.py:94-95).
+// Latency: the dependent adds are the only serial part, so the terms arrive
+// in 64-byte blocks loaded one block AHEAD of the chain (a batch-then-add
+// loop exposes the load latency every block: 2.3x slower, tools/ubench5.cu).
 template <int K>
 __device__ __noinline__ double2 chain_sum(const typename Ar<K>::C* t, int n, const FmtP& f) {
   typedef Ar<K> A;
+  typedef typename A::C C;
+  constexpr int B = sizeof(C) >= 16 ? 2 : 64 / sizeof(C);
   typename A::C s = t[0];
-  int k = 1;
+  if (n % B == 0 && al16(t)) {
+    C v[B], nv[B];
+    ld_blk<B>(t, v);
 #pragma unroll 1
-  for (; k + 8 <= n; k += 8) {
-    typename A::C v[8];
+    for (int k = 0; k < n; k += B) {
+      const bool more = k + B < n;
+      if (more) ld_blk<B>(t + k + B, nv);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) v[j] = t[k + j];
+      for (int j = 0; j < B; ++j)
+        if (k + j > 0) s = A::add(s, v[j], f);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) s = A::add(s, v[j], f);
+      for (int j = 0; j < B; ++j) v[j] = nv[j];
+    }
+    return A::wide(A::asmc(s));
   }
 #pragma unroll 1
-  for (; k < n; ++k) s = A::add(s, t[k], f);
+  for (int k = 1; k < n; ++k) s = A::add(s, t[k], f);
   return A::wide(A::asmc(s));
 }
 
-// w_i = sum_k A(i,k) p_k at u_MV (matvec_fp), A column-major in shared memory;
-// returned assembled (`sr + 1j*si`) in-format
+// w_i = sum_k A(i,k) p_k at u_MV (matvec_fp) over one row of A (row-major,
+// pitch lda_for), returned assembled (`sr + 1j*si`) in-format.  The products
+// of a block are independent; the block's operands are loaded one block
+// ahead of the sequential sum.
 template <int K>
-__device__ __noinline__ typename Ar<K>::C mv_row(const typename Ar<K>::C* col, const typename Ar<K>::P* pv, int N,
-                                               int ldA, const FmtP& f) {
+__device__ __noinline__ typename Ar<K>::C mv_row(const typename Ar<K>::C* row, const typename Ar<K>::P* pv, int N,
+                                               const FmtP& f) {
   typedef Ar<K> A;
-  typename A::C s = A::mulp(col[0], pv[0], f);
-  int k = 1;
+  typedef typename A::C C;
+  typedef typename A::P P;
+  constexpr int B = sizeof(C) >= 16 ? 2 : (sizeof(C) >= 8 ? 4 : 8);
+  if (N % B == 0 && al16(row, pv)) {
+    C a[B], na[B];
+    P p[B], np[B];
+    ld_blk<B>(row, a);
+    ld_blk<B>(pv, p);
+    C s = A::mulp(a[0], p[0], f);
 #pragma unroll 1
-  for (; k + 8 <= N; k += 8) {
-    typename A::C t[8];
+    for (int k = 0; k < N; k += B) {
+      const bool more = k + B < N;
+      if (more) {
+        ld_blk<B>(row + k + B, na);
+        ld_blk<B>(pv + k + B, np);
+      }
+      C t[B];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) t[j] = A::mulp(col[(k + j) * ldA], pv[k + j], f);
+      for (int j = 0; j < B; ++j) t[j] = A::mulp(a[j], p[j], f);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) s = A::add(s, t[j], f);
+      for (int j = 0; j < B; ++j)
+        if (k + j > 0) s = A::add(s, t[j], f);
+#pragma unroll
+      for (int j = 0; j < B; ++j) {
+        a[j] = na[j];
+        p[j] = np[j];
+      }
+    }
+    return A::asmc(s);
   }
+  C s = A::mulp(row[0], pv[0], f);
 #pragma unroll 1
-  for (; k < N; ++k) s = A::add(s, A::mulp(col[k * ldA], pv[k], f), f);
+  for (int k = 1; k < N; ++k) s = A::add(s, A::mulp(row[k], pv[k], f), f);
   return A::asmc(s);
 }
 
@@ -211,6 +300,7 @@ __device__ void cg_group(CgSmem<K>& S, int Rv, int iters, bool bj, bool textbook
   bar.sync();
   if (!rho_fresh && og >= 0 && ow == 0) S.sc[og * 8 + 4] = chain_sum<K>(S.tr1 + og * N, N, fi);
   bar.sync();
+  FPM_STAMP(tr, 0);
 
 #pragma unroll 1
   for (int it = 1; it <= iters; ++it) {
@@ -220,25 +310,31 @@ __device__ void cg_group(CgSmem<K>& S, int Rv, int iters, bool bj, bool textbook
       const int q = tid + k * nthreads;
       const int g = q / N, i = q - g * N;
       if (!S.fl[g * 4]) continue;
-      const C wc = mv_row<K>(S.At + g * N * S.ldA + i, S.pmv + g * N, N, S.ldA, fm);
+      const C wc = mv_row<K>(S.At + (g * N + i) * S.ldA, S.pmv + g * N, N, fm);
       S.w[q] = A::wide(wc);
       const C pi = K == FK_GEN ? ipr(S.p[q]) : A::rnd(S.p[q], fm);
       S.tphi[q] = A::mulc(pi, mv_to_ip(wc), fi);
     }
     if (rho_fresh && og >= 0 && ow == 1 && S.fl[og * 4]) S.sc[og * 8 + 3] = chain_sum<K>(S.trho + og * N, N, fi);
     bar.sync();
+    FPM_STAMP(tr, 1 + (it - 1) * 6 + 0);
     // ---- B: phi, flags, alpha ----
     if (og >= 0 && ow == 0 && S.fl[og * 4]) {
       const int g = og;
+      if (tr && g == 0 && it <= 2) tr[50 + (it - 1) * 4] = clock64();
       const double2 phi = chain_sum<K>(S.tphi + g * N, N, fi);
+      if (tr && g == 0 && it <= 2) tr[51 + (it - 1) * 4] = clock64() + (phi.x == 1.2345e300);
       const double2 rho0 = rho_fresh ? S.sc[g * 8 + 3] : S.sc[g * 8 + 4];
       S.sc[g * 8 + 3] = rho0;
       const bool stall = (rho0.x == 0.0) && (rho0.y == 0.0);
       if (!stall && phi.x <= 0.0) S.fl[g * 4 + 2] = it;  // breakdown
       if (stall || phi.x <= 0.0) S.fl[g * 4] = 0;
-      S.sc[g * 8 + 0] = wdiv<WK>(rho0, phi, fw);
+      const double2 al = wdiv<WK>(rho0, phi, fw);
+      S.sc[g * 8 + 0] = al;
+      if (tr && g == 0 && it <= 2) tr[52 + (it - 1) * 4] = clock64() + (al.x == 1.2345e300);
     }
     bar.sync();
+    FPM_STAMP(tr, 1 + (it - 1) * 6 + 1);
     // ---- C: x, r updates (u_W) + finiteness ----
 #pragma unroll 1
     for (int k = 0; k < nrow; ++k) {
@@ -253,6 +349,7 @@ __device__ void cg_group(CgSmem<K>& S, int Rv, int iters, bool bj, bool textbook
       if (!(finite2(xn) && finite2(rn))) S.fl[g * 4 + 1] = 1;
     }
     bar.sync();
+    FPM_STAMP(tr, 1 + (it - 1) * 6 + 2);
     // ---- D: commit; z = M r_new; rho1 terms ----
 #pragma unroll 1
     for (int k = 0; k < nrow; ++k) {
@@ -273,6 +370,7 @@ __device__ void cg_group(CgSmem<K>& S, int Rv, int iters, bool bj, bool textbook
       }
     }
     bar.sync();
+    FPM_STAMP(tr, 1 + (it - 1) * 6 + 3);
     // ---- E: rho1, beta, divergence flag ----
     if (og >= 0 && ow == 0 && S.fl[og * 4]) {
       const int g = og;
@@ -286,6 +384,7 @@ __device__ void cg_group(CgSmem<K>& S, int Rv, int iters, bool bj, bool textbook
       }
     }
     bar.sync();
+    FPM_STAMP(tr, 1 + (it - 1) * 6 + 4);
     // ---- F: p = (z|r) + beta p ; pmv = rnd(p) ; next rho0 terms ----
     int any = 0;
 #pragma unroll 1
@@ -301,6 +400,7 @@ __device__ void cg_group(CgSmem<K>& S, int Rv, int iters, bool bj, bool textbook
       if (rho_fresh) S.trho[q] = A::mulc(S.rip[q], K == FK_GEN ? ipr(pn) : pm, fi);
     }
     const int more = bar.any(any);
+    FPM_STAMP(tr, 1 + (it - 1) * 6 + 5);
     if (!more) break;
   }
   bar.sync();

@@ -40,6 +40,9 @@ struct DetectArgs {
   long long* trace;  // nullable: phase clock stamps of CTA 0 (diagnostic)
   // warp-specialised persistent kernel: Gram / CG thread counts, slots base
   int ws_gt, ws_ct, off_slot, off_bsm;
+  int ws_order;  // 0: [Gram | producer | CG] threads, 1: [CG | producer | Gram]
+  int ws_ncg, ws_ct0;  // CG groups (1 or 2) and the thread count of group 0
+  int cg_stride;       // bytes between the two CG groups' state regions
   int debug;  // diagnostic bits (FPM_DEBUG): 1 = WS kernel skips the CG side
 };
 

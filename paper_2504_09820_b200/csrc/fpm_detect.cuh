@@ -66,7 +66,7 @@ struct EmitSmem {
   double sigma2;
   __device__ __forceinline__ void job(const GramJob& jb, const double2 (&acc)[16], int nb) {
     const int N = NB > 0 ? 4 * NB : S->N;
-    const int ldA = NB > 0 ? 4 * NB + 1 : S->ldA;
+    const int ldA = NB > 0 ? lda_for(4 * NB, (int)sizeof(typename Ar<K>::C)) : S->ldA;
     const int L = LB > 0 ? LB : S->L;
     const int g = jb.g;
     typename Ar<K>::C* At = S->At + g * N * ldA;
@@ -77,8 +77,8 @@ struct EmitSmem {
     gram_entries(
         jb, acc, nb, N, sigma2,
         [&](int i, int j, double2 vij, double2 vji) {
-          At[j * ldA + i] = Ar<K>::rnd(vij, f);
-          At[i * ldA + j] = Ar<K>::rnd(vji, f);
+          At[i * ldA + j] = Ar<K>::rnd(vij, f);
+          At[j * ldA + i] = Ar<K>::rnd(vji, f);
           if (onchip) {
             const int kb = i / L;
             if (kb == j / L) {
@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_kernel(const DetectArgs arg
   S.R = G.R;
   S.N = N;
   S.L = args.bj ? (LB > 0 ? LB : args.L) : 1;
-  S.ldA = NB > 0 ? N + 1 : args.ldA;
+  S.ldA = NB > 0 ? lda_for(N, (int)sizeof(typename Ar<K>::C)) : args.ldA;
   S.At = reinterpret_cast<C*>(smem + args.off_union);
   S.minv = reinterpret_cast<double2*>(smem + args.off_minv);
   double2* vec = reinterpret_cast<double2*>(smem + args.off_vec);
@@ -284,14 +284,14 @@ __global__ void __launch_bounds__(256) fpm_cg_kernel(const CgArgs args) {
   S.sc = reinterpret_cast<double2*>(smem + args.off_sc);
   S.fl = reinterpret_cast<int*>(smem + args.off_fl);
 
-  // A (row-major, global) -> At (transposed, u_MV), coalesced along k
+  // A (row-major, global) -> At (row-major, pitch ldA, u_MV), coalesced
   const int NN = N * N;
 #pragma unroll 1
   for (int q = tid; q < Rv * NN; q += nthreads) {
     const int g = q / NN;
     const int e = q - g * NN;
     const int i = e / N, k = e - i * N;
-    S.At[g * N * S.ldA + k * S.ldA + i] = Ar<K>::rnd(args.A[(t0 + g) * NN + e], args.pr.mv);
+    S.At[(g * N + i) * S.ldA + k] = Ar<K>::rnd(args.A[(t0 + g) * NN + e], args.pr.mv);
   }
 #pragma unroll 1
   for (int q = tid; q < Rv * N; q += nthreads) S.b[q] = args.b[t0 * N + q];

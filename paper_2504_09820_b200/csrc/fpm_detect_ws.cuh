@@ -15,15 +15,39 @@
 // Each CTA owns groups blockIdx.x, blockIdx.x + gridDim.x, ...  Named
 // hardware barriers: 1 = Gram group, 2 = CG group.
 #pragma once
+#include <algorithm>
+#include <cstdlib>
+
 #include "fpm_detect.cuh"
 
 namespace fpm {
+
+#ifndef FPM_GRAM_PIPE
+#define FPM_GRAM_PIPE 1
+#endif
 
 struct WsLayout {  // byte offsets inside one hand-off slot
   int at, b, d, bytes;
 };
 
-template <int WK, int K, int NB, int LB>
+// role order (FPM_WS_ORDER: 1 = CG warps first, default; 0 = Gram first)
+inline int env_order() {
+  const char* v = std::getenv("FPM_WS_ORDER");
+  return v ? (std::atoi(v) != 0) : 1;
+}
+
+// CG group width under the register split (FPM_WS_CT, default: all 224
+// remaining threads), rounded to whole warps
+inline int env_ct() {
+  const char* v = std::getenv("FPM_WS_CT");
+  const int c = v ? std::atoi(v) : 224;
+  return c / 32 * 32;
+}
+
+// RS > 0: register split (setmaxnreg) for a 512-thread block with gt == 256:
+// the two Gram warp groups run with RS registers per thread, the other two
+// (producer + CG + idle warps) with 256 - RS.
+template <int WK, int K, int NB, int LB, int RS>
 __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const DetectArgs args, const WsLayout sl) {
   extern __shared__ __align__(128) unsigned char smem[];
   typedef typename Ar<K>::C C;
@@ -40,7 +64,7 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const DetectArgs 
   const int nch = (G.M + G.MC - 1) / G.MC;
   const int L = args.bj ? (LB > 0 ? LB : args.L) : 1;
   const int nblk = args.bj ? (N + L - 1) / L : 1;
-  const int ldA = NB > 0 ? N + 1 : args.ldA;
+  const int ldA = NB > 0 ? lda_for(N, (int)sizeof(C)) : args.ldA;
 
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + G.S;
@@ -72,37 +96,16 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const DetectArgs 
 
   const int stage_elems = R * G.MC * Np;
   const long total = (long)my_groups * nch;
-  if (tid >= gt && tid < gt + 32) {
-    // ========================= producer warp ==========================
-    if (tid == gt) {
-      // issue global chunk gc (group gc/nch, local chunk gc%nch) into its stage
-      auto issue = [&](long gc) {
-        const int jj = (int)(gc / nch), c = (int)(gc - (long)jj * nch);
-        const long t0 = ((long)blockIdx.x + (long)jj * gridDim.x) * R;
-        const int Rv = (int)min((long)R, args.T - t0);
-        if (c == 0) {  // this group's y rides with its first chunk
-          double2* yd = ysb + (jj & 1) * R * G.M;
-          mbar_expect_tx(&ybar[jj & 1], (uint32_t)Rv * (uint32_t)G.M * 16u);
-          for (int g = 0; g < Rv; ++g)
-            bulk_g2s(yd + g * G.M, args.y + (t0 + g) * (long)G.M, G.M * 16u, &ybar[jj & 1]);
-        }
-        const int s = (int)(gc % G.S);
-        gram_issue(args.H, t0, Rv, G, c, stages + s * stage_elems, &full[s]);
-      };
-      fence_proxy_async();
-#pragma unroll 1
-      for (long gc = 0; gc < total; ++gc) {
-        if (gc >= G.S) mbar_wait(&empty[gc % G.S], (uint32_t)(((gc - G.S) / G.S) & 1));
-        if (gc >= 2 * nch && gc % nch == 0) {
-          // the y buffer of group jj was last read by group jj-2: wait until
-          // that group's Gram is done (its hand-off has been published)
-          const int jj = (int)(gc / nch);
-          mbar_wait(&sfull[jj & 1], (uint32_t)(((jj - 2) >> 1) & 1));
-        }
-        issue(gc);
-      }
-    }
-  } else if (tid < gt) {
+  // role layout: ws_order 0 = [Gram | producer | CG], 1 = [CG | producer |
+  // Gram].  CG-first gives the latency-bound CG warps the lower warp ids,
+  // which the warp schedulers favour when several warps are ready, so the
+  // throughput-bound Gram warps fill the issue slots the CG chains leave.
+  const int cbase = args.ws_order ? 0 : gt + 32;
+  const int pbase = args.ws_order ? ct : gt;
+  const int gbase = args.ws_order ? ct + 32 : 0;
+  if (tid >= gbase && tid < gbase + gt) {
+    if constexpr (RS > 0) reg_alloc<RS>();
+    const int tid = threadIdx.x - gbase;  // Gram-local thread id
     // =========================== Gram warps ===========================
     NamedBar gbar{1, gt};
     const GramJob job = gram_job(tid, R, nb);
@@ -148,7 +151,61 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const DetectArgs 
         const int rows = min(G.MC, G.M - m0);
         const double2* pa = sb + joff + job.a;
         const double2* pc = sb + joff + job.c;
-        if (active && !job.half) {
+        if (args.debug & 4) {
+          // diagnostic: Gram math skipped (CG measured without FP64 contention)
+        } else if (active && !job.half && FPM_GRAM_PIPE) {
+          // software-pipelined: row mm+1's operands (tile and chain) are in
+          // flight while row mm's products run.  The chain runs branch-free
+          // (its operands are in-bounds stale data for an idle chain, and the
+          // result is only stored when chain_ok); part 1 reads (yi, yr) and
+          // flips the sign of yr exactly (sign-bit xor = IEEE negation).
+          const double* yrow = reinterpret_cast<const double*>(ys + cq_yoff + m0);
+          const double* y1p = yrow + cq_part;
+          const double* y2p = yrow + (1 - cq_part);
+          const unsigned long long yneg = cq_part ? 0x8000000000000000ULL : 0ULL;
+          const double2* hcp = sb + cq_hoff;
+          double2 hi[4], hj[4], hc = make_double2(0.0, 0.0);
+          double y1 = 0.0, y2 = 0.0;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) hi[u] = pa[nb * u];
+#pragma unroll
+          for (int v = 0; v < 4; ++v) hj[v] = pc[nb * v];
+          if (kChainInLoop) {
+            hc = hcp[0];
+            y1 = y1p[0];
+            y2 = y2p[0];
+          }
+#pragma unroll 1
+          for (int mm = 0; mm < rows; ++mm) {
+            const int mn = (mm + 1 < rows) ? mm + 1 : mm;
+            double2 ni[4], nj[4], nhc = hc;
+            double ny1 = y1, ny2 = y2;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) ni[u] = pa[mn * Np + nb * u];
+#pragma unroll
+            for (int v = 0; v < 4; ++v) nj[v] = pc[mn * Np + nb * v];
+            if (kChainInLoop) {
+              nhc = hcp[mn * Np];
+              ny1 = y1p[2 * mn];
+              ny2 = y2p[2 * mn];
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+              for (int v = 0; v < 4; ++v) cmac_conj(acc[u * 4 + v], hi[u], hj[v]);
+            if (kChainInLoop) {
+              const double y2s = __longlong_as_double(__double_as_longlong(y2) ^ yneg);
+              ca = __dadd_rn(ca, __dadd_rn(__dmul_rn(hc.x, y1), __dmul_rn(hc.y, y2s)));
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) hi[u] = ni[u];
+#pragma unroll
+            for (int v = 0; v < 4; ++v) hj[v] = nj[v];
+            hc = nhc;
+            y1 = ny1;
+            y2 = ny2;
+          }
+        } else if (active && !job.half) {
 FPM_ROW_UNROLL
           for (int mm = 0; mm < rows; ++mm) {
             double2 hi[4], hj[4];
@@ -251,8 +308,8 @@ FPM_ROW_UNROLL
         gram_entries(
             job, acc, nb, N, args.sigma2,
             [&](int i, int jx, double2 vij, double2 vji) {
-              Ag[jx * ldA + i] = Ar<K>::rnd(vij, args.pr.mv);
-              Ag[i * ldA + jx] = Ar<K>::rnd(vji, args.pr.mv);
+              Ag[i * ldA + jx] = Ar<K>::rnd(vij, args.pr.mv);
+              Ag[jx * ldA + i] = Ar<K>::rnd(vji, args.pr.mv);
               if (onchip) {
                 const int kb = i / L;
                 if (kb == jx / L) {
@@ -285,16 +342,55 @@ FPM_ROW_UNROLL
       if (tr && tid == 0 && j < 8) tr[j * 8 + 3] = clock64();
     }
   } else {
+    // the producer warp and the CG warp groups hand registers to the Gram warps
+    if constexpr (RS > 0) reg_dealloc<256 - RS>();
+    if (tid >= pbase && tid < pbase + 32) {
+    // ========================= producer warp ==========================
+    if (tid == pbase) {
+      // issue global chunk gc (group gc/nch, local chunk gc%nch) into its stage
+      auto issue = [&](long gc) {
+        const int jj = (int)(gc / nch), c = (int)(gc - (long)jj * nch);
+        const long t0 = ((long)blockIdx.x + (long)jj * gridDim.x) * R;
+        const int Rv = (int)min((long)R, args.T - t0);
+        if (c == 0) {  // this group's y rides with its first chunk
+          double2* yd = ysb + (jj & 1) * R * G.M;
+          mbar_expect_tx(&ybar[jj & 1], (uint32_t)Rv * (uint32_t)G.M * 16u);
+          for (int g = 0; g < Rv; ++g)
+            bulk_g2s(yd + g * G.M, args.y + (t0 + g) * (long)G.M, G.M * 16u, &ybar[jj & 1]);
+        }
+        const int s = (int)(gc % G.S);
+        gram_issue(args.H, t0, Rv, G, c, stages + s * stage_elems, &full[s]);
+      };
+      fence_proxy_async();
+#pragma unroll 1
+      for (long gc = 0; gc < total; ++gc) {
+        if (gc >= G.S) mbar_wait(&empty[gc % G.S], (uint32_t)(((gc - G.S) / G.S) & 1));
+        if (gc >= 2 * nch && gc % nch == 0) {
+          // the y buffer of group jj was last read by group jj-2: wait until
+          // that group's Gram is done (its hand-off has been published)
+          const int jj = (int)(gc / nch);
+          mbar_wait(&sfull[jj & 1], (uint32_t)(((jj - 2) >> 1) & 1));
+        }
+        issue(gc);
+      }
+    }
+    } else if (tid >= cbase && tid < cbase + ct) {
     // ============================ CG warps ============================
-    const int lt = tid - gt - 32;
-    NamedBar cbar{2, ct};
+    // ws_ncg CG groups; group cgi owns hand-off slot cgi, i.e. realization
+    // groups j = cgi, cgi + ncg, ... (two latency-bound solves in flight)
+    const int ncg = args.ws_ncg;
+    const int cgi = (ncg == 2 && tid - cbase >= args.ws_ct0) ? 1 : 0;
+    const int lt = tid - cbase - (cgi ? args.ws_ct0 : 0);
+    const int ctg = ncg == 2 ? (cgi ? ct - args.ws_ct0 : args.ws_ct0) : ct;
+    unsigned char* cgs = smem + cgi * args.cg_stride;  // this group's CG state
+    NamedBar cbar{2 + cgi, ctg};
     CgSmem<K> S;
     S.R = R;
     S.N = N;
     S.L = L;
     S.ldA = ldA;
-    S.minv = reinterpret_cast<double2*>(smem + args.off_minv);
-    double2* vec = reinterpret_cast<double2*>(smem + args.off_vec);
+    S.minv = reinterpret_cast<double2*>(cgs + args.off_minv);
+    double2* vec = reinterpret_cast<double2*>(cgs + args.off_vec);
     const int RN = R * N;
     S.x = vec + RN;
     S.r = vec + 2 * RN;
@@ -303,18 +399,18 @@ FPM_ROW_UNROLL
     S.w = vec + 5 * RN;
     S.xn = vec + 6 * RN;
     S.rn = vec + 7 * RN;
-    S.pmv = reinterpret_cast<P*>(smem + args.off_pmv);
-    S.tphi = reinterpret_cast<C*>(smem + args.off_tip);
+    S.pmv = reinterpret_cast<P*>(cgs + args.off_pmv);
+    S.tphi = reinterpret_cast<C*>(cgs + args.off_tip);
     S.trho = S.tphi + RN;
     S.tr1 = S.trho + RN;
     S.rip = S.tr1 + RN;
-    S.sc = reinterpret_cast<double2*>(smem + args.off_sc);
-    S.fl = reinterpret_cast<int*>(smem + args.off_fl);
-    double2* scr2 = reinterpret_cast<double2*>(smem + args.off_scr2);
+    S.sc = reinterpret_cast<double2*>(cgs + args.off_sc);
+    S.fl = reinterpret_cast<int*>(cgs + args.off_fl);
+    double2* scr2 = reinterpret_cast<double2*>(cgs + args.off_scr2);
     const int bps = 2 * args.sl.bpa;
     unsigned long long be = 0, se = 0;
 #pragma unroll 1
-    for (int j = 0; j < my_groups; ++j) {
+    for (int j = cgi; j < my_groups; j += ncg) {
       const long t0 = ((long)blockIdx.x + (long)j * gridDim.x) * R;
       const int Rv = (int)min((long)R, args.T - t0);
       const int slot = j & 1;
@@ -325,13 +421,13 @@ FPM_ROW_UNROLL
       mbar_wait(&sfull[slot], (uint32_t)((j >> 1) & 1));
       if (tr && lt == 0 && j < 8) tr[j * 8 + 4] = clock64();
 #pragma unroll 1
-      for (int g = lt; g < R; g += ct) S.fl[g * 4] = g < Rv ? 1 : 0;
+      for (int g = lt; g < R; g += ctg) S.fl[g * 4] = g < Rv ? 1 : 0;
       cbar.sync();
       // block-Jacobi inverses (on-chip fp64 Cholesky, or injected)
       if (args.bj) {
         if (args.minv_in) {
 #pragma unroll 1
-          for (int q = lt; q < Rv * N * L; q += ct) {
+          for (int q = lt; q < Rv * N * L; q += ctg) {
             const int g = q / (N * L);
             const int e = q - g * N * L;
             const int kb = e / (L * L), o = e - kb * L * L;
@@ -344,7 +440,7 @@ FPM_ROW_UNROLL
         } else {
           const int nbt = R * nblk;
 #pragma unroll 1
-          for (int q = lt; q < Rv * nblk; q += ct) {
+          for (int q = lt; q < Rv * nblk; q += ctg) {
             const int g = q / nblk, kb = q - g * nblk;
             const int Lk = min(L, N - kb * L);
             double2* out = S.minv + g * N * L + kb * L * L;
@@ -360,13 +456,18 @@ FPM_ROW_UNROLL
         }
         cbar.sync();
       }
-      if (!(args.debug & 1)) cg_group<WK, K, LB>(S, Rv, args.iters, args.bj != 0, args.textbook != 0, args.pr, ct, lt, cbar);
+      long long* tc = (tr && j == 2 && args.iters <= 8) ? tr + 96 : nullptr;  // CG phase stamps, group 2
+      if (tc && lt == 0) {
+        __shared__ int _fpm_dummy_ws;
+        tc[60] = (long long)clock64() + (*(volatile int*)&_fpm_dummy_ws == 0x7fffffff);
+      }
+      if (!(args.debug & 1)) cg_group<WK, K, LB>(S, Rv, args.iters, args.bj != 0, args.textbook != 0, args.pr, ctg, lt, cbar, tc);
       // slot no longer needed (A, b, diagonal blocks consumed)
       if (lt == 0) mbar_arrive(&sempty[slot]);
       if (tr && lt == 0 && j < 8) tr[j * 8 + 5] = clock64();
       // slicer + counters + write-back
 #pragma unroll 1
-      for (int q = lt; q < Rv * N; q += ct) {
+      for (int q = lt; q < Rv * N; q += ctg) {
         const long gq = t0 * N + q;
         const double2 xv = S.x[q];
         args.x[gq] = xv;
@@ -376,7 +477,7 @@ FPM_ROW_UNROLL
         se += sym;
       }
 #pragma unroll 1
-      for (int g = lt; g < Rv; g += ct) {
+      for (int g = lt; g < Rv; g += ctg) {
         const int bk = S.fl[g * 4 + 2], dv = S.fl[g * 4 + 3];
         args.brk[t0 + g] = bk;
         args.div[t0 + g] = dv;
@@ -395,17 +496,37 @@ FPM_ROW_UNROLL
       if (be) atomicAdd(&cnt[FPM_CNT_BIT_ERRORS], be);
       if (se) atomicAdd(&cnt[FPM_CNT_SYMBOL_ERRORS], se);
     }
+    }
   }
   __syncthreads();
   if (tid < FPM_NCOUNTERS && cnt[tid]) atomicAdd(&args.counters[tid], cnt[tid]);
 }
 
+#ifndef FPM_WS_GRAM_REGS
+#define FPM_WS_GRAM_REGS 176
+#endif
+
 template <int WK, int K, int NB, int LB>
 int launch_detect_ws_t(const DetectArgs& a, const WsLayout& sl, int grid, cudaStream_t st) {
-  auto k = fpm_detect_ws_kernel<WK, K, NB, LB>;
+  DetectArgs b = a;
+  b.ws_order = env_order();
+  const int threads = a.ws_gt + 32 + a.ws_ct;
+  if constexpr (NB == 16) {
+    // N = 64, R = 2: 256 Gram threads = two warp groups and a 512-thread
+    // block -> register split between the Gram and the other warp groups
+    if (a.ws_gt == 256 && threads == 512 && !std::getenv("FPM_WS_NOSPLIT")) {
+      auto k = fpm_detect_ws_kernel<WK, K, NB, LB, FPM_WS_GRAM_REGS>;
+      if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, a.smem_bytes) != cudaSuccess)
+        return FPM_ECUDA;
+      k<<<(unsigned)grid, 512, a.smem_bytes, st>>>(b, sl);
+      count_launch();
+      return cudaGetLastError() == cudaSuccess ? FPM_OK : FPM_ECUDA;
+    }
+  }
+  auto k = fpm_detect_ws_kernel<WK, K, NB, LB, 0>;
   if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, a.smem_bytes) != cudaSuccess)
     return FPM_ECUDA;
-  k<<<(unsigned)grid, a.ws_gt + 32 + a.ws_ct, a.smem_bytes, st>>>(a, sl);
+  k<<<(unsigned)grid, threads, a.smem_bytes, st>>>(b, sl);
   count_launch();
   return cudaGetLastError() == cudaSuccess ? FPM_OK : FPM_ECUDA;
 }

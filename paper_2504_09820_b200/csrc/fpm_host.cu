@@ -308,7 +308,7 @@ static bool plan_detect(int M, int N, int L, int bj, int mvk, int ipk, DetectArg
     gram_geom(R, M, N, G, env_int("FPM_STAGE_KB", 24));
     threads = gram_threads(G);
     if (threads > 512) continue;
-    const int ldA = N + 1;
+    const int ldA = lda_for(N, mv_bytes(mvk));
     size_t off = 128;  // mbarriers (2S+1)
     a.off_ys = (int)off;
     off = align_up(off + (size_t)R * M * 16, 128);
@@ -348,7 +348,7 @@ static bool plan_cg(int N, int L, int bj, int mvk, int ipk, CgArgs& a, int& smem
   const int limit = std::min(max_smem_optin(), 110 * 1024);  // aim for >= 2 CTAs / SM
   int R = std::max(1, 256 / N);
   for (; R >= 1; R = (R > 1 ? R / 2 : 0)) {
-    const int ldA = N + 1;
+    const int ldA = lda_for(N, mv_bytes(mvk));
     size_t off = 0;
     off = align_up(off + (size_t)R * N * ldA * mv_bytes(mvk), 128);
     a.off_minv = (int)off;
@@ -405,47 +405,68 @@ static bool plan_detect_ws(int M, int N, int L, int bj, int mvk, int ipk, Detect
   if (best < 0) return false;
   const int R = best;
   const int Lb = bj ? L : 1;
-  for (int stage_kb = env_int("FPM_STAGE_KB", 24); stage_kb >= 4; stage_kb /= 2) {
-    GramGeom G;
-    gram_geom(R, M, N, G, stage_kb);
-    G.S = std::max(3, G.S);  // the producer refills two chunks behind
-    const int ldA = N + 1;
-    size_t off = 128;  // mbarriers
-    a.off_union = (int)off;  // H stage ring
-    off = align_up(off + (size_t)G.S * R * G.MC * G.Np * 16, 128);
-    a.off_ys = (int)off;
-    off = align_up(off + (size_t)2 * R * M * 16, 128);
-    sl.at = 0;
-    sl.b = (int)align_up((size_t)R * N * ldA * mv_bytes(mvk), 128);
-    sl.d = (int)align_up(sl.b + (size_t)R * N * 16, 128);
-    sl.bytes = (int)align_up(sl.d + (bj ? (size_t)R * N * Lb * 16 : 0), 128);
-    a.off_slot = (int)off;
-    off = align_up(off + (size_t)2 * sl.bytes, 128);
-    a.off_bsm = (int)off;  // matched-filter chain accumulators
-    off = align_up(off + (size_t)2 * R * N * 8, 128);
-    a.off_minv = (int)off;
-    off = align_up(off + (bj ? (size_t)R * N * Lb * 16 : 0), 128);
-    a.off_scr2 = (int)off;
-    off = align_up(off + (bj ? (size_t)R * N * Lb * 16 : 0), 128);
-    a.off_vec = (int)off;
-    off = align_up(off + (size_t)8 * R * N * 16, 128);
-    a.off_pmv = (int)off;
-    off = align_up(off + (size_t)R * N * p_bytes(mvk), 128);
-    a.off_tip = (int)off;
-    off = align_up(off + (size_t)4 * R * N * mv_bytes(ipk), 128);
-    a.off_sc = (int)off;
-    off = align_up(off + (size_t)R * 8 * 16, 128);
-    a.off_fl = (int)off;
-    off = align_up(off + (size_t)R * 4 * 4, 128);
-    if ((long)off + 1024 <= limit) {
-      a.G = G;
-      a.ldA = ldA;
-      a.smem_bytes = (int)off;
-      a.ws_gt = R * nb * nb / 2;
-      a.ws_ct = (R * N + 31) / 32 * 32 + 32;
-      const long ngroups = (a.T + R - 1) / R;
-      grid = (int)std::min<long>(ngroups, (long)sm_count() * env_int("FPM_CTAS_PER_SM", 1));
-      return true;
+  const int gt = R * nb * nb / 2;
+  // two CG groups (alternating hand-off slots) when the Gram side is two full
+  // warp groups: 512 threads = 256 Gram + 32 producer + 128 + 96 CG
+  const int ncg_env = env_int("FPM_WS_NCG", 0);
+  const int stage_list[] = {24, 20, 16, 12, 8, 4};
+  for (int ncg = (gt == 256 ? 2 : 1); ncg >= 1; --ncg) {
+    if (ncg_env && ncg != ncg_env) continue;
+    for (int si = 0; si < 6; ++si) {
+      const int stage_kb = env_int("FPM_STAGE_KB", 0) ? env_int("FPM_STAGE_KB", 0) : stage_list[si];
+      if (env_int("FPM_STAGE_KB", 0) && si > 0) break;
+      GramGeom G;
+      gram_geom(R, M, N, G, stage_kb);
+      G.S = std::max(3, G.S);  // the producer refills two chunks behind
+      const int ldA = lda_for(N, mv_bytes(mvk));
+      size_t off = 128;  // mbarriers
+      a.off_union = (int)off;  // H stage ring
+      off = align_up(off + (size_t)G.S * R * G.MC * G.Np * 16, 128);
+      a.off_ys = (int)off;
+      off = align_up(off + (size_t)2 * R * M * 16, 128);
+      sl.at = 0;
+      sl.b = (int)align_up((size_t)R * N * ldA * mv_bytes(mvk), 128);
+      sl.d = (int)align_up(sl.b + (size_t)R * N * 16, 128);
+      sl.bytes = (int)align_up(sl.d + (bj ? (size_t)R * N * Lb * 16 : 0), 128);
+      a.off_slot = (int)off;
+      off = align_up(off + (size_t)2 * sl.bytes, 128);
+      a.off_bsm = (int)off;  // matched-filter chain accumulators
+      off = align_up(off + (size_t)2 * R * N * 8, 128);
+      // ---- per-CG-group state (replicated ncg times, cg_stride apart) ----
+      const size_t cg0 = off;
+      a.off_minv = (int)off;
+      off = align_up(off + (bj ? (size_t)R * N * Lb * 16 : 0), 128);
+      a.off_vec = (int)off;
+      off = align_up(off + (size_t)8 * R * N * 16, 128);
+      // the inverse's scratch is dead before the CG vectors are initialised
+      if (!bj || Lb <= 8) {
+        a.off_scr2 = a.off_vec;
+      } else {
+        a.off_scr2 = (int)off;
+        off = align_up(off + (size_t)R * N * Lb * 16, 128);
+      }
+      a.off_pmv = (int)off;
+      off = align_up(off + (size_t)R * N * p_bytes(mvk), 128);
+      a.off_tip = (int)off;
+      off = align_up(off + (size_t)4 * R * N * mv_bytes(ipk), 128);
+      a.off_sc = (int)off;
+      off = align_up(off + (size_t)R * 8 * 16, 128);
+      a.off_fl = (int)off;
+      off = align_up(off + (size_t)R * 4 * 4, 128);
+      a.cg_stride = (int)(off - cg0);
+      off += (size_t)(ncg - 1) * a.cg_stride;
+      if ((long)off + 1024 <= limit) {
+        a.G = G;
+        a.ldA = ldA;
+        a.smem_bytes = (int)off;
+        a.ws_gt = gt;
+        a.ws_ct = gt == 256 ? 224 : (R * N + 31) / 32 * 32 + 32;
+        a.ws_ncg = ncg;
+        a.ws_ct0 = ncg == 2 ? 128 : a.ws_ct;
+        const long ngroups = (a.T + R - 1) / R;
+        grid = (int)std::min<long>(ngroups, (long)sm_count() * env_int("FPM_CTAS_PER_SM", 1));
+        return true;
+      }
     }
   }
   return false;

@@ -98,7 +98,7 @@ def main():
         out["cg"] = {"ms": ms, "det_s": T / ms * 1e3, "hbm_gbs": byts * T / (ms / 1e3) / 1e9,
                      "hbm_frac": byts * T / (ms / 1e3) / 6554.9e9}
     if a.wstrace:
-        tr = torch.zeros(96, dtype=torch.int64, device=dev)
+        tr = torch.zeros(160, dtype=torch.int64, device=dev)
         lib.fpm_debug_set_trace(tr.data_ptr())
         fused()
         torch.cuda.synchronize()
@@ -110,6 +110,18 @@ def main():
                                "w0_empty_wait": t[j*8+6], "w0_full_wait": t[j*8+7], "w1_full_wait": t[64+j]}
                               for j in range(8)]
         out["ws_warp_loopend_g2"] = [t[72 + w] - t[2*8+0] for w in range(12)]
+        c = t[96:160]
+        if c[60]:
+            ph = ["A:matvec", "B:phi/alpha", "C:axpy", "D:commit/z", "E:rho1/beta", "F:p"]
+            out["ws_cg_g2"] = {"bj": c[60] - t[2*8+4], "init": c[0] - c[60]}
+            prev = c[0]
+            for it in range(8):
+                for k in range(6):
+                    v = c[1 + it * 6 + k]
+                    if v:
+                        out["ws_cg_g2"].setdefault(ph[k], []).append(v - prev)
+                        prev = v
+            out["ws_cg_g2"]["B_owner_it1"] = {"start_after_A": c[50] - c[1], "chain": c[51] - c[50], "wdiv": c[52] - c[51], "to_barrier_release": c[2] - c[52]}
     if a.trace:
         tr = torch.zeros(64, dtype=torch.int64, device=dev)
         lib.fpm_debug_set_trace(tr.data_ptr())
