@@ -224,6 +224,70 @@ FPM_ROW_UNROLL
               ca = __dadd_rn(ca, __dadd_rn(__dmul_rn(h.x, y1), __dmul_rn(h.y, y2)));
             }
           }
+        } else if (active && FPM_GRAM_PIPE) {
+          // half-pair job, software-pipelined like the circulant loop above
+          const double2* py = sb + joff + job.y + nb * job.yo;
+          const double* yrow = reinterpret_cast<const double*>(ys + cq_yoff + m0);
+          const double* y1p = yrow + cq_part;
+          const double* y2p = yrow + (1 - cq_part);
+          const unsigned long long yneg = cq_part ? 0x8000000000000000ULL : 0ULL;
+          const double2* hcp = sb + cq_hoff;
+          double2 hx[4], hy[2], hz[4], hc = make_double2(0.0, 0.0);
+          double y1 = 0.0, y2 = 0.0;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) hx[u] = pa[nb * u];
+#pragma unroll
+          for (int w = 0; w < 2; ++w) hy[w] = py[nb * w];
+#pragma unroll
+          for (int v = 0; v < 4; ++v) hz[v] = pc[nb * v];
+          if (kChainInLoop) {
+            hc = hcp[0];
+            y1 = y1p[0];
+            y2 = y2p[0];
+          }
+#pragma unroll 1
+          for (int mm = 0; mm < rows; ++mm) {
+            const int mn = (mm + 1 < rows) ? mm + 1 : mm;
+            double2 nx[4], ny[2], nz[4], nhc = hc;
+            double ny1 = y1, ny2 = y2;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) nx[u] = pa[mn * Np + nb * u];
+#pragma unroll
+            for (int w = 0; w < 2; ++w) ny[w] = py[mn * Np + nb * w];
+#pragma unroll
+            for (int v = 0; v < 4; ++v) nz[v] = pc[mn * Np + nb * v];
+            if (kChainInLoop) {
+              nhc = hcp[mn * Np];
+              ny1 = y1p[2 * mn];
+              ny2 = y2p[2 * mn];
+            }
+            int p = 0;
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+              for (int v = u + 1; v < 4; ++v) cmac_conj(acc[p++], hx[u], hx[v]);
+            acc[14].x = __dadd_rn(acc[14].x, sqmag(hx[0]));
+            acc[14].y = __dadd_rn(acc[14].y, sqmag(hx[1]));
+            acc[15].x = __dadd_rn(acc[15].x, sqmag(hx[2]));
+            acc[15].y = __dadd_rn(acc[15].y, sqmag(hx[3]));
+#pragma unroll
+            for (int w = 0; w < 2; ++w)
+#pragma unroll
+              for (int v = 0; v < 4; ++v) cmac_conj(acc[6 + w * 4 + v], hy[w], hz[v]);
+            if (kChainInLoop) {
+              const double y2s = __longlong_as_double(__double_as_longlong(y2) ^ yneg);
+              ca = __dadd_rn(ca, __dadd_rn(__dmul_rn(hc.x, y1), __dmul_rn(hc.y, y2s)));
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) hx[u] = nx[u];
+#pragma unroll
+            for (int w = 0; w < 2; ++w) hy[w] = ny[w];
+#pragma unroll
+            for (int v = 0; v < 4; ++v) hz[v] = nz[v];
+            hc = nhc;
+            y1 = ny1;
+            y2 = ny2;
+          }
         } else if (active) {
           const double2* py = sb + joff + job.y + nb * job.yo;
 FPM_ROW_UNROLL
