@@ -100,6 +100,31 @@ int fpm_cg(const double* A, const double* b, const double* Minv, int64_t T, int3
            int32_t iters, const fpm_precision* prec, int32_t rho_update, double* x, int32_t* breakdown_at,
            int32_t* diverged_at, void* stream);
 
+/* Optional run_batch outputs (BatchResult, solvers.py:188-204; recorded at
+ * solvers.py:306-319, 371-386).  Every pointer may be NULL.  Layouts are the
+ * reference's, complex values as interleaved binary64 (re, im):
+ *   residual_norms, iterate_norms  (iters+1, T)  norm2 of r_i / x_i (linalg.py:122-134)
+ *   alphas, betas                  (iters, T)    complex; 0 where the reference records 0
+ *   converged_at                   (T,)          first i with ||r_i|| <= rtol*max(||b||, 1e-300), else -1
+ *   iterates, residual_vectors     (iters+1, T, N) complex (record_iterates / record_residual_vectors)
+ * b_norm is residual_norms[0].  Norms are within a few ulps of NumPy's (its
+ * hypot / pairwise sum), everything else is bit-identical. */
+typedef struct fpm_cg_history {
+  double* residual_norms;
+  double* iterate_norms;
+  double* alphas;
+  double* betas;
+  int32_t* converged_at;
+  double rtol;
+  double* iterates;
+  double* residual_vectors;
+} fpm_cg_history;
+
+/* fpm_cg plus the BatchResult histories (run_batch, solvers.py:262-393). */
+int fpm_cg_ex(const double* A, const double* b, const double* Minv, int64_t T, int32_t N, int32_t L,
+              int32_t iters, const fpm_precision* prec, int32_t rho_update, double* x, int32_t* breakdown_at,
+              int32_t* diverged_at, const fpm_cg_history* hist, void* stream);
+
 /* qam = 16 (reference) or 64 (extension).  tx_bits / rx_bits: (T, bits*N)
  * uint8 in the reference's layout, both nullable. */
 int fpm_slice_count(const double* x, const uint8_t* tx_bits, int64_t T, int32_t N, int32_t qam,

@@ -21,7 +21,7 @@ COUNTERS = ("bit_errors", "symbol_errors", "diverged", "breakdown", "trials", "n
 NCOUNTERS = 8
 
 # every symbol include/fpmimo_b200.h declares
-EXPORTS = ("fpm_version", "fpm_strerror", "fpm_limits", "fpm_gram", "fpm_bj_setup", "fpm_cg",
+EXPORTS = ("fpm_version", "fpm_strerror", "fpm_limits", "fpm_gram", "fpm_bj_setup", "fpm_cg", "fpm_cg_ex",
            "fpm_slice_count", "fpm_detect", "fpm_detect_host", "fpm_launch_count", "fpm_last_kernel", "fpm_probe_fp64",
            "fpm_debug_set_trace")
 
@@ -32,6 +32,13 @@ class Format(ctypes.Structure):
 
 class Precision(ctypes.Structure):
     _fields_ = [("work", Format), ("matvec", Format), ("inner", Format)]
+
+
+class CgHistory(ctypes.Structure):
+    """fpm_cg_history (include/fpmimo_b200.h): device pointers, NULL = skip."""
+    _fields_ = [("residual_norms", ctypes.c_void_p), ("iterate_norms", ctypes.c_void_p),
+                ("alphas", ctypes.c_void_p), ("betas", ctypes.c_void_p), ("converged_at", ctypes.c_void_p),
+                ("rtol", ctypes.c_double), ("iterates", ctypes.c_void_p), ("residual_vectors", ctypes.c_void_p)]
 
 
 _P = ctypes.c_void_p
@@ -47,6 +54,8 @@ _SIGS = {
     "fpm_bj_setup": (ctypes.c_int, [_P, _I64, _I32, _I32, _I32, _P, _P, _P]),
     "fpm_cg": (ctypes.c_int, [_P, _P, _P, _I64, _I32, _I32, _I32, ctypes.POINTER(Precision), _I32,
                               _P, _P, _P, _P]),
+    "fpm_cg_ex": (ctypes.c_int, [_P, _P, _P, _I64, _I32, _I32, _I32, ctypes.POINTER(Precision), _I32,
+                                 _P, _P, _P, ctypes.POINTER(CgHistory), _P]),
     "fpm_slice_count": (ctypes.c_int, [_P, _P, _I64, _I32, _I32, _P, _P, _P]),
     "fpm_detect": (ctypes.c_int, [_P, _P, _P, _I64, _I32, _I32, _D, _I32, _I32, _I32,
                                   ctypes.POINTER(Precision), _I32, _I32, _P, _P, _P, _P, _P, _P, _P]),

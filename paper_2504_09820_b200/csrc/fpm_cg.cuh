@@ -33,6 +33,21 @@
 
 namespace fpm {
 
+// run_batch history outputs (fpm_cg_history); null pointers are skipped
+struct CgHist {
+  double* res;    // (iters+1, T)
+  double* xn;     // (iters+1, T)
+  double2* al;    // (iters, T)
+  double2* be;    // (iters, T)
+  int* conv;      // (T,)
+  double rtol;
+  double2* xit;   // (iters+1, T, N)
+  double2* rit;   // (iters+1, T, N)
+  long T;         // leading stride of the histories
+  long t0;        // first realization of this CTA
+  int on;         // any output requested
+};
+
 template <int K>
 struct CgSmem {
   typedef typename Ar<K>::C C;
@@ -46,6 +61,7 @@ struct CgSmem {
   double2 *b, *x, *r, *p, *z, *w, *xn, *rn;  // R * N each (u_W values, binary64 carriers)
   double2* sc;            // R * 8 : 0 alpha, 1 beta, 3 rho0, 4 carry
   int* fl;                // R * 4 : live, nonfinite, breakdown_at, diverged_at
+  const CgHist* h = nullptr;  // run_batch histories (standalone CG kernel only)
 };
 
 // Owner of the sequential sums of slot g (which = 0: phi/rho1/carry,
@@ -201,6 +217,31 @@ __device__ __noinline__ double2 bj_row(const double2* minv, const double2* r, in
   return assemble(s.x, s.y);
 }
 
+// norm2 (linalg.py:122-134): scale = max|v_k| (NaN-propagating, 1 if not a
+// finite positive number), scale * sqrt(sum (|v_k|/scale)^2), inf if any
+// |v_k| is inf.  |v| is hypot; the sum runs left to right (NumPy's pairwise
+// sum and libm hypot may differ in the last bits).
+static __device__ __noinline__ double norm2_c(const double2* v, int n) {
+  double scale = 0.0;
+  bool nan = false, inf = false;
+#pragma unroll 1
+  for (int k = 0; k < n; ++k) {
+    const double m = hypot(v[k].x, v[k].y);
+    nan |= isnan(m);
+    inf |= isinf(m);
+    scale = m > scale ? m : scale;
+  }
+  if (nan || !isfinite(scale) || !(scale > 0.0)) scale = 1.0;
+  double s = 0.0;
+#pragma unroll 1
+  for (int k = 0; k < n; ++k) {
+    const double q = __ddiv_rn(hypot(v[k].x, v[k].y), scale);
+    s = __dadd_rn(s, __dmul_rn(q, q));
+  }
+  const double out = __dmul_rn(scale, __dsqrt_rn(s));
+  return inf ? __longlong_as_double(0x7ff0000000000000LL) : out;
+}
+
 // phase timestamps (diagnostic): thread 0 of CTA 0 writes clock64 values
 // (a volatile shared-memory read first forces the deferred-blocking barrier
 // to actually release before the clock is sampled)
@@ -299,8 +340,29 @@ __device__ void cg_group(CgSmem<K>& S, int Rv, int iters, bool bj, bool textbook
   }
   bar.sync();
   if (!rho_fresh && og >= 0 && ow == 0) S.sc[og * 8 + 4] = chain_sum<K>(S.tr1 + og * N, N, fi);
+  // ---- run_batch histories (solvers.py:306-319; standalone kernel only) ----
+  const CgHist* H = S.h;
+  double h_bn = 0.0, h_res = 0.0, h_xn = 0.0;
+  int h_conv = -1;
+  auto h_at = [&](int i, int g) -> long { return (long)i * H->T + H->t0 + g; };
+  if (H && og >= 0 && ow == 1) {
+    h_bn = h_res = norm2_c(S.r + og * N, N);
+    if (H->res) H->res[h_at(0, og)] = h_res;
+    if (H->xn) H->xn[h_at(0, og)] = 0.0;
+  }
+  auto h_rows = [&](int i) {  // iterates / residual vectors of sweep i, every row
+#pragma unroll 1
+    for (int k = 0; k < nrow; ++k) {
+      const int q = tid + k * nthreads;
+      const int g = q / N, row = q - g * N;
+      if (H->xit) H->xit[h_at(i, g) * N + row] = S.x[q];
+      if (H->rit) H->rit[h_at(i, g) * N + row] = S.r[q];
+    }
+  };
+  if (H) h_rows(0);
   bar.sync();
   FPM_STAMP(tr, 0);
+  int it_last = iters;
 
 #pragma unroll 1
   for (int it = 1; it <= iters; ++it) {
@@ -319,6 +381,7 @@ __device__ void cg_group(CgSmem<K>& S, int Rv, int iters, bool bj, bool textbook
     bar.sync();
     FPM_STAMP(tr, 1 + (it - 1) * 6 + 0);
     // ---- B: phi, flags, alpha ----
+    if (H && H->al && og >= 0 && ow == 0 && !S.fl[og * 4]) H->al[h_at(it - 1, og)] = make_double2(0.0, 0.0);
     if (og >= 0 && ow == 0 && S.fl[og * 4]) {
       const int g = og;
       if (tr && g == 0 && it <= 2) tr[50 + (it - 1) * 4] = clock64();
@@ -331,6 +394,8 @@ __device__ void cg_group(CgSmem<K>& S, int Rv, int iters, bool bj, bool textbook
       if (stall || phi.x <= 0.0) S.fl[g * 4] = 0;
       const double2 al = wdiv<WK>(rho0, phi, fw);
       S.sc[g * 8 + 0] = al;
+      // alphas[i-1] = alpha where active | newly_bad | broke (solvers.py:371)
+      if (H && H->al) H->al[h_at(it - 1, g)] = stall ? make_double2(0.0, 0.0) : al;
       if (tr && g == 0 && it <= 2) tr[52 + (it - 1) * 4] = clock64() + (al.x == 1.2345e300);
     }
     bar.sync();
@@ -372,20 +437,32 @@ __device__ void cg_group(CgSmem<K>& S, int Rv, int iters, bool bj, bool textbook
     bar.sync();
     FPM_STAMP(tr, 1 + (it - 1) * 6 + 3);
     // ---- E: rho1, beta, divergence flag ----
+    if (H && H->be && og >= 0 && ow == 0 && !S.fl[og * 4]) H->be[h_at(it - 1, og)] = make_double2(0.0, 0.0);
     if (og >= 0 && ow == 0 && S.fl[og * 4]) {
       const int g = og;
       if (S.fl[g * 4 + 1]) {  // non-finite update: diverged, frozen at the last finite iterate
         S.fl[g * 4 + 3] = it;
         S.fl[g * 4] = 0;
+        if (H && H->be) H->be[h_at(it - 1, g)] = make_double2(0.0, 0.0);
       } else {
         const double2 rho1 = chain_sum<K>(S.tr1 + g * N, N, fi);
-        S.sc[g * 8 + 1] = wdiv<WK>(rho1, S.sc[g * 8 + 3], fw);
+        const double2 be = wdiv<WK>(rho1, S.sc[g * 8 + 3], fw);
+        S.sc[g * 8 + 1] = be;
         S.sc[g * 8 + 4] = rho1;
+        if (H && H->be) H->be[h_at(it - 1, g)] = be;  // betas: where(active, beta, 0)
       }
+    }
+    if (H && og >= 0 && ow == 1) {  // res_hist[i], xn_hist[i] (solvers.py:373-374)
+      h_res = norm2_c(S.r + og * N, N);
+      h_xn = norm2_c(S.x + og * N, N);
+      if (H->res) H->res[h_at(it, og)] = h_res;
+      if (H->xn) H->xn[h_at(it, og)] = h_xn;
+      if (h_conv < 0 && h_res <= H->rtol * fmax(h_bn, 1e-300)) h_conv = it;
     }
     bar.sync();
     FPM_STAMP(tr, 1 + (it - 1) * 6 + 4);
     // ---- F: p = (z|r) + beta p ; pmv = rnd(p) ; next rho0 terms ----
+    if (H) h_rows(it);
     int any = 0;
 #pragma unroll 1
     for (int k = 0; k < nrow; ++k) {
@@ -401,9 +478,30 @@ __device__ void cg_group(CgSmem<K>& S, int Rv, int iters, bool bj, bool textbook
     }
     const int more = bar.any(any);
     FPM_STAMP(tr, 1 + (it - 1) * 6 + 5);
-    if (!more) break;
+    if (!more) {
+      it_last = it;
+      break;
+    }
   }
   bar.sync();
+  if (H) {
+    // every lane frozen early: the remaining sweeps record frozen values
+    // (alphas / betas 0, unchanged norms and vectors)
+#pragma unroll 1
+    for (int i = it_last + 1; i <= iters; ++i) {
+      if (og >= 0 && ow == 0) {
+        if (H->al) H->al[h_at(i - 1, og)] = make_double2(0.0, 0.0);
+        if (H->be) H->be[h_at(i - 1, og)] = make_double2(0.0, 0.0);
+      }
+      if (og >= 0 && ow == 1) {
+        if (H->res) H->res[h_at(i, og)] = h_res;
+        if (H->xn) H->xn[h_at(i, og)] = h_xn;
+      }
+      h_rows(i);
+    }
+    if (og >= 0 && ow == 1 && H->conv) H->conv[H->t0 + og] = h_conv;
+    bar.sync();
+  }
 }
 
 }  // namespace fpm

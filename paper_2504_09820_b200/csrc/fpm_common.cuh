@@ -6,6 +6,7 @@
 #include <stdint.h>
 
 #include "fpm_arith.cuh"
+#include "fpm_cg.cuh"
 #include "fpm_gram.cuh"
 
 namespace fpm {
@@ -60,6 +61,7 @@ struct CgArgs {
   int* brk;
   int* div;
   int off_minv, off_vec, off_pmv, off_tip, off_sc, off_fl;
+  CgHist h;
 };
 
 // Launchers (return FPM_* codes).  nb / lb: compile-time specialisation

@@ -310,6 +310,9 @@ __global__ void __launch_bounds__(256) fpm_cg_kernel(const CgArgs args) {
   }
 #pragma unroll 1
   for (int g = tid; g < args.R; g += nthreads) S.fl[g * 4] = g < Rv ? 1 : 0;
+  CgHist hh = args.h;  // run_batch histories (fpm_cg_ex)
+  hh.t0 = t0;
+  if (hh.on) S.h = &hh;
   __syncthreads();
   {
     CtaBar bar;

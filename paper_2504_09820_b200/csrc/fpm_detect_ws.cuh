@@ -30,10 +30,10 @@ struct WsLayout {  // byte offsets inside one hand-off slot
   int at, b, d, bytes;
 };
 
-// role order (FPM_WS_ORDER: 1 = CG warps first, default; 0 = Gram first)
+// role order (FPM_WS_ORDER: 0 = Gram warps first, default; 1 = CG first)
 inline int env_order() {
   const char* v = std::getenv("FPM_WS_ORDER");
-  return v ? (std::atoi(v) != 0) : 1;
+  return v ? (std::atoi(v) != 0) : 0;
 }
 
 // CG group width under the register split (FPM_WS_CT, default: all 224

@@ -687,9 +687,9 @@ int fpm_bj_setup(const double* A, int64_t T, int32_t N, int32_t L, int32_t allow
   return h_nonpd ? FPM_ENOTPD : FPM_OK;
 }
 
-int fpm_cg(const double* A, const double* b, const double* Minv, int64_t T, int32_t N, int32_t L, int32_t iters,
-           const fpm_precision* prec, int32_t rho_update, double* x, int32_t* breakdown_at,
-           int32_t* diverged_at, void* stream) {
+int fpm_cg_ex(const double* A, const double* b, const double* Minv, int64_t T, int32_t N, int32_t L, int32_t iters,
+              const fpm_precision* prec, int32_t rho_update, double* x, int32_t* breakdown_at,
+              int32_t* diverged_at, const fpm_cg_history* hist, void* stream) {
   if (T < 0 || N < 1 || !A || !b || !x || !breakdown_at || !diverged_at) return FPM_EINVAL;
   if (iters < 1) return FPM_EINVAL;                                                   // solvers.py:282-283
   if (rho_update != FPM_RHO_AS_WRITTEN && rho_update != FPM_RHO_TEXTBOOK) return FPM_EINVAL;  // :280-281
@@ -718,9 +718,27 @@ int fpm_cg(const double* A, const double* b, const double* Minv, int64_t T, int3
   a.brk = breakdown_at;
   a.div = diverged_at;
   a.tl = pick_tl(N);
+  if (hist) {
+    a.h.res = hist->residual_norms;
+    a.h.xn = hist->iterate_norms;
+    a.h.al = reinterpret_cast<double2*>(hist->alphas);
+    a.h.be = reinterpret_cast<double2*>(hist->betas);
+    a.h.conv = hist->converged_at;
+    a.h.rtol = hist->rtol;
+    a.h.xit = reinterpret_cast<double2*>(hist->iterates);
+    a.h.rit = reinterpret_cast<double2*>(hist->residual_vectors);
+    a.h.T = T;
+    a.h.on = a.h.res || a.h.xn || a.h.al || a.h.be || a.h.conv || a.h.xit || a.h.rit;
+  }
   int smem = 0;
   if (!plan_cg(N, a.L, bj, k.mv, k.ip, a, smem)) return FPM_EUNSUPPORTED;
   return launch_cg(k, a, smem, (cudaStream_t)stream);
+}
+
+int fpm_cg(const double* A, const double* b, const double* Minv, int64_t T, int32_t N, int32_t L, int32_t iters,
+           const fpm_precision* prec, int32_t rho_update, double* x, int32_t* breakdown_at,
+           int32_t* diverged_at, void* stream) {
+  return fpm_cg_ex(A, b, Minv, T, N, L, iters, prec, rho_update, x, breakdown_at, diverged_at, nullptr, stream);
 }
 
 int fpm_slice_count(const double* x, const uint8_t* tx_bits, int64_t T, int32_t N, int32_t qam,

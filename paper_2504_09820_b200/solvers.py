@@ -63,6 +63,9 @@ class BatchResult:
     betas: object = None
     b_norm: object = None
     converged_at: object = None
+    residual_gaps: object = None      # (iters+1, T) record_gaps
+    iterates: object = None           # (iters+1, T, N) record_iterates
+    residual_vectors: object = None   # (iters+1, T, N) record_residual_vectors
 
 
 class BatchBlocks:
@@ -165,14 +168,31 @@ def build_blocks_batch(A, L: int, *, allow_ragged: bool = False) -> BatchBlocks:
     return BatchBlocks(_out(packed, host), N, L)
 
 
+def _norm2_t(v):
+    """norm2 over the trailing axis (linalg.py:122-134) on the device:
+    scale = max|v| (NaN-propagating, 1 unless finite and > 0), inf if any |v|
+    is inf."""
+    torch = _torch()
+    mags = torch.abs(v)
+    scale = mags.amax(-1) if mags.shape[-1] else torch.zeros(mags.shape[:-1], dtype=mags.dtype, device=mags.device)
+    scale = torch.where(torch.isfinite(scale) & (scale > 0), scale, torch.ones_like(scale))
+    sc = mags / scale[..., None]
+    out = scale * torch.sqrt((sc * sc).sum(-1))
+    return torch.where(torch.isinf(mags).any(-1), torch.full_like(out, float("inf")), out)
+
+
 def run_batch(A, b, max_iters: int, prec: PrecisionConfig | None = None, blocks=None, *,
-              rho_update: str = "as_written", rtol: float = 1e-6, **unsupported) -> BatchResult:
+              rho_update: str = "as_written", rtol: float = 1e-6, x_ref=None, a_norm=None,
+              record_gaps: bool = False, record_iterates: bool = False,
+              record_residual_vectors: bool = False) -> BatchResult:
     """Lockstep mixed-precision (BJ-)CG on the GPU (solvers.py:262-393).
 
     `blocks` may be a BatchBlocks, or anything with a `.mats` list of
-    (T, Lk, Lk) arrays (the reference's _BatchBlocks).  Returns x and the
-    breakdown/diverged flags bit-identical to the reference; the optional
-    history recording of the reference is not produced.
+    (T, Lk, Lk) arrays (the reference's _BatchBlocks).  Returns the
+    reference's BatchResult: x, breakdown_at, diverged_at, alphas, betas and
+    the record_iterates / record_residual_vectors outputs bit-identical;
+    residual / iterate norms and gaps within a few ulps (norm2's hypot and
+    summation order).  NumPy in -> NumPy out; CUDA tensors -> CUDA tensors.
     """
     torch = _torch()
     if prec is None:
@@ -181,8 +201,8 @@ def run_batch(A, b, max_iters: int, prec: PrecisionConfig | None = None, blocks=
         raise ContractViolation(f"unknown rho_update variant {rho_update!r}")
     if max_iters < 1:
         raise ContractViolation("max_iters must be at least 1")
-    if any(unsupported.get(k) for k in ("record_gaps", "record_iterates", "record_residual_vectors")):
-        raise NotImplementedError("history recording is not part of the GPU hot path")
+    if record_gaps and x_ref is None:
+        raise ContractViolation("gap recording needs a reference solution")
     host = not _is_torch(b)
     Ad = _to_dev(A, torch.complex128)
     bd = _to_dev(b, torch.complex128)
@@ -197,14 +217,46 @@ def run_batch(A, b, max_iters: int, prec: PrecisionConfig | None = None, blocks=
             L = mats[0].shape[-1]
             packed = pack_blocks([np.asarray(m) for m in mats], N, L)
         minv = _to_dev(packed, torch.complex128)
-    x = torch.empty((T, N), dtype=torch.complex128, device=bd.device)
-    brk = torch.empty((T,), dtype=torch.int32, device=bd.device)
-    div = torch.empty((T,), dtype=torch.int32, device=bd.device)
+    dev = bd.device
+    it1 = max_iters + 1
+    x = torch.empty((T, N), dtype=torch.complex128, device=dev)
+    brk = torch.empty((T,), dtype=torch.int32, device=dev)
+    div = torch.empty((T,), dtype=torch.int32, device=dev)
+    res = torch.empty((it1, T), dtype=torch.float64, device=dev)
+    xnh = torch.empty((it1, T), dtype=torch.float64, device=dev)
+    alphas = torch.empty((max_iters, T), dtype=torch.complex128, device=dev)
+    betas = torch.empty((max_iters, T), dtype=torch.complex128, device=dev)
+    conv = torch.empty((T,), dtype=torch.int32, device=dev)
+    need_vec = record_iterates or record_gaps
+    xit = torch.empty((it1, T, N), dtype=torch.complex128, device=dev) if need_vec else None
+    rit = torch.empty((it1, T, N), dtype=torch.complex128, device=dev) \
+        if (record_residual_vectors or record_gaps) else None
+    hist = _lib.CgHistory(res.data_ptr(), xnh.data_ptr(), alphas.data_ptr(), betas.data_ptr(), conv.data_ptr(),
+                          float(rtol), None if xit is None else xit.data_ptr(),
+                          None if rit is None else rit.data_ptr())
     lib = _lib.load()
     ps = _lib.precision_struct(prec)
-    rc = lib.fpm_cg(Ad.data_ptr(), bd.data_ptr(), None if minv is None else minv.data_ptr(), T, N, L,
-                    int(max_iters), ps, _lib.FPM_RHO[rho_update], x.data_ptr(), brk.data_ptr(),
-                    div.data_ptr(), _stream())
+    rc = lib.fpm_cg_ex(Ad.data_ptr(), bd.data_ptr(), None if minv is None else minv.data_ptr(), T, N, L,
+                       int(max_iters), ps, _lib.FPM_RHO[rho_update], x.data_ptr(), brk.data_ptr(),
+                       div.data_ptr(), hist, _stream())
     _lib.check(rc, "run_batch")
-    return BatchResult(x=_out(x, host), breakdown_at=_out(brk.to(torch.int64), host),
-                       diverged_at=_out(div.to(torch.int64), host), iterations_run=int(max_iters))
+    gaps = None
+    if record_gaps:  # solvers.py:289-294, 375-377: ||b - A x_i - r_i|| / (||A|| ||x_ref||)
+        xr = _to_dev(x_ref, torch.complex128)
+        if a_norm is None:
+            w = torch.linalg.eigvalsh(Ad)
+            an = torch.maximum(w[:, 0].abs(), w[:, -1].abs())
+        else:
+            an = _to_dev(np.asarray(a_norm, np.float64) if not _is_torch(a_norm) else a_norm, torch.float64)
+        scale = an * _norm2_t(xr)
+        gaps = torch.zeros((it1, T), dtype=torch.float64, device=dev)
+        for i in range(1, it1):
+            true_res = bd - torch.einsum("tij,tj->ti", Ad, xit[i]) - rit[i]
+            gaps[i] = _norm2_t(true_res) / scale
+    return BatchResult(
+        x=_out(x, host), breakdown_at=_out(brk.to(torch.int64), host), diverged_at=_out(div.to(torch.int64), host),
+        iterations_run=int(max_iters), residual_norms=_out(res, host), iterate_norms=_out(xnh, host),
+        alphas=_out(alphas, host), betas=_out(betas, host), b_norm=_out(res[0].clone(), host),
+        converged_at=_out(conv.to(torch.int64), host), residual_gaps=None if gaps is None else _out(gaps, host),
+        iterates=_out(xit, host) if record_iterates else None,
+        residual_vectors=_out(rit, host) if record_residual_vectors else None)

@@ -130,6 +130,38 @@ def _kernel_kats():
     return out
 
 
+def _cg_history():
+    """run_batch's full BatchResult (solvers.py:188-204, 306-393): residual /
+    iterate norm histories, alphas, betas, b_norm, converged_at and the
+    record_iterates / record_residual_vectors / record_gaps outputs, on the
+    crafted flag systems (breakdown, stall, divergence lanes) and on a c5
+    block-Jacobi batch."""
+    e = _solver_edge_cases()
+    A, b = e["A"], e["b"]
+    out = {"edge_A": A, "edge_b": b}
+    x_ref = np.linalg.solve(A, b[..., None])[..., 0]
+    for tag, prec in (("fp16", PrecisionConfig(matvec=get_format("fp16"), inner=get_format("fp16"))),
+                      ("fp64", PrecisionConfig())):
+        res = run_batch(A, b, 6, prec, x_ref=x_ref, record_gaps=True, record_iterates=True,
+                        record_residual_vectors=True, rtol=1e-3)
+        for k in ("x", "residual_norms", "iterate_norms", "alphas", "betas", "b_norm", "converged_at",
+                  "breakdown_at", "diverged_at", "residual_gaps", "iterates", "residual_vectors"):
+            out[f"edge_{tag}_{k}"] = getattr(res, k)
+    out["edge_x_ref"] = x_ref
+    d = _detector_case("c5_hist", 128, 64, 0.5, 15.0, 4,
+                       dict(algorithm="fp_bj_cg", iters=8, L=4, matvec="fp16", inner="fp16"))
+    A5, b5 = d["A"], d["b"]
+    blocks = build_blocks_batch(A5, 4)
+    res = run_batch(A5, b5, 8, PrecisionConfig(matvec=get_format("fp16"), inner=get_format("fp16")), blocks=blocks,
+                    record_iterates=True, record_residual_vectors=True, rtol=1e-2)
+    out["c5_A"], out["c5_b"] = A5, b5
+    out["c5_Minv"] = np.concatenate([m.reshape(4, -1) for m in blocks.mats], axis=1)
+    for k in ("x", "residual_norms", "iterate_norms", "alphas", "betas", "b_norm", "converged_at",
+              "iterates", "residual_vectors"):
+        out[f"c5_{k}"] = getattr(res, k)
+    return out
+
+
 def main():
     for name, (M, K, zeta, snr, T, kw) in CASES.items():
         d = _detector_case(name, M, K, zeta, snr, T, kw)
@@ -138,6 +170,7 @@ def main():
               "diverged", int((d["diverged_at"] >= 0).sum()))
     np.savez_compressed(os.path.join(OUT, "solver_edges.npz"), **_solver_edge_cases())
     np.savez_compressed(os.path.join(OUT, "kernel_kats.npz"), **_kernel_kats())
+    np.savez_compressed(os.path.join(OUT, "hist_cg.npz"), **_cg_history())
     # slicer known answers (detect.py:70-84, tests/test_detect.py:55-69)
     vals = np.array([complex(np.nan, 1.0), complex(np.inf, np.inf), complex(-np.inf, -np.inf),
                      -2 / np.sqrt(10), 0.0, 2 / np.sqrt(10), complex(0.3, -0.9), complex(-0.0, 0.0)])

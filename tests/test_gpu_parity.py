@@ -39,6 +39,11 @@ def _spec_from_golden(g):
                         rho_update=str(g["rho_update"]))
 
 
+# norm2 (linalg.py:122-134) runs through hypot and a pairwise sum in NumPy,
+# through CUDA hypot and a sequential sum here: a few ulps apart
+NORM_RTOL = 1e-14
+
+
 def _prec_tol(g):
     sig = int(g["fmts"][1][0])          # matvec significand bits incl. hidden
     return 1e-12 if sig == 53 else 2.0 ** -(sig - 1 - 2)
@@ -93,6 +98,9 @@ def test_run_batch_bit_exact(name):
     assert bits_equal(res.x, g["x"])
     np.testing.assert_array_equal(res.breakdown_at, g["breakdown_at"])
     np.testing.assert_array_equal(res.diverged_at, g["diverged_at"])
+    # norm histories: NumPy's hypot / pairwise sum vs a sequential sum
+    np.testing.assert_allclose(res.residual_norms, g["residual_norms"], rtol=NORM_RTOL, atol=0)
+    np.testing.assert_array_equal(res.converged_at, g["converged_at"])
 
 
 @pytest.mark.parametrize("name", [n for n in golden_cases() if "bj" in n])
@@ -267,3 +275,53 @@ def test_persistent_kernel_multi_group_and_partial_group():
     finally:
         del os.environ["FPM_NO_WS"]
     assert bits_equal(res2.x, ref.x)
+
+
+HIST_EXACT = ("x", "breakdown_at", "diverged_at", "alphas", "betas", "converged_at", "iterates", "residual_vectors")
+HIST_NORMS = ("residual_norms", "iterate_norms", "b_norm")
+
+
+def _check_history(res, want, tag):
+    for k in HIST_EXACT:
+        got, w = getattr(res, k), want[k]
+        assert got is not None, (tag, k)
+        assert bits_equal(np.asarray(got, w.dtype), w), (tag, k)
+    for k in HIST_NORMS:
+        np.testing.assert_allclose(getattr(res, k), want[k], rtol=NORM_RTOL, atol=0, err_msg=f"{tag} {k}")
+
+
+def test_run_batch_histories_match_reference():
+    """Full BatchResult (solvers.py:188-204, 306-393) against the reference's
+    own run_batch on the flag systems (breakdown / stall / divergence lanes,
+    with record_iterates / record_residual_vectors / record_gaps) and on a
+    c5 block-Jacobi batch."""
+    from paper_2504_09820_b200.formats import get_format
+    from paper_2504_09820_b200.solvers import BatchBlocks, PrecisionConfig, run_batch
+    g = load_golden("hist_cg")
+    for tag, prec in (("fp16", PrecisionConfig(matvec=get_format("fp16"), inner=get_format("fp16"))),
+                      ("fp64", PrecisionConfig())):
+        res = run_batch(g["edge_A"], g["edge_b"], 6, prec, x_ref=g["edge_x_ref"], record_gaps=True,
+                        record_iterates=True, record_residual_vectors=True, rtol=1e-3)
+        want = {k: g[f"edge_{tag}_{k}"] for k in HIST_EXACT + HIST_NORMS + ("residual_gaps",)}
+        _check_history(res, want, tag)
+        # gaps: a difference of nearly equal fp64 quantities through cuBLAS vs einsum
+        np.testing.assert_allclose(res.residual_gaps, want["residual_gaps"], rtol=1e-6, atol=1e-13)
+    prec = PrecisionConfig(matvec=get_format("fp16"), inner=get_format("fp16"))
+    res = run_batch(g["c5_A"], g["c5_b"], 8, prec, BatchBlocks(g["c5_Minv"], 64, 4), record_iterates=True,
+                    record_residual_vectors=True, rtol=1e-2)
+    _check_history(res, {k: g[f"c5_{k}"] for k in HIST_EXACT if k not in ("breakdown_at", "diverged_at")}
+                   | {k: g[f"c5_{k}"] for k in HIST_NORMS} | {"breakdown_at": np.full(4, -1), "diverged_at":
+                                                             np.full(4, -1)}, "c5")
+
+
+def test_run_batch_histories_all_lanes_frozen_early(oracle):
+    """Every lane frozen after sweep 1 (breakdown + stall): the kernel exits
+    early and must still record the remaining sweeps as the reference does
+    (frozen norms and vectors, zero alphas / betas)."""
+    from paper_2504_09820_b200.solvers import PrecisionConfig, run_batch
+    O = oracle
+    g = load_golden("hist_cg")
+    A, b = g["edge_A"][1:3], g["edge_b"][1:3]
+    res = run_batch(A, b, 6, PrecisionConfig(), record_iterates=True, record_residual_vectors=True)
+    want = O.cg_batch(A, b, 6, record=True)
+    _check_history(res, {k: getattr(want, k) for k in HIST_EXACT + HIST_NORMS}, "frozen")

@@ -123,3 +123,27 @@ def test_fast_paths_equal_restatement(oracle):
     a1, b1 = oracle.gram_mf(H, y, 0.03)
     a2, b2 = oracle.gram_mf_einsum(H, y, 0.03)
     assert bits_equal(a1, a2) and bits_equal(b1, b2)
+
+
+HIST_KEYS = ("x", "residual_norms", "iterate_norms", "alphas", "betas", "b_norm", "converged_at",
+             "iterates", "residual_vectors")
+
+
+def test_cg_histories_bit_exact(oracle):
+    """The oracle's BatchResult histories (solvers.py:306-393) equal the
+    reference's on the flag systems (breakdown / stall / divergence lanes)
+    and on a c5 block-Jacobi batch, including the record_* outputs."""
+    O = oracle
+    g = load_golden("hist_cg")
+    for tag, (mv, ip) in (("fp16", (O.FP16, O.FP16)), ("fp64", (O.FP64, O.FP64))):
+        out = O.cg_batch(g["edge_A"], g["edge_b"], 6, O.FP64, mv, ip, None, rtol=1e-3, x_ref=g["edge_x_ref"],
+                         record=True)
+        for k in HIST_KEYS + ("breakdown_at", "diverged_at", "residual_gaps"):
+            got, want = getattr(out, k), g[f"edge_{tag}_{k}"]
+            assert bits_equal(np.asarray(got, want.dtype), want), (tag, k)
+    mats = O.unpack_blocks(g["c5_Minv"], 64, 4) if hasattr(O, "unpack_blocks") else \
+        [g["c5_Minv"][:, k * 16:(k + 1) * 16].reshape(-1, 4, 4) for k in range(16)]
+    out = O.cg_batch(g["c5_A"], g["c5_b"], 8, O.FP64, O.FP16, O.FP16, mats, rtol=1e-2, record=True)
+    for k in HIST_KEYS:
+        got, want = getattr(out, k), g[f"c5_{k}"]
+        assert bits_equal(np.asarray(got, want.dtype), want), k
