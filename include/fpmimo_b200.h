@@ -153,7 +153,7 @@ int64_t fpm_launch_count(void);
 
 /* Name and specialisation of the last fused detector kernel this library
  * launched ("" before the first fpm_detect / fpm_detect_host call); for
- * benchmark / profile reports.  Not thread-safe across host threads. */
+ * benchmark / profile reports; kept per calling host thread. */
 const char* fpm_last_kernel(void);
 
 /* Diagnostic: measured rate of non-fused fp64 DMUL/DADD operations per

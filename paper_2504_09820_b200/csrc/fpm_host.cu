@@ -260,16 +260,11 @@ static int mv_bytes(int kind) {
 
 static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
-static int max_smem_optin() {
-  static int v = -1;
-  if (v < 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    int s = 0;
-    if (cudaDeviceGetAttribute(&s, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess || s <= 0)
-      s = 227 * 1024;
-    v = s;
-  }
+static int max_smem_optin() {  // per call: re-entrant, follows the caller's current device
+  int dev = 0, v = 0;
+  cudaGetDevice(&dev);
+  if (cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess || v <= 0)
+    v = 227 * 1024;
   return v;
 }
 
@@ -377,12 +372,9 @@ static bool plan_cg(int N, int L, int bj, int mvk, int ipk, CgArgs& a, int& smem
 // Specialisations the per-kind units provide (nb = N/4, lb = L): see
 // fpm_inst_<kind>.cu.  Anything else runs the kind's generic instance.
 static int sm_count() {
-  static int v = -1;
-  if (v < 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
-  }
+  int dev = 0, v = 0;
+  cudaGetDevice(&dev);
+  if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
   return v;
 }
 
@@ -487,7 +479,7 @@ static void pick_spec(int N, int L, int bj, int& nb, int& lb) {
   if (bj && nb && (nb % L)) nb = 0;
 }
 
-static char g_last_kernel[96] = "";
+static thread_local char g_last_kernel[96] = "";  // per calling thread (re-entrant)
 
 static const char* kind_name(int k) {
   switch (k) {

@@ -325,3 +325,37 @@ def test_run_batch_histories_all_lanes_frozen_early(oracle):
     res = run_batch(A, b, 6, PrecisionConfig(), record_iterates=True, record_residual_vectors=True)
     want = O.cg_batch(A, b, 6, record=True)
     _check_history(res, {k: getattr(want, k) for k in HIST_EXACT + HIST_NORMS}, "frozen")
+
+
+def test_detect_batch_reentrant_from_threads(oracle):
+    """The boundary may be called concurrently (experiments.py:257-261 runs
+    detectors in a ThreadPoolExecutor): per-call streams and buffers, no
+    shared mutable state -> identical results to sequential calls."""
+    from concurrent.futures import ThreadPoolExecutor
+    from paper_2504_09820_b200.detect import DetectorSpec, _detect_batch
+    dets = [DetectorSpec("fp_bj_cg", iters=6, L=4, matvec="fp16", inner="fp16"),
+            DetectorSpec("fp_cg", iters=5, matvec="bfloat16", inner="bfloat16"), DetectorSpec("cg", iters=4)]
+    jobs = []
+    for s in range(6):
+        H, y, bits, s2 = oracle.simulate(64, 32, 0.5, 10.0, range(s * 24, s * 24 + 24), 11)
+        jobs.append((dets[s % 3], {"H": H, "H_est": H, "y": y, "bits": bits, "sigma_n2": s2}))
+    seq = [_detect_batch(d, b) for d, b in jobs]
+    with ThreadPoolExecutor(4) as ex:
+        par = list(ex.map(lambda j: _detect_batch(*j), jobs))
+    for (x1, d1), (x2, d2) in zip(seq, par):
+        assert bits_equal(x1, x2)
+        np.testing.assert_array_equal(d1, d2)
+
+
+def test_install_patches_reference_style_module():
+    """install() swaps `_detect_batch` into a module the way run_ber_sweep
+    looks it up (detect.py:259) and uninstall() restores it."""
+    import types
+    from paper_2504_09820_b200 import detect as D
+    mod = types.ModuleType("fake_fpmimo_detect")
+    sentinel = object()
+    mod._detect_batch = sentinel
+    prev = D.install(mod)
+    assert prev is sentinel and mod._detect_batch is D._detect_batch
+    D.uninstall(mod)
+    assert mod._detect_batch is sentinel
