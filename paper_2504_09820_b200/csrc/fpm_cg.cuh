@@ -202,6 +202,67 @@ __device__ __noinline__ typename Ar<K>::C mv_row(const typename Ar<K>::C* row, c
   return A::asmc(s);
 }
 
+// Compile-time N (NC > 0): the whole sum is one basic block, so the
+// scheduler overlaps every load and product with the dependent add chain
+// (the loop versions above issue in order: a block's adds stall the next
+// block's loads / products).
+template <int K, int NC>
+__device__ __noinline__ double2 chain_sum_n(const typename Ar<K>::C* t, const FmtP& f) {
+  typedef Ar<K> A;
+  typedef typename A::C C;
+  constexpr int n16 = V16<C>::n;
+  if constexpr (NC % n16 == 0 && NC * sizeof(C) <= 256) {
+    C v[NC];
+#pragma unroll
+    for (int i = 0; i < NC / n16; ++i) V16<C>::ld(t + i * n16, v + i * n16);
+    C s = v[0];
+#pragma unroll
+    for (int j = 1; j < NC; ++j) s = A::add(s, v[j], f);
+    return A::wide(A::asmc(s));
+  } else {
+    return chain_sum<K>(t, NC, f);
+  }
+}
+
+template <int K, int NC>
+__device__ __noinline__ typename Ar<K>::C mv_row_n(const typename Ar<K>::C* row, const typename Ar<K>::P* pv,
+                                                 const FmtP& f) {
+  typedef Ar<K> A;
+  typedef typename A::C C;
+  typedef typename A::P P;
+  constexpr int B = sizeof(C) >= 16 ? 2 : (sizeof(C) >= 8 ? 4 : 8);
+  if constexpr (NC % B == 0 && NC * sizeof(C) <= 256) {
+    C s;
+#pragma unroll
+    for (int k = 0; k < NC; k += B) {
+      C a[B];
+      P p[B];
+      ld_blk<B>(row + k, a);
+      ld_blk<B>(pv + k, p);
+#pragma unroll
+      for (int j = 0; j < B; ++j) {
+        const C t = A::mulp(a[j], p[j], f);
+        s = (k + j == 0) ? t : A::add(s, t, f);
+      }
+    }
+    return A::asmc(s);
+  } else {
+    return mv_row<K>(row, pv, NC, f);
+  }
+}
+
+// row jl of block-diagonal apply from the block's r values already in
+// registers (rl[0..LB-1], on the u_W grid): same operations as bj_row
+template <int WK, int LB>
+__device__ __forceinline__ double2 bj_row_reg(const double2* Mblk, const double2 (&rl)[LB], int jl, const FmtP& w) {
+  typedef Ar<WK> A;
+  const double2* M = Mblk + jl;  // column-major block
+  double2 s = A::mul(M[0], rl[0], w);
+#pragma unroll
+  for (int l = 1; l < LB; ++l) s = A::add(s, A::mul(M[l * LB], rl[l], w), w);
+  return assemble(s.x, s.y);
+}
+
 // one row of the block-diagonal apply M r (solvers.py:222-225) at u_W
 template <int WK, int LB>
 __device__ __noinline__ double2 bj_row(const double2* minv, const double2* r, int j, int L_rt, int N, const FmtP& w) {
@@ -284,17 +345,25 @@ struct NamedBar {
 // the group; each realization's sequential sums run in an "owner" thread,
 // placed past the row threads when the group has spare lanes.  bar.sync()
 // is the group barrier, bar.any(v) a barrier that ORs v over the group.
-template <int WK, int K, int LB, class Bar>
+//
+// Five group barriers per sweep: A (matvec, phi terms) | B (phi, alpha) |
+// C (x, r updates + z = M r + rho1 terms, each thread recomputing the r
+// updates of its own diagonal block so z needs no extra barrier) | E (rho1,
+// beta, divergence) | F (commit x, r; p update).  NC > 0: N known at
+// compile time (fully unrolled sums).  Ragged blocks (LB == 0 with BJ)
+// take one more barrier between the r updates and z.
+template <int WK, int K, int LB, int NC = 0, class Bar>
 __device__ void cg_group(CgSmem<K>& S, int Rv, int iters, bool bj, bool textbook, const Prec& pr, int nthreads,
                          int tid, Bar& bar, long long* tr = nullptr) {
   typedef Ar<K> A;
   typedef typename A::C C;
-  const int N = S.N;
+  const int N = NC > 0 ? NC : S.N;
   const int RN = Rv * N;
   const FmtP& fw = pr.work;
   const FmtP& fm = pr.mv;
   const FmtP& fi = pr.ip;
   const bool rho_fresh = bj && !textbook;  // as_written: rho0 = r^H p every sweep
+  const bool merged = !bj || LB > 0;       // z from registers (no barrier between r and z)
   // roles, once
   const int nrow = RN > tid ? (RN - tid + nthreads - 1) / nthreads : 0;
   int og = -1, ow = 0;
@@ -307,6 +376,10 @@ __device__ void cg_group(CgSmem<K>& S, int Rv, int iters, bool bj, bool textbook
   // (native kinds: u_IP == u_MV, so the matvec's rounding of p is reused)
   auto ipr = [&](double2 v) -> C { return A::rnd(v, fi); };
   auto mv_to_ip = [&](C v) -> C { return K == FK_GEN ? A::rnd(A::wide(v), fi) : v; };
+  auto csum = [&](const C* t) -> double2 {
+    if constexpr (NC > 0) return chain_sum_n<K, NC>(t, fi);
+    else return chain_sum<K>(t, N, fi);
+  };
 
   // ---- init (solvers.py:297-328) ----
 #pragma unroll 1
@@ -339,17 +412,12 @@ __device__ void cg_group(CgSmem<K>& S, int Rv, int iters, bool bj, bool textbook
     if (rho_fresh) S.trho[q] = A::mulc(ri, pi, fi);
   }
   bar.sync();
-  if (!rho_fresh && og >= 0 && ow == 0) S.sc[og * 8 + 4] = chain_sum<K>(S.tr1 + og * N, N, fi);
+  if (!rho_fresh && og >= 0 && ow == 0) S.sc[og * 8 + 4] = csum(S.tr1 + og * N);
   // ---- run_batch histories (solvers.py:306-319; standalone kernel only) ----
   const CgHist* H = S.h;
   double h_bn = 0.0, h_res = 0.0, h_xn = 0.0;
   int h_conv = -1;
   auto h_at = [&](int i, int g) -> long { return (long)i * H->T + H->t0 + g; };
-  if (H && og >= 0 && ow == 1) {
-    h_bn = h_res = norm2_c(S.r + og * N, N);
-    if (H->res) H->res[h_at(0, og)] = h_res;
-    if (H->xn) H->xn[h_at(0, og)] = 0.0;
-  }
   auto h_rows = [&](int i) {  // iterates / residual vectors of sweep i, every row
 #pragma unroll 1
     for (int k = 0; k < nrow; ++k) {
@@ -359,7 +427,18 @@ __device__ void cg_group(CgSmem<K>& S, int Rv, int iters, bool bj, bool textbook
       if (H->rit) H->rit[h_at(i, g) * N + row] = S.r[q];
     }
   };
-  if (H) h_rows(0);
+  auto h_norms = [&](int i) {  // res_hist[i], xn_hist[i] (solvers.py:373-374)
+    h_res = norm2_c(S.r + og * N, N);
+    h_xn = i ? norm2_c(S.x + og * N, N) : 0.0;
+    if (i == 0) h_bn = h_res;
+    if (H->res) H->res[h_at(i, og)] = h_res;
+    if (H->xn) H->xn[h_at(i, og)] = h_xn;
+    if (i > 0 && h_conv < 0 && h_res <= H->rtol * fmax(h_bn, 1e-300)) h_conv = i;
+  };
+  if (H) {
+    if (og >= 0 && ow == 1) h_norms(0);
+    h_rows(0);
+  }
   bar.sync();
   FPM_STAMP(tr, 0);
   int it_last = iters;
@@ -372,70 +451,93 @@ __device__ void cg_group(CgSmem<K>& S, int Rv, int iters, bool bj, bool textbook
       const int q = tid + k * nthreads;
       const int g = q / N, i = q - g * N;
       if (!S.fl[g * 4]) continue;
-      const C wc = mv_row<K>(S.At + (g * N + i) * S.ldA, S.pmv + g * N, N, fm);
+      if (tr && tid == 0 && it == 2) tr[75] = clock64();
+      C wc;
+      if constexpr (NC > 0) wc = mv_row_n<K, NC>(S.At + (g * N + i) * S.ldA, S.pmv + g * N, fm);
+      else wc = mv_row<K>(S.At + (g * N + i) * S.ldA, S.pmv + g * N, N, fm);
+      if (tr && tid == 0 && it == 2) tr[76] = clock64() + (h2u(*reinterpret_cast<__half2*>(&wc)) == 12345u);
       S.w[q] = A::wide(wc);
       const C pi = K == FK_GEN ? ipr(S.p[q]) : A::rnd(S.p[q], fm);
       S.tphi[q] = A::mulc(pi, mv_to_ip(wc), fi);
+      if (tr && tid == 0 && it == 2) tr[77] = clock64() + (S.w[q].x == 1.234e300);
     }
-    if (rho_fresh && og >= 0 && ow == 1 && S.fl[og * 4]) S.sc[og * 8 + 3] = chain_sum<K>(S.trho + og * N, N, fi);
+    if (rho_fresh && og >= 0 && ow == 1 && S.fl[og * 4]) S.sc[og * 8 + 3] = csum(S.trho + og * N);
     bar.sync();
     FPM_STAMP(tr, 1 + (it - 1) * 6 + 0);
     // ---- B: phi, flags, alpha ----
     if (H && H->al && og >= 0 && ow == 0 && !S.fl[og * 4]) H->al[h_at(it - 1, og)] = make_double2(0.0, 0.0);
     if (og >= 0 && ow == 0 && S.fl[og * 4]) {
       const int g = og;
-      if (tr && g == 0 && it <= 2) tr[50 + (it - 1) * 4] = clock64();
-      const double2 phi = chain_sum<K>(S.tphi + g * N, N, fi);
-      if (tr && g == 0 && it <= 2) tr[51 + (it - 1) * 4] = clock64() + (phi.x == 1.2345e300);
+      const bool st = tr && g == 0 && it == 2;
+      if (st) tr[78] = clock64();
+      const double2 phi = csum(S.tphi + g * N);
+      if (st) tr[79] = clock64() + (phi.x == 1.234e300);
       const double2 rho0 = rho_fresh ? S.sc[g * 8 + 3] : S.sc[g * 8 + 4];
       S.sc[g * 8 + 3] = rho0;
       const bool stall = (rho0.x == 0.0) && (rho0.y == 0.0);
       if (!stall && phi.x <= 0.0) S.fl[g * 4 + 2] = it;  // breakdown
       if (stall || phi.x <= 0.0) S.fl[g * 4] = 0;
       const double2 al = wdiv<WK>(rho0, phi, fw);
+      if (st) tr[80] = clock64() + (al.x == 1.234e300);
       S.sc[g * 8 + 0] = al;
       // alphas[i-1] = alpha where active | newly_bad | broke (solvers.py:371)
       if (H && H->al) H->al[h_at(it - 1, g)] = stall ? make_double2(0.0, 0.0) : al;
-      if (tr && g == 0 && it <= 2) tr[52 + (it - 1) * 4] = clock64() + (al.x == 1.2345e300);
     }
     bar.sync();
     FPM_STAMP(tr, 1 + (it - 1) * 6 + 1);
-    // ---- C: x, r updates (u_W) + finiteness ----
-#pragma unroll 1
-    for (int k = 0; k < nrow; ++k) {
-      const int q = tid + k * nthreads;
-      const int g = q / N;
-      if (!S.fl[g * 4]) continue;
-      const double2 al = S.sc[g * 8 + 0];
-      const double2 xn = axpy1<WK>(al, S.p[q], S.x[q], fw);
-      const double2 rn = axpy1<WK>(make_double2(-al.x, -al.y), S.w[q], S.r[q], fw);
-      S.xn[q] = xn;
-      S.rn[q] = rn;
-      if (!(finite2(xn) && finite2(rn))) S.fl[g * 4 + 1] = 1;
-    }
-    bar.sync();
-    FPM_STAMP(tr, 1 + (it - 1) * 6 + 2);
-    // ---- D: commit; z = M r_new; rho1 terms ----
+    // ---- C: x, r updates (u_W) + finiteness; z = M r and rho1 terms ----
 #pragma unroll 1
     for (int k = 0; k < nrow; ++k) {
       const int q = tid + k * nthreads;
       const int g = q / N, i = q - g * N;
-      if (!S.fl[g * 4] || S.fl[g * 4 + 1]) continue;
-      const double2 rn = S.rn[q];
-      S.x[q] = S.xn[q];
-      S.r[q] = rn;
-      const C ri = ipr(rn);
-      S.rip[q] = ri;
-      if (bj) {
+      if (!S.fl[g * 4]) continue;
+      const bool st = tr && tid == 0 && it == 2;
+      if (st) tr[70] = clock64();
+      const double2 al = S.sc[g * 8 + 0];
+      const double2 nal = make_double2(-al.x, -al.y);
+      const double2 xn = axpy1<WK>(al, S.p[q], S.x[q], fw);
+      const double2 rn = axpy1<WK>(nal, S.w[q], S.r[q], fw);
+      S.xn[q] = xn;
+      S.rn[q] = rn;
+      if (st) tr[71] = clock64() + (rn.x == 1.234e300);
+      if (!(finite2(xn) && finite2(rn))) S.fl[g * 4 + 1] = 1;
+      if (merged) {
+        const C ri = ipr(rn);
+        if (bj) {
+          if constexpr (LB > 0) {
+            // this thread recomputes its block's r updates (same bits as the
+            // owning threads) so z = M r needs no barrier
+            const int kb = i / LB, jl = i - kb * LB, s0 = g * N + kb * LB;
+            double2 rl[LB];
+#pragma unroll
+            for (int l = 0; l < LB; ++l)  // branch-free: row jl recomputes rn bit-identically
+              rl[l] = Ar<WK>::rnd(axpy1<WK>(nal, S.w[s0 + l], S.r[s0 + l], fw), fw);
+            if (st) tr[72] = clock64() + (rl[LB - 1].x == 1.234e300);
+            const double2 zv = bj_row_reg<WK, LB>(S.minv + g * N * S.L + kb * LB * LB, rl, jl, fw);
+            if (st) tr[73] = clock64() + (zv.x == 1.234e300);
+            S.z[q] = zv;
+            S.tr1[q] = A::mulc(ri, ipr(zv), fi);
+            if (st) tr[74] = clock64() + (h2u(*reinterpret_cast<__half2*>(&S.tr1[q])) == 12345u);
+          }
+        } else {
+          S.tr1[q] = A::mulc(ri, ri, fi);
+        }
+      }
+    }
+    if (!merged) {  // ragged block-Jacobi: z after a barrier
+      bar.sync();
+#pragma unroll 1
+      for (int k = 0; k < nrow; ++k) {
+        const int q = tid + k * nthreads;
+        const int g = q / N, i = q - g * N;
+        if (!S.fl[g * 4] || S.fl[g * 4 + 1]) continue;
         const double2 zv = bj_row<WK, LB>(S.minv + g * N * S.L, S.rn + g * N, i, S.L, N, fw);
         S.z[q] = zv;
-        S.tr1[q] = A::mulc(ri, ipr(zv), fi);
-      } else {
-        S.tr1[q] = A::mulc(ri, ri, fi);
+        S.tr1[q] = A::mulc(ipr(S.rn[q]), ipr(zv), fi);
       }
     }
     bar.sync();
-    FPM_STAMP(tr, 1 + (it - 1) * 6 + 3);
+    FPM_STAMP(tr, 1 + (it - 1) * 6 + 2);
     // ---- E: rho1, beta, divergence flag ----
     if (H && H->be && og >= 0 && ow == 0 && !S.fl[og * 4]) H->be[h_at(it - 1, og)] = make_double2(0.0, 0.0);
     if (og >= 0 && ow == 0 && S.fl[og * 4]) {
@@ -445,24 +547,16 @@ __device__ void cg_group(CgSmem<K>& S, int Rv, int iters, bool bj, bool textbook
         S.fl[g * 4] = 0;
         if (H && H->be) H->be[h_at(it - 1, g)] = make_double2(0.0, 0.0);
       } else {
-        const double2 rho1 = chain_sum<K>(S.tr1 + g * N, N, fi);
+        const double2 rho1 = csum(S.tr1 + g * N);
         const double2 be = wdiv<WK>(rho1, S.sc[g * 8 + 3], fw);
         S.sc[g * 8 + 1] = be;
         S.sc[g * 8 + 4] = rho1;
         if (H && H->be) H->be[h_at(it - 1, g)] = be;  // betas: where(active, beta, 0)
       }
     }
-    if (H && og >= 0 && ow == 1) {  // res_hist[i], xn_hist[i] (solvers.py:373-374)
-      h_res = norm2_c(S.r + og * N, N);
-      h_xn = norm2_c(S.x + og * N, N);
-      if (H->res) H->res[h_at(it, og)] = h_res;
-      if (H->xn) H->xn[h_at(it, og)] = h_xn;
-      if (h_conv < 0 && h_res <= H->rtol * fmax(h_bn, 1e-300)) h_conv = it;
-    }
     bar.sync();
-    FPM_STAMP(tr, 1 + (it - 1) * 6 + 4);
-    // ---- F: p = (z|r) + beta p ; pmv = rnd(p) ; next rho0 terms ----
-    if (H) h_rows(it);
+    FPM_STAMP(tr, 1 + (it - 1) * 6 + 3);
+    // ---- F: commit x, r; p = (z|r) + beta p ; pmv = rnd(p) ; next rho0 terms ----
     int any = 0;
 #pragma unroll 1
     for (int k = 0; k < nrow; ++k) {
@@ -470,14 +564,24 @@ __device__ void cg_group(CgSmem<K>& S, int Rv, int iters, bool bj, bool textbook
       const int g = q / N;
       if (!S.fl[g * 4]) continue;
       any = 1;
-      const double2 pn = axpy1<WK>(S.sc[g * 8 + 1], S.p[q], bj ? S.z[q] : S.r[q], fw);
+      const double2 rn = S.rn[q];
+      S.x[q] = S.xn[q];
+      S.r[q] = rn;
+      const C ri = ipr(rn);
+      S.rip[q] = ri;
+      const double2 pn = axpy1<WK>(S.sc[g * 8 + 1], S.p[q], bj ? S.z[q] : rn, fw);
       S.p[q] = pn;
       const C pm = A::rnd(pn, fm);
       S.pmv[q] = A::prep(pm);
-      if (rho_fresh) S.trho[q] = A::mulc(S.rip[q], K == FK_GEN ? ipr(pn) : pm, fi);
+      if (rho_fresh) S.trho[q] = A::mulc(ri, K == FK_GEN ? ipr(pn) : pm, fi);
     }
     const int more = bar.any(any);
     FPM_STAMP(tr, 1 + (it - 1) * 6 + 5);
+    // x, r are stable until the next F: record this sweep without a barrier
+    if (H) {
+      if (og >= 0 && ow == 1) h_norms(it);
+      h_rows(it);
+    }
     if (!more) {
       it_last = it;
       break;

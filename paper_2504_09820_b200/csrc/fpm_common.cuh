@@ -44,6 +44,7 @@ struct DetectArgs {
   int ws_order;  // 0: [Gram | producer | CG] threads, 1: [CG | producer | Gram]
   int ws_ncg, ws_ct0;  // CG groups (1 or 2) and the thread count of group 0
   int cg_stride;       // bytes between the two CG groups' state regions
+  int ws_nslot;        // hand-off slots (2 double-buffered, 1 when two do not fit)
   int debug;  // diagnostic bits (FPM_DEBUG): 1 = WS kernel skips the CG side
 };
 
@@ -62,6 +63,7 @@ struct CgArgs {
   int* div;
   int off_minv, off_vec, off_pmv, off_tip, off_sc, off_fl;
   CgHist h;
+  long long* trace;  // nullable: phase clock stamps of CTA 0 (diagnostic)
 };
 
 // Launchers (return FPM_* codes).  nb / lb: compile-time specialisation

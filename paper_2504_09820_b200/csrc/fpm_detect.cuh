@@ -209,7 +209,7 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_kernel(const DetectArgs arg
   // 3) CG in shared memory
   {
     CtaBar bar;
-    cg_group<WK, K, LB>(S, Rv, args.iters, args.bj != 0, args.textbook != 0, args.pr, nthreads, tid, bar,
+    cg_group<WK, K, LB, (NB > 0 ? 4 * NB : 0)>(S, Rv, args.iters, args.bj != 0, args.textbook != 0, args.pr, nthreads, tid, bar,
                         tr ? tr + 3 : nullptr);
   }
   FPM_STAMP(tr, 10);
@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_kernel(const DetectArgs arg
   FPM_STAMP(tr, 15);
 }
 
-template <int WK, int K, int LB>
+template <int WK, int K, int LB, int NC>
 __global__ void __launch_bounds__(256) fpm_cg_kernel(const CgArgs args) {
   extern __shared__ __align__(128) unsigned char smem[];
   typedef typename Ar<K>::C C;
@@ -258,7 +258,7 @@ __global__ void __launch_bounds__(256) fpm_cg_kernel(const CgArgs args) {
   const int tid = threadIdx.x, nthreads = blockDim.x;
   const long t0 = (long)blockIdx.x * args.R;
   const int Rv = (int)min((long)args.R, args.T - t0);
-  const int N = args.N;
+  const int N = NC > 0 ? NC : args.N;
   CgSmem<K> S;
   S.R = args.R;
   S.N = N;
@@ -316,7 +316,9 @@ __global__ void __launch_bounds__(256) fpm_cg_kernel(const CgArgs args) {
   __syncthreads();
   {
     CtaBar bar;
-    cg_group<WK, K, LB>(S, Rv, args.iters, args.bj != 0, args.textbook != 0, args.pr, nthreads, tid, bar);
+    long long* tr = (args.trace && blockIdx.x == 0) ? args.trace : nullptr;
+    if (tr && tid == 0) tr[60] = clock64();
+    cg_group<WK, K, LB, NC>(S, Rv, args.iters, args.bj != 0, args.textbook != 0, args.pr, nthreads, tid, bar, tr);
   }
 #pragma unroll 1
   for (int q = tid; q < Rv * N; q += nthreads) args.x[t0 * N + q] = S.x[q];
@@ -338,14 +340,21 @@ int launch_detect_t(const DetectArgs& a, int threads, cudaStream_t st) {
   return cudaGetLastError() == cudaSuccess ? FPM_OK : FPM_ECUDA;
 }
 
-template <int WK, int K, int LB>
-int launch_cg_t(const CgArgs& a, int smem, cudaStream_t st) {
-  auto k = fpm_cg_kernel<WK, K, LB>;
+template <int WK, int K, int LB, int NC>
+int launch_cg_nc(const CgArgs& a, int smem, cudaStream_t st) {
+  auto k = fpm_cg_kernel<WK, K, LB, NC>;
   if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return FPM_ECUDA;
   const long grid = (a.T + a.R - 1) / a.R;
   k<<<(unsigned)grid, 256, smem, st>>>(a);
   count_launch();
   return cudaGetLastError() == cudaSuccess ? FPM_OK : FPM_ECUDA;
+}
+
+// N = 64 (c2/c3/c5 shapes) gets the compile-time-N (fully unrolled) sums
+template <int WK, int K, int LB>
+int launch_cg_t(const CgArgs& a, int smem, cudaStream_t st) {
+  if (a.N == 64) return launch_cg_nc<WK, K, LB, 64>(a, smem, st);
+  return launch_cg_nc<WK, K, LB, 0>(a, smem, st);
 }
 
 }  // namespace fpm

@@ -7,7 +7,8 @@
 //                          inverses, (BJ-)CG, slicing, counters, write-back.
 //
 // The hand-off is a double-buffered shared-memory slot (A at u_MV, b, fp64
-// diagonal blocks) guarded by two mbarrier pairs (slot full / slot empty), so
+// diagonal blocks; a single slot when two do not fit, e.g. fp64 matvec)
+// guarded by two mbarrier pairs (slot full / slot empty), so
 // the latency-bound CG of one group never stalls the FP64 pipe: the Gram
 // warps only wait for a slot when the CG side is more than one group behind.
 // The H ring runs continuously across groups (the producer prefetches the
@@ -30,10 +31,10 @@ struct WsLayout {  // byte offsets inside one hand-off slot
   int at, b, d, bytes;
 };
 
-// role order (FPM_WS_ORDER: 0 = Gram warps first, default; 1 = CG first)
-inline int env_order() {
+// role order (planner's choice, FPM_WS_ORDER overrides: 0 = Gram warps first, 1 = CG first)
+inline int env_order(int planned) {
   const char* v = std::getenv("FPM_WS_ORDER");
-  return v ? (std::atoi(v) != 0) : 0;
+  return v ? (std::atoi(v) != 0) : planned;
 }
 
 // CG group width under the register split (FPM_WS_CT, default: all 224
@@ -71,6 +72,8 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const DetectArgs 
   uint64_t* ybar = full + 2 * G.S;   // [2]
   uint64_t* sfull = ybar + 2;        // [2]
   uint64_t* sempty = sfull + 2;      // [2]
+  uint64_t* ydone = sempty + 2;      // [2] Gram finished reading y buffer b
+  const int nsl = args.ws_nslot;     // hand-off slots (2, or 1 when two do not fit)
   double2* stages = reinterpret_cast<double2*>(smem + args.off_union);
   double2* ysb = reinterpret_cast<double2*>(smem + args.off_ys);  // [2][R*M]
   unsigned char* slots = smem + args.off_slot;
@@ -88,6 +91,7 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const DetectArgs 
       mbar_init(&ybar[k], 1);
       mbar_init(&sfull[k], 1);
       mbar_init(&sempty[k], 1);
+      mbar_init(&ydone[k], 1);
     }
     fence_mbar_init();
   }
@@ -125,7 +129,9 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const DetectArgs 
     for (int j = 0; j < my_groups; ++j) {
       const long t0 = ((long)blockIdx.x + (long)j * gridDim.x) * R;
       const int Rv = (int)min((long)R, args.T - t0);
-      const int slot = j & 1;
+      const int yb = j & 1;                     // y double buffer
+      const int slot = nsl == 2 ? (j & 1) : 0;  // hand-off slot and its use count
+      const int use = nsl == 2 ? (j >> 1) : j;
       const bool active = job.g >= 0 && job.g < Rv;
       const int nchain = 2 * Rv * N;
       const bool chain_ok = kChainInLoop && tid < nchain;
@@ -137,8 +143,8 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const DetectArgs 
 #pragma unroll 1
         for (int q = tid; q < nchain; q += gt) bsm[q] = 0.0;
       }
-      const double2* ys = ysb + slot * R * G.M;
-      mbar_wait(&ybar[slot], (uint32_t)((j >> 1) & 1));
+      const double2* ys = ysb + yb * R * G.M;
+      mbar_wait(&ybar[yb], (uint32_t)((j >> 1) & 1));
       if (tr && tid == 0 && j < 8) tr[j * 8 + 0] = clock64();
 
 #pragma unroll 1
@@ -358,7 +364,7 @@ FPM_ROW_UNROLL
       // ---- hand-off: wait until the CG side has released this slot ----
       if (tr && tid == 0 && j < 8) tr[j * 8 + 1] = clock64();
       if (tr && (tid & 31) == 0 && j == 2) tr[72 + tid / 32] = clock64();
-      if (j >= 2) mbar_wait(&sempty[slot], (uint32_t)(((j >> 1) - 1) & 1));
+      if (j >= nsl) mbar_wait(&sempty[slot], (uint32_t)((use - 1) & 1));
       if (tr && tid == 0 && j < 8) tr[j * 8 + 2] = clock64();
       unsigned char* sp = slots + slot * sl.bytes;
       C* At = reinterpret_cast<C*>(sp + sl.at);
@@ -402,7 +408,10 @@ FPM_ROW_UNROLL
         }
       }
       gbar.sync();
-      if (tid == 0) mbar_arrive(&sfull[slot]);
+      if (tid == 0) {
+        mbar_arrive(&sfull[slot]);
+        mbar_arrive(&ydone[yb]);  // every Gram warp is past this group's y reads
+      }
       if (tr && tid == 0 && j < 8) tr[j * 8 + 3] = clock64();
     }
   } else {
@@ -433,7 +442,7 @@ FPM_ROW_UNROLL
           // the y buffer of group jj was last read by group jj-2: wait until
           // that group's Gram is done (its hand-off has been published)
           const int jj = (int)(gc / nch);
-          mbar_wait(&sfull[jj & 1], (uint32_t)(((jj - 2) >> 1) & 1));
+          mbar_wait(&ydone[jj & 1], (uint32_t)(((jj - 2) >> 1) & 1));
         }
         issue(gc);
       }
@@ -477,12 +486,13 @@ FPM_ROW_UNROLL
     for (int j = cgi; j < my_groups; j += ncg) {
       const long t0 = ((long)blockIdx.x + (long)j * gridDim.x) * R;
       const int Rv = (int)min((long)R, args.T - t0);
-      const int slot = j & 1;
+      const int slot = nsl == 2 ? (j & 1) : 0;
+      const int use = nsl == 2 ? (j >> 1) : j;
       unsigned char* sp = slots + slot * sl.bytes;
       S.At = reinterpret_cast<C*>(sp + sl.at);
       S.b = reinterpret_cast<double2*>(sp + sl.b);
       double2* dS = reinterpret_cast<double2*>(sp + sl.d);
-      mbar_wait(&sfull[slot], (uint32_t)((j >> 1) & 1));
+      mbar_wait(&sfull[slot], (uint32_t)(use & 1));
       if (tr && lt == 0 && j < 8) tr[j * 8 + 4] = clock64();
 #pragma unroll 1
       for (int g = lt; g < R; g += ctg) S.fl[g * 4] = g < Rv ? 1 : 0;
@@ -525,7 +535,7 @@ FPM_ROW_UNROLL
         __shared__ int _fpm_dummy_ws;
         tc[60] = (long long)clock64() + (*(volatile int*)&_fpm_dummy_ws == 0x7fffffff);
       }
-      if (!(args.debug & 1)) cg_group<WK, K, LB>(S, Rv, args.iters, args.bj != 0, args.textbook != 0, args.pr, ctg, lt, cbar, tc);
+      if (!(args.debug & 1)) cg_group<WK, K, LB, (NB > 0 ? 4 * NB : 0)>(S, Rv, args.iters, args.bj != 0, args.textbook != 0, args.pr, ctg, lt, cbar, tc);
       // slot no longer needed (A, b, diagonal blocks consumed)
       if (lt == 0) mbar_arrive(&sempty[slot]);
       if (tr && lt == 0 && j < 8) tr[j * 8 + 5] = clock64();
@@ -573,7 +583,7 @@ FPM_ROW_UNROLL
 template <int WK, int K, int NB, int LB>
 int launch_detect_ws_t(const DetectArgs& a, const WsLayout& sl, int grid, cudaStream_t st) {
   DetectArgs b = a;
-  b.ws_order = env_order();
+  b.ws_order = env_order(a.ws_order);
   const int threads = a.ws_gt + 32 + a.ws_ct;
   if constexpr (NB == 16) {
     // N = 64, R = 2: 256 Gram threads = two warp groups and a 512-thread

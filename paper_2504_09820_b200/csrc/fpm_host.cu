@@ -380,7 +380,8 @@ static int sm_count() {
 
 // Warp-specialised persistent kernel geometry (fpm_detect_ws.cuh): R realizations
 // per group with uniform Gram warps, gt Gram threads + ct CG threads <= 512.
-static bool plan_detect_ws(int M, int N, int L, int bj, int mvk, int ipk, DetectArgs& a, WsLayout& sl, int& grid) {
+static bool plan_detect_ws(int M, int N, int L, int bj, int iters, int mvk, int ipk, DetectArgs& a, WsLayout& sl,
+                           int& grid) {
   if (std::getenv("FPM_NO_WS")) return false;
   const int Np = (N + 7) / 8 * 8, nb = Np / 4, Cc = nb * (nb / 2 - 1);
   const int limit = max_smem_optin();
@@ -402,16 +403,31 @@ static bool plan_detect_ws(int M, int N, int L, int bj, int mvk, int ipk, Detect
   // warp groups: 512 threads = 256 Gram + 32 producer + 128 + 96 CG
   const int ncg_env = env_int("FPM_WS_NCG", 0);
   const int stage_list[] = {24, 20, 16, 12, 8, 4};
-  for (int ncg = (gt == 256 ? 2 : 1); ncg >= 1; --ncg) {
+  // candidates (CG groups, hand-off slots).  When one CG pass is shorter
+  // than one Gram pass (few sweeps relative to the antenna rows; measured:
+  // c5 fp16 CG 84 K vs Gram 89 K cycles per group) a single CG group on a
+  // single slot keeps up and leaves the most shared memory to the H ring;
+  // otherwise two CG groups on alternating slots, then fallbacks.
+  const bool cg_short = (long)iters * N <= 8L * M && mvk != FK_F64;
+  const int cand_short[4][2] = {{1, 1}, {2, 2}, {1, 2}, {1, 1}};
+  const int cand_long[4][2] = {{2, 2}, {1, 2}, {1, 1}, {1, 1}};
+  const int(*cand)[2] = cg_short ? cand_short : cand_long;
+  const int stage_short[6] = {32, 24, 20, 16, 12, 8};
+  for (int ci = 0; ci < 4; ++ci) {
+    const int ncg = cand[ci][0], nslot = cand[ci][1];
+    if (ncg == 2 && gt != 256) continue;
     if (ncg_env && ncg != ncg_env) continue;
+    if (env_int("FPM_WS_NSLOT", 0) && nslot != env_int("FPM_WS_NSLOT", 0)) continue;
     for (int si = 0; si < 6; ++si) {
-      const int stage_kb = env_int("FPM_STAGE_KB", 0) ? env_int("FPM_STAGE_KB", 0) : stage_list[si];
+      const int stage_kb = env_int("FPM_STAGE_KB", 0) ? env_int("FPM_STAGE_KB", 0)
+                           : (ncg == 1 && nslot == 1 && cg_short ? stage_short[si] : stage_list[si]);
       if (env_int("FPM_STAGE_KB", 0) && si > 0) break;
       GramGeom G;
       gram_geom(R, M, N, G, stage_kb);
       G.S = std::max(3, G.S);  // the producer refills two chunks behind
       const int ldA = lda_for(N, mv_bytes(mvk));
-      size_t off = 128;  // mbarriers
+      size_t off = 256;  // mbarriers: full[S], empty[S], ybar, sfull, sempty, ydone [2 each]
+      if ((2 * G.S + 8) * 8 > 256) continue;
       a.off_union = (int)off;  // H stage ring
       off = align_up(off + (size_t)G.S * R * G.MC * G.Np * 16, 128);
       a.off_ys = (int)off;
@@ -421,7 +437,7 @@ static bool plan_detect_ws(int M, int N, int L, int bj, int mvk, int ipk, Detect
       sl.d = (int)align_up(sl.b + (size_t)R * N * 16, 128);
       sl.bytes = (int)align_up(sl.d + (bj ? (size_t)R * N * Lb * 16 : 0), 128);
       a.off_slot = (int)off;
-      off = align_up(off + (size_t)2 * sl.bytes, 128);
+      off = align_up(off + (size_t)nslot * sl.bytes, 128);
       a.off_bsm = (int)off;  // matched-filter chain accumulators
       off = align_up(off + (size_t)2 * R * N * 8, 128);
       // ---- per-CG-group state (replicated ncg times, cg_stride apart) ----
@@ -455,6 +471,8 @@ static bool plan_detect_ws(int M, int N, int L, int bj, int mvk, int ipk, Detect
         a.ws_ct = gt == 256 ? 224 : (R * N + 31) / 32 * 32 + 32;
         a.ws_ncg = ncg;
         a.ws_ct0 = ncg == 2 ? 128 : a.ws_ct;
+        a.ws_nslot = nslot;
+        a.ws_order = ncg == 1 ? 1 : 0;  // measured: CG-first for one group, Gram-first for two
         const long ngroups = (a.T + R - 1) / R;
         grid = (int)std::min<long>(ngroups, (long)sm_count() * env_int("FPM_CTAS_PER_SM", 1));
         return true;
@@ -710,6 +728,7 @@ int fpm_cg_ex(const double* A, const double* b, const double* Minv, int64_t T, i
   a.brk = breakdown_at;
   a.div = diverged_at;
   a.tl = pick_tl(N);
+  a.trace = g_trace;
   if (hist) {
     a.h.res = hist->residual_norms;
     a.h.xn = hist->iterate_norms;
@@ -789,7 +808,7 @@ static int detect_args(const double* H, const double* y, const uint8_t* tx_bits,
   a.debug = env_int("FPM_DEBUG", 0);
   k = pick_kinds(*pp);
   DetectArgs aw = a;
-  ws = plan_detect_ws(M, N, a.L, bj, k.mv, k.ip, aw, sl, grid);
+  ws = plan_detect_ws(M, N, a.L, bj, iters, k.mv, k.ip, aw, sl, grid);
   if (ws) {
     a = aw;
     return FPM_OK;

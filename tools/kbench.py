@@ -49,6 +49,7 @@ def main():
     ap.add_argument("--L", type=int, default=bench.L)
     ap.add_argument("--trace", action="store_true")
     ap.add_argument("--wstrace", action="store_true")
+    ap.add_argument("--cgtrace", action="store_true")
     a = ap.parse_args()
     bench.M, bench.N, bench.L = a.M, a.N, a.L
     M, N, L, T = a.M, a.N, a.L, a.T
@@ -97,6 +98,29 @@ def main():
         byts = 16 * N * N + 16 * N * (2 + L) + 8
         out["cg"] = {"ms": ms, "det_s": T / ms * 1e3, "hbm_gbs": byts * T / (ms / 1e3) / 1e9,
                      "hbm_frac": byts * T / (ms / 1e3) / 6554.9e9}
+    if a.cgtrace:  # standalone CG kernel, CTA 0 phase stamps (one wave: 1 CTA per SM)
+        gram()
+        bj()
+        tr = torch.zeros(160, dtype=torch.int64, device=dev)
+        lib.fpm_debug_set_trace(tr.data_ptr())
+        cg()
+        torch.cuda.synchronize()
+        lib.fpm_debug_set_trace(None)
+        c = tr.cpu().tolist()
+        ph = ["A:matvec", "B:phi/alpha", "C:axpy+z", "E:rho1/beta", "-", "F:commit+p"]
+        o = {"init": c[0] - c[60]}
+        prev = c[0]
+        for it in range(8):
+            for k in range(6):
+                v = c[1 + it * 6 + k]
+                if v:
+                    o.setdefault(ph[k], []).append(v - prev)
+                    prev = v
+        o["total"] = prev - c[60]
+        o["A_detail_it2"] = [c[75] - c[1 + 6 + 5 - 6 + 0] if False else c[75] - c[6], c[76] - c[75], c[77] - c[76], c[1 + 6] - c[77]]
+        o["B_detail_it2"] = [c[78] - c[1 + 6], c[79] - c[78], c[80] - c[79], c[1 + 6 + 1] - c[80]]
+        o["C_detail_it2"] = [c[71] - c[70], c[72] - c[71], c[73] - c[72], c[74] - c[73], c[1 + 6 + 2] - c[74]]
+        out["cg_trace"] = o
     if a.wstrace:
         tr = torch.zeros(160, dtype=torch.int64, device=dev)
         lib.fpm_debug_set_trace(tr.data_ptr())
@@ -112,7 +136,7 @@ def main():
         out["ws_warp_loopend_g2"] = [t[72 + w] - t[2*8+0] for w in range(12)]
         c = t[96:160]
         if c[60]:
-            ph = ["A:matvec", "B:phi/alpha", "C:axpy", "D:commit/z", "E:rho1/beta", "F:p"]
+            ph = ["A:matvec", "B:phi/alpha", "C:axpy+z", "E:rho1/beta", "-", "F:commit+p"]
             out["ws_cg_g2"] = {"bj": c[60] - t[2*8+4], "init": c[0] - c[60]}
             prev = c[0]
             for it in range(8):
@@ -121,7 +145,6 @@ def main():
                     if v:
                         out["ws_cg_g2"].setdefault(ph[k], []).append(v - prev)
                         prev = v
-            out["ws_cg_g2"]["B_owner_it1"] = {"start_after_A": c[50] - c[1], "chain": c[51] - c[50], "wdiv": c[52] - c[51], "to_barrier_release": c[2] - c[52]}
     if a.trace:
         tr = torch.zeros(64, dtype=torch.int64, device=dev)
         lib.fpm_debug_set_trace(tr.data_ptr())
