@@ -219,6 +219,25 @@ __device__ __noinline__ double2 chain_sum_n(const typename Ar<K>::C* t, const Fm
 #pragma unroll
     for (int j = 1; j < NC; ++j) s = A::add(s, v[j], f);
     return A::wide(A::asmc(s));
+  } else if constexpr (NC % 8 == 0 && NC <= 128) {
+    // wide terms: 8-term blocks, each loaded two blocks ahead of its adds
+    C v0[8], v1[8], v2[8];
+    ld_blk<8>(t, v0);
+    if (NC > 8) ld_blk<8>(t + 8, v1);
+    C s = v0[0];
+#pragma unroll
+    for (int k = 0; k < NC; k += 8) {
+      if (k + 16 < NC) ld_blk<8>(t + k + 16, v2);
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (k + j > 0) s = A::add(s, v0[j], f);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        v0[j] = v1[j];
+        v1[j] = v2[j];
+      }
+    }
+    return A::wide(A::asmc(s));
   } else {
     return chain_sum<K>(t, NC, f);
   }
@@ -243,6 +262,38 @@ __device__ __noinline__ typename Ar<K>::C mv_row_n(const typename Ar<K>::C* row,
       for (int j = 0; j < B; ++j) {
         const C t = A::mulp(a[j], p[j], f);
         s = (k + j == 0) ? t : A::add(s, t, f);
+      }
+    }
+    return A::asmc(s);
+  } else if constexpr (NC % 4 == 0 && NC <= 128) {
+    // wide terms: 4-term blocks loaded two blocks ahead; the products of a
+    // block are formed before its adds so they overlap the add chain
+    C a0[4], a1[4], a2[4];
+    P p0[4], p1[4], p2[4];
+    ld_blk<4>(row, a0);
+    ld_blk<4>(pv, p0);
+    if (NC > 4) {
+      ld_blk<4>(row + 4, a1);
+      ld_blk<4>(pv + 4, p1);
+    }
+    C s;
+#pragma unroll
+    for (int k = 0; k < NC; k += 4) {
+      if (k + 8 < NC) {
+        ld_blk<4>(row + k + 8, a2);
+        ld_blk<4>(pv + k + 8, p2);
+      }
+      C t[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) t[j] = A::mulp(a0[j], p0[j], f);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) s = (k + j == 0) ? t[0] : A::add(s, t[j], f);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        a0[j] = a1[j];
+        a1[j] = a2[j];
+        p0[j] = p1[j];
+        p1[j] = p2[j];
       }
     }
     return A::asmc(s);

@@ -64,6 +64,10 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const DetectArgs 
   const int my_groups = blockIdx.x < ngroups ? (int)((ngroups - blockIdx.x + gridDim.x - 1) / gridDim.x) : 0;
   const int nch = (G.M + G.MC - 1) / G.MC;
   const int L = args.bj ? (LB > 0 ? LB : args.L) : 1;
+  // compile-time N for the CG sums, except for 16-byte (fp64 / generic)
+  // matvec terms under the register split: their unrolled sums do not fit the
+  // CG warps' 256 - RS registers, the loop versions do
+  constexpr int kCgNC = (NB > 0 && (RS == 0 || sizeof(typename Ar<K>::C) < 16)) ? 4 * NB : 0;
   const int nblk = args.bj ? (N + L - 1) / L : 1;
   const int ldA = NB > 0 ? lda_for(N, (int)sizeof(C)) : args.ldA;
 
@@ -535,7 +539,7 @@ FPM_ROW_UNROLL
         __shared__ int _fpm_dummy_ws;
         tc[60] = (long long)clock64() + (*(volatile int*)&_fpm_dummy_ws == 0x7fffffff);
       }
-      if (!(args.debug & 1)) cg_group<WK, K, LB, (NB > 0 ? 4 * NB : 0)>(S, Rv, args.iters, args.bj != 0, args.textbook != 0, args.pr, ctg, lt, cbar, tc);
+      if (!(args.debug & 1)) cg_group<WK, K, LB, kCgNC>(S, Rv, args.iters, args.bj != 0, args.textbook != 0, args.pr, ctg, lt, cbar, tc);
       // slot no longer needed (A, b, diagonal blocks consumed)
       if (lt == 0) mbar_arrive(&sempty[slot]);
       if (tr && lt == 0 && j < 8) tr[j * 8 + 5] = clock64();

@@ -1,3 +1,2 @@
-nvidia-smi --query-gpu=pcie.link.gen.current,pcie.link.width.current --format=csv
-for i in 1 2; do python bench.py --T 65536 --steps 3 --warmup 3 --no-cpu 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['e2e']['value'])"; done
-FPM_WS_NSLOT=2 python bench.py --T 65536 --steps 3 --warmup 3 --no-cpu 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('nslot2', d['value'], d['e2e']['value'])"
+python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+for p in fp16 fp64; do timeout 300 python tools/kbench.py --only detect --T 131072 --precision $p 2>&1 | tail -1; done
