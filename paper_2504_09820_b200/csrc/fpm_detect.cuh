@@ -284,14 +284,33 @@ __global__ void __launch_bounds__(256) fpm_cg_kernel(const CgArgs args) {
   S.sc = reinterpret_cast<double2*>(smem + args.off_sc);
   S.fl = reinterpret_cast<int*>(smem + args.off_fl);
 
-  // A (row-major, global) -> At (row-major, pitch ldA, u_MV), coalesced
+  // A (row-major, global) -> At (row-major, pitch ldA, u_MV), coalesced;
+  // 8 streaming loads in flight per thread (the copy is HBM-latency bound
+  // with one outstanding load per thread)
   const int NN = N * N;
+  {
+    constexpr int U = 8;
+    const double2* Ag = args.A + t0 * (long)NN;
+    const int tot = Rv * NN;
 #pragma unroll 1
-  for (int q = tid; q < Rv * NN; q += nthreads) {
-    const int g = q / NN;
-    const int e = q - g * NN;
-    const int i = e / N, k = e - i * N;
-    S.At[(g * N + i) * S.ldA + k] = Ar<K>::rnd(args.A[(t0 + g) * NN + e], args.pr.mv);
+    for (int q0 = tid; q0 < tot; q0 += nthreads * U) {
+      double2 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int q = q0 + u * nthreads;
+        if (q < tot) v[u] = __ldcs(Ag + q);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int q = q0 + u * nthreads;
+        if (q < tot) {
+          const int g = q / NN;
+          const int e = q - g * NN;
+          const int i = e / N, k = e - i * N;
+          S.At[(g * N + i) * S.ldA + k] = Ar<K>::rnd(v[u], args.pr.mv);
+        }
+      }
+    }
   }
 #pragma unroll 1
   for (int q = tid; q < Rv * N; q += nthreads) S.b[q] = args.b[t0 * N + q];
