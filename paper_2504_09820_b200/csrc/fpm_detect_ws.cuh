@@ -26,6 +26,10 @@ namespace fpm {
 #ifndef FPM_GRAM_PIPE
 #define FPM_GRAM_PIPE 1
 #endif
+#ifndef FPM_PIPE_UNROLL_N
+#define FPM_PIPE_UNROLL_N 1
+#endif
+#define FPM_PIPE_UNROLL FPM_UNROLL_(FPM_PIPE_UNROLL_N)
 
 struct WsLayout {  // byte offsets inside one hand-off slot
   int at, b, d, bytes;
@@ -185,7 +189,7 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const DetectArgs 
             y1 = y1p[0];
             y2 = y2p[0];
           }
-#pragma unroll 1
+FPM_PIPE_UNROLL
           for (int mm = 0; mm < rows; ++mm) {
             const int mn = (mm + 1 < rows) ? mm + 1 : mm;
             double2 ni[4], nj[4], nhc = hc;
@@ -255,7 +259,7 @@ FPM_ROW_UNROLL
             y1 = y1p[0];
             y2 = y2p[0];
           }
-#pragma unroll 1
+FPM_PIPE_UNROLL
           for (int mm = 0; mm < rows; ++mm) {
             const int mn = (mm + 1 < rows) ? mm + 1 : mm;
             double2 nx[4], ny[2], nz[4], nhc = hc;
