@@ -68,8 +68,9 @@ enum {
 
 enum { FPM_RHO_AS_WRITTEN = 0, FPM_RHO_TEXTBOOK = 1 };
 
-/* DetectorSpec.algorithm (detect.py:115); "cg" computes at fp64 throughout */
-enum { FPM_ALG_CG = 1, FPM_ALG_FP_CG = 2, FPM_ALG_FP_BJ_CG = 3 };
+/* DetectorSpec.algorithm (detect.py:115); "cg" computes at fp64 throughout;
+ * "lmmse" is the direct Cholesky comparator (detect.py:230-231) */
+enum { FPM_ALG_LMMSE = 0, FPM_ALG_CG = 1, FPM_ALG_FP_CG = 2, FPM_ALG_FP_BJ_CG = 3 };
 
 enum {
   FPM_CNT_BIT_ERRORS = 0,
@@ -124,6 +125,14 @@ typedef struct fpm_cg_history {
 int fpm_cg_ex(const double* A, const double* b, const double* Minv, int64_t T, int32_t N, int32_t L,
               int32_t iters, const fpm_precision* prec, int32_t rho_update, double* x, int32_t* breakdown_at,
               int32_t* diverged_at, const fpm_cg_history* hist, void* stream);
+
+/* LMMSE direct solve x = A^-1 b by fp64 Cholesky (linalg.py:223-231
+ * _solve_direct_batch: scipy cho_factor / cho_solve).  A (T,N,N), b (T,N)
+ * complex128 on the device.  nonpd: optional device int32 counter of
+ * realizations whose A is not positive definite (their x is NaN; the
+ * reference raises LinAlgError).  LAPACK bits are not reproduced: x agrees
+ * to ~1e-13 normwise. */
+int fpm_lmmse(const double* A, const double* b, int64_t T, int32_t N, double* x, int32_t* nonpd, void* stream);
 
 /* qam = 16 (reference) or 64 (extension).  tx_bits / rx_bits: (T, bits*N)
  * uint8 in the reference's layout, both nullable. */

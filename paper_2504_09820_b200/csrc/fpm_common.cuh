@@ -84,4 +84,8 @@ FPM_DECLARE_KIND(gen_w)  // everything generic (W != fp64)
 
 void count_launch();
 
+// LMMSE direct comparator (fpm_lmmse.cu): one CTA per realization
+int launch_lmmse(const double2* A, const double2* b, long T, int N, double2* x, int* nonpd,
+                 unsigned long long* nonpd64, cudaStream_t st);
+
 }  // namespace fpm

@@ -150,6 +150,10 @@ __global__ void fpm_slice_kernel(const double2* __restrict__ x, const uint8_t* _
   }
 }
 
+__global__ void fpm_add_counter_kernel(unsigned long long* counters, int idx, unsigned long long v) {
+  atomicAdd(&counters[idx], v);
+}
+
 // ---------------------------------------------------------------------------
 // FP64 issue-rate probe: independent non-fused DMUL/DADD chains (the only DP
 // ops the bit-exact Gram may use).  Gives the denominator of the fp64
@@ -752,6 +756,14 @@ int fpm_cg(const double* A, const double* b, const double* Minv, int64_t T, int3
   return fpm_cg_ex(A, b, Minv, T, N, L, iters, prec, rho_update, x, breakdown_at, diverged_at, nullptr, stream);
 }
 
+int fpm_lmmse(const double* A, const double* b, int64_t T, int32_t N, double* x, int32_t* nonpd, void* stream) {
+  if (T < 0 || N < 1 || !A || !b || !x) return FPM_EINVAL;
+  if (N > kMaxN) return FPM_EUNSUPPORTED;
+  if (T == 0) return FPM_OK;
+  return launch_lmmse(reinterpret_cast<const double2*>(A), reinterpret_cast<const double2*>(b), T, N,
+                      reinterpret_cast<double2*>(x), nonpd, nullptr, (cudaStream_t)stream);
+}
+
 int fpm_slice_count(const double* x, const uint8_t* tx_bits, int64_t T, int32_t N, int32_t qam,
                     uint8_t* rx_bits, int64_t* counters, void* stream) {
   if (T < 0 || N < 1 || !x || !counters || (qam != 16 && qam != 64)) return FPM_EINVAL;
@@ -775,9 +787,12 @@ static int detect_args(const double* H, const double* y, const uint8_t* tx_bits,
   if (iters < 1) return FPM_EINVAL;
   if (rho_update != FPM_RHO_AS_WRITTEN && rho_update != FPM_RHO_TEXTBOOK) return FPM_EINVAL;
   if (qam != 16 && qam != 64) return FPM_EINVAL;
-  if (algorithm != FPM_ALG_CG && algorithm != FPM_ALG_FP_CG && algorithm != FPM_ALG_FP_BJ_CG) return FPM_EINVAL;
+  if (algorithm != FPM_ALG_LMMSE && algorithm != FPM_ALG_CG && algorithm != FPM_ALG_FP_CG &&
+      algorithm != FPM_ALG_FP_BJ_CG)
+    return FPM_EINVAL;
   fpm_precision p64 = {{53, 11, 1}, {53, 11, 1}, {53, 11, 1}};
-  const fpm_precision* pp = algorithm == FPM_ALG_CG ? &p64 : prec;  // detect.py:131-133
+  // detect.py:131-133 (cg and lmmse compute in fp64)
+  const fpm_precision* pp = (algorithm == FPM_ALG_CG || algorithm == FPM_ALG_LMMSE) ? &p64 : prec;
   int rc = check_prec(pp);
   if (rc) return rc;
   const int bj = algorithm == FPM_ALG_FP_BJ_CG;
@@ -807,6 +822,10 @@ static int detect_args(const double* H, const double* y, const uint8_t* tx_bits,
   a.tl = pick_tl(N);
   a.debug = env_int("FPM_DEBUG", 0);
   k = pick_kinds(*pp);
+  if (algorithm == FPM_ALG_LMMSE) {  // Gram + Cholesky kernels, no fused plan
+    a.G.R = 1;
+    return FPM_OK;
+  }
   DetectArgs aw = a;
   ws = plan_detect_ws(M, N, a.L, bj, iters, k.mv, k.ip, aw, sl, grid);
   if (ws) {
@@ -815,6 +834,37 @@ static int detect_args(const double* H, const double* y, const uint8_t* tx_bits,
   }
   if (!plan_detect(M, N, a.L, bj, k.mv, k.ip, a, threads)) return FPM_EUNSUPPORTED;
   return FPM_OK;
+}
+
+// LMMSE comparator on device buffers (detect.py:230-231): Gram -> Cholesky
+// solve per chunk, then the slicer / counters; flags are -1 (no iteration).
+static int run_lmmse(const DetectArgs& a, int M, int N, cudaStream_t st) {
+  const long T = a.T;
+  const long chunk = std::min<long>(T, 8192);
+  double2 *A = nullptr, *b = nullptr;
+  if (cudaMallocAsync(&A, (size_t)chunk * N * N * 16, st) != cudaSuccess) return FPM_ECUDA;
+  if (cudaMallocAsync(&b, (size_t)chunk * N * 16, st) != cudaSuccess) {
+    cudaFreeAsync(A, st);
+    return FPM_ECUDA;
+  }
+  int rc = FPM_OK;
+  for (long c0 = 0; !rc && c0 < T; c0 += chunk) {
+    const long n = std::min(chunk, T - c0);
+    rc = fpm_gram(reinterpret_cast<const double*>(a.H + c0 * (long)M * N), reinterpret_cast<const double*>(a.y + c0 * M),
+                  n, M, N, a.sigma2, reinterpret_cast<double*>(A), reinterpret_cast<double*>(b), st);
+    if (!rc) rc = launch_lmmse(A, b, n, N, a.x + c0 * N, nullptr, a.counters + FPM_CNT_NONPD, st);
+  }
+  cudaFreeAsync(A, st);
+  cudaFreeAsync(b, st);
+  if (rc) return rc;
+  cudaMemsetAsync(a.brk, 0xFF, (size_t)T * 4, st);
+  cudaMemsetAsync(a.div, 0xFF, (size_t)T * 4, st);
+  const long TN = T * (long)N;
+  const long grid = std::min((TN + 255) / 256, 148L * 8);
+  fpm_slice_kernel<<<(unsigned)grid, 256, 0, st>>>(a.x, a.tx, TN, a.rx, a.counters, a.sl);
+  fpm_add_counter_kernel<<<1, 1, 0, st>>>(a.counters, FPM_CNT_TRIALS, (unsigned long long)T);
+  g_launches += 2;
+  return cudaGetLastError() == cudaSuccess ? FPM_OK : FPM_ECUDA;
 }
 
 int fpm_detect(const double* H, const double* y, const uint8_t* tx_bits, int64_t T, int32_t M, int32_t N,
@@ -831,6 +881,7 @@ int fpm_detect(const double* H, const double* y, const uint8_t* tx_bits, int64_t
                        breakdown_at, diverged_at, rx_bits, counters, a, k, threads, ws, sl, grid);
   if (rc) return rc;
   if (T == 0) return FPM_OK;
+  if (algorithm == FPM_ALG_LMMSE) return run_lmmse(a, M, N, (cudaStream_t)stream);
   if (ws) return launch_detect_ws(k, a, sl, grid, (cudaStream_t)stream);
   return launch_detect(k, a, threads, (cudaStream_t)stream);
 }
@@ -902,7 +953,9 @@ int fpm_detect_host(const double* H, const double* y, const uint8_t* tx_bits, in
     b.div = ddv;
     b.rx = rx_bits ? drx : nullptr;
     b.counters = reinterpret_cast<unsigned long long*>(dcnt + s * FPM_NCOUNTERS);
-    if (ws) {
+    if (algorithm == FPM_ALG_LMMSE) {
+      rc = run_lmmse(b, M, N, st[s]);
+    } else if (ws) {
       const int grid = (int)std::min<long>((n + a.G.R - 1) / a.G.R, (long)sm_count() * env_int("FPM_CTAS_PER_SM", 1));
       rc = launch_detect_ws(k, b, sl, grid, st[s]);
     } else {

@@ -103,8 +103,6 @@ def detect(det, H, y, sigma2: float, tx_bits=None, *, qam: int = 16, minv=None, 
     list of (T,Lk,Lk)); default builds them on-chip.  `counters` may be an
     int64 CUDA tensor of length 8 to accumulate into (no host sync)."""
     det = _spec(det)
-    if det.algorithm == "lmmse":
-        raise NotImplementedError("the direct LMMSE comparator is not on the GPU hot path yet")
     torch = _torch()
     host = not _is_torch(H)
     Hd = _to_dev(H, torch.complex128)
@@ -149,8 +147,6 @@ def detect_host(det, H, y, sigma2: float, tx_bits=None, *, qam: int = 16, minv=N
     chunked H2D / kernel / D2H pipeline (fpm_detect_host); use pinned arrays
     for full PCIe rate."""
     det = _spec(det)
-    if det.algorithm == "lmmse":
-        raise NotImplementedError("the direct LMMSE comparator is not on the GPU hot path yet")
     H = np.ascontiguousarray(H, np.complex128)
     y = np.ascontiguousarray(y, np.complex128)
     T, M, N = H.shape

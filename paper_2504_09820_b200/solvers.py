@@ -168,6 +168,24 @@ def build_blocks_batch(A, L: int, *, allow_ragged: bool = False) -> BatchBlocks:
     return BatchBlocks(_out(packed, host), N, L)
 
 
+def solve_direct_batch(A, b):
+    """Batched Cholesky solve x = A^-1 b (linalg.py:223-231,
+    _solve_direct_batch: the LMMSE comparator) on the GPU.  Raises
+    ContractViolation where scipy's cho_factor would fail (non-PD A)."""
+    torch = _torch()
+    host = not _is_torch(b)
+    Ad = _to_dev(A, torch.complex128)
+    bd = _to_dev(b, torch.complex128)
+    T, N = bd.shape
+    x = torch.empty((T, N), dtype=torch.complex128, device=bd.device)
+    bad = torch.zeros((1,), dtype=torch.int32, device=bd.device)
+    _lib.check(_lib.load().fpm_lmmse(Ad.data_ptr(), bd.data_ptr(), T, N, x.data_ptr(), bad.data_ptr(), _stream()),
+               "solve_direct_batch")
+    if int(bad.item()):
+        raise ContractViolation("matrix is not positive definite")
+    return _out(x, host)
+
+
 def _norm2_t(v):
     """norm2 over the trailing axis (linalg.py:122-134) on the device:
     scale = max|v| (NaN-propagating, 1 unless finite and > 0), inf if any |v|

@@ -162,6 +162,24 @@ def _cg_history():
     return out
 
 
+def _lmmse():
+    """The direct comparator (detect.py:230-231 -> linalg.py:223-231) on a
+    c5-shaped and a c2-shaped batch."""
+    from fpmimo.linalg import _solve_direct_batch
+    out = {}
+    for tag, (M, K, zeta, snr, T) in (("c5", (128, 64, 0.5, 15.0, 8)), ("c2", (128, 32, 0.5, 4.0, 8))):
+        ch = ChannelConfig(M=M, K=K, N_UE=1, zeta_r=zeta, zeta_t=zeta)
+        det = DetectorSpec("lmmse")
+        cfg = BERConfig(channel=ch, detectors=(det,), snr_grid=(snr,), trials=T, seed=SEED)
+        batch = simulate_trials(cfg, 0, range(T))
+        x = _solve_direct_batch(batch["A"], batch["b"])
+        got = demodulate_16qam(x)
+        out.update({f"{tag}_H": batch["H_est"], f"{tag}_y": batch["y"], f"{tag}_sigma2": np.float64(batch["sigma_n2"]),
+                    f"{tag}_A": batch["A"], f"{tag}_b": batch["b"], f"{tag}_x": x, f"{tag}_tx_bits": batch["bits"],
+                    f"{tag}_rx_bits": got, f"{tag}_bit_errors": (got != batch["bits"]).sum(-1).astype(np.int64)})
+    return out
+
+
 def main():
     for name, (M, K, zeta, snr, T, kw) in CASES.items():
         d = _detector_case(name, M, K, zeta, snr, T, kw)
@@ -171,6 +189,7 @@ def main():
     np.savez_compressed(os.path.join(OUT, "solver_edges.npz"), **_solver_edge_cases())
     np.savez_compressed(os.path.join(OUT, "kernel_kats.npz"), **_kernel_kats())
     np.savez_compressed(os.path.join(OUT, "hist_cg.npz"), **_cg_history())
+    np.savez_compressed(os.path.join(OUT, "lmmse.npz"), **_lmmse())
     # slicer known answers (detect.py:70-84, tests/test_detect.py:55-69)
     vals = np.array([complex(np.nan, 1.0), complex(np.inf, np.inf), complex(-np.inf, -np.inf),
                      -2 / np.sqrt(10), 0.0, 2 / np.sqrt(10), complex(0.3, -0.9), complex(-0.0, 0.0)])

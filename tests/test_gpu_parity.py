@@ -359,3 +359,40 @@ def test_install_patches_reference_style_module():
     assert prev is sentinel and mod._detect_batch is D._detect_batch
     D.uninstall(mod)
     assert mod._detect_batch is sentinel
+
+
+def _normwise(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    return np.linalg.norm(a - b, axis=-1) / np.maximum(np.linalg.norm(b, axis=-1), 1e-300)
+
+
+def test_lmmse_direct_solve_and_fused_detector():
+    """LMMSE comparator (detect.py:230-231, linalg.py:223-231): x within
+    1e-12 normwise of LAPACK's Cholesky solve (bits of zpotrf are not
+    reproducible); sliced bits and error counts identical."""
+    from paper_2504_09820_b200.detect import DetectorSpec, _detect_batch, detect, detect_host
+    from paper_2504_09820_b200.solvers import solve_direct_batch
+    g = load_golden("lmmse")
+    det = DetectorSpec("lmmse")
+    for tag in ("c5", "c2"):
+        x = solve_direct_batch(g[f"{tag}_A"], g[f"{tag}_b"])
+        assert _normwise(x, g[f"{tag}_x"]).max() <= 1e-12
+        res = detect(det, g[f"{tag}_H"], g[f"{tag}_y"], float(g[f"{tag}_sigma2"]), g[f"{tag}_tx_bits"], want_bits=True)
+        assert _normwise(res.x, g[f"{tag}_x"]).max() <= 1e-12
+        np.testing.assert_array_equal(res.bits, g[f"{tag}_rx_bits"])
+        assert res.counters["bit_errors"] == int(g[f"{tag}_bit_errors"].sum())
+        assert res.counters["trials"] == g[f"{tag}_H"].shape[0]
+        assert (res.diverged_at == -1).all() and (res.breakdown_at == -1).all()
+        hres = detect_host(det, g[f"{tag}_H"], g[f"{tag}_y"], float(g[f"{tag}_sigma2"]), g[f"{tag}_tx_bits"])
+        assert bits_equal(hres.x, res.x) and hres.counters["bit_errors"] == res.counters["bit_errors"]
+        xb, bad = _detect_batch(det, {"H_est": g[f"{tag}_H"], "y": g[f"{tag}_y"], "sigma_n2": g[f"{tag}_sigma2"]})
+        assert bits_equal(xb, res.x) and not bad.any()
+
+
+def test_lmmse_non_pd_raises():
+    from paper_2504_09820_b200.errors import ContractViolation
+    from paper_2504_09820_b200.solvers import solve_direct_batch
+    A = np.eye(4, dtype=np.complex128)[None].repeat(2, 0)
+    A[1, 2, 2] = -1.0
+    with pytest.raises(ContractViolation):
+        solve_direct_batch(A, np.ones((2, 4), np.complex128))

@@ -147,3 +147,12 @@ def test_cg_histories_bit_exact(oracle):
     for k in HIST_KEYS:
         got, want = getattr(out, k), g[f"c5_{k}"]
         assert bits_equal(np.asarray(got, want.dtype), want), k
+
+
+def test_lmmse_restatement_matches_reference(oracle):
+    """linalg.py:223-231 restated (scipy cho_factor / cho_solve) equals the
+    reference's _solve_direct_batch bit for bit on the fixture systems."""
+    g = load_golden("lmmse")
+    for tag in ("c5", "c2"):
+        assert bits_equal(oracle.lmmse(g[f"{tag}_A"], g[f"{tag}_b"]), g[f"{tag}_x"])
+        np.testing.assert_array_equal(oracle.demod16(g[f"{tag}_x"]), g[f"{tag}_rx_bits"])
