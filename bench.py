@@ -100,39 +100,24 @@ def cpu_throughput(prec, per_worker, workers=None):
 # GPU side
 # ---------------------------------------------------------------------------
 
-def _psd_sqrt(n, zeta):
-    import numpy as np
-    idx = np.arange(n)
-    R = zeta ** np.abs(idx[:, None] - idx[None, :])
-    w, V = np.linalg.eigh(R)
-    S = (V * np.sqrt(np.clip(w, 0, None))) @ V.T
-    return 0.5 * (S + S.T)
-
-
-def gen_inputs(T, rank, device, chunk=8192):
-    """Reference channel model (channel.py:138-161, detect.py:189-214) sampled
-    on the GPU: H = sqrt(Rr) W sqrt(Rt), W ~ CN(0, 1/M); 16-QAM Gray bits;
-    y = H s + CN(0, sigma^2)."""
+def gen_inputs(T, rank, device, chunk=8192, trial0=0):
+    """Reference link model (channel.py:138-161, detect.py:189-214) sampled
+    on the GPU by the library's generator (channel.simulate_batch: keyed
+    per-trial Philox streams, so trial t's inputs are the same at any GPU
+    count): H = sqrt(Rr) W sqrt(Rt), W ~ CN(0, 1/M); 16-QAM Gray bits;
+    y = H s + CN(0, sigma^2).  Trials trial0 .. trial0+T-1."""
     import torch
-    Sr = torch.from_numpy(_psd_sqrt(M, ZETA)).to(device=device, dtype=torch.complex128)
-    St = torch.from_numpy(_psd_sqrt(N, ZETA)).to(device=device, dtype=torch.complex128)
+    from paper_2504_09820_b200 import channel
     H = torch.empty((T, M, N), dtype=torch.complex128, device=device)
     y = torch.empty((T, M), dtype=torch.complex128, device=device)
     bits = torch.empty((T, 4 * N), dtype=torch.uint8, device=device)
-    lv = torch.tensor([-3.0, -1.0, 3.0, 1.0], dtype=torch.float64, device=device) / math.sqrt(10.0)
     for c0 in range(0, T, chunk):
         c1 = min(T, c0 + chunk)
-        g = torch.Generator(device=device).manual_seed(SEED * 1000003 + rank * 65537 + c0)
-        W = torch.randn((c1 - c0, M, N), dtype=torch.complex128, device=device, generator=g) / math.sqrt(M)
-        Hc = Sr @ W @ St
-        H[c0:c1] = Hc
-        bt = torch.randint(0, 2, (c1 - c0, 4 * N), dtype=torch.uint8, device=device, generator=g)
-        bits[c0:c1] = bt
-        q = bt.view(c1 - c0, N, 4).long()
-        s = torch.complex(lv[2 * q[..., 0] + q[..., 1]], lv[2 * q[..., 2] + q[..., 3]])
-        noise = torch.randn((c1 - c0, M), dtype=torch.complex128, device=device, generator=g) * math.sqrt(SIGMA2)
-        y[c0:c1] = torch.einsum("tmn,tn->tm", Hc, s) + noise
-        del W, Hc, s, noise, q, bt
+        b = channel.simulate_batch(M, N, ZETA, ZETA, SNR_DB, trial0 + c0, c1 - c0, SEED, device=device)
+        H[c0:c1] = b["H"]
+        y[c0:c1] = b["y"]
+        bits[c0:c1] = b["bits"]
+        del b
     return H, y, bits
 
 
@@ -220,7 +205,7 @@ def run_ours(args):
     if need > free:  # resident pool reused within a step (documented in config)
         pool = 1 << int(math.log2(max(1, (free - (8 << 30)) // (16 * M * N + 16 * M + 4 * N + 16 * N + 8))))
     tg = time.time()
-    H, y, bits = gen_inputs(pool, rank, dev)
+    H, y, bits = gen_inputs(pool, rank, dev, trial0=t0)
     torch.cuda.synchronize()
     gen_s = time.time() - tg
     x = torch.empty((pool, N), dtype=torch.complex128, device=dev)
@@ -318,7 +303,8 @@ def run_ours(args):
             "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": f"f64 work / {args.precision} matvec+inner",
-            "data": "synthetic (reference channel model sampled on GPU: Kronecker zeta=0.5, CN(0,1/M), 16-QAM, AWGN)",
+            "data": "synthetic: the reference's link model sampled on the GPU (fpm_gen_trials keyed Philox streams; "
+                    "Kronecker zeta=0.5, W ~ CN(0,1/M), 16-QAM Gray, AWGN at the reference SNR convention)",
             "config": {"workload": f"c5: FP-BJ-CG L={L}, M={M} x N={N}, zeta={ZETA}, 16-QAM, SNR {SNR_DB} dB, "
                                    f"{ITERS} iters, batch {T_total} realizations/step",
                        "precision": {"work": "fp64", "matvec": args.precision, "inner": args.precision},

@@ -134,6 +134,19 @@ int fpm_cg_ex(const double* A, const double* b, const double* Minv, int64_t T, i
  * to ~1e-13 normwise. */
 int fpm_lmmse(const double* A, const double* b, int64_t T, int32_t N, double* x, int32_t* nonpd, void* stream);
 
+/* Input generation (detect.py:189-214 simulate_trials; channel.py:138-161;
+ * rng.py:19-39): per-trial counter-based Philox4x32-10 streams keyed by
+ * (seed, context, point, trial) -- trial t's draws are independent of the
+ * batch, chunking and device.  Writes, for trials trial0 .. trial0+T-1:
+ *   W     (T, M, N) complex  i.i.d. CN(0, 1/M) core (colour with sqrt(R_r) W sqrt(R_t))
+ *   bits  (T, nbits) uint8   uniform {0, 1} payload (nbits = 4N for 16-QAM)
+ *   noise (T, M)    complex  unit complex normals (scale by sqrt(sigma^2 / 2))
+ *   csi   (T, M, N) complex  unit complex normals for perturb_csi, or NULL
+ * Distribution-level parity: NumPy's Philox / libm stream is not
+ * reproduced.  context < 2^12, point < 2^16 as in rng.py. */
+int fpm_gen_trials(uint64_t seed, int32_t context, int32_t point, int64_t trial0, int64_t T, int32_t M, int32_t N,
+                   int32_t nbits, double* W, uint8_t* bits, double* noise, double* csi, void* stream);
+
 /* qam = 16 (reference) or 64 (extension).  tx_bits / rx_bits: (T, bits*N)
  * uint8 in the reference's layout, both nullable. */
 int fpm_slice_count(const double* x, const uint8_t* tx_bits, int64_t T, int32_t N, int32_t qam,

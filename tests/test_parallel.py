@@ -23,7 +23,7 @@ def _cfg(trials=23, chunk=10):
     dets = (DetectorSpec("fp_cg", iters=4, matvec="fp16", inner="fp16"),
             DetectorSpec("fp_bj_cg", iters=4, L=2, matvec="fp16", inner="fp16"),
             DetectorSpec("cg", iters=3))
-    return SimpleNamespace(channel=SimpleNamespace(M=M, N=N, zeta_t=0.5), detectors=dets,
+    return SimpleNamespace(channel=SimpleNamespace(M=M, N=N, zeta_r=0.5, zeta_t=0.5), detectors=dets,
                            snr_grid=(0.0, 8.0), trials=trials, chunk=chunk, seed=11)
 
 
@@ -145,3 +145,21 @@ def test_gpu_sweep_counters_equal_oracle():
     for cg, cr in zip(gpu, ref):
         for pg, pr in zip(cg.points, cr.points):
             assert (pg.bit_errors, pg.divergence_rate) == (pr.bit_errors, pr.divergence_rate)
+
+
+@pytest.mark.gpu
+def test_gpu_generated_sweep_is_chunk_invariant():
+    """With the keyed per-trial generator (channel.simulate_trials) the sweep's
+    counts do not depend on the chunking -- the property that makes them
+    independent of the GPU count (each rank draws only its own trials)."""
+    import torch
+    from paper_2504_09820_b200 import channel
+    cfg = _cfg(trials=48, chunk=16)
+    cfg.context = 2
+    a = P.sharded_ber_sweep(cfg, channel.simulate_trials, device=torch.device("cuda"))
+    cfg2 = _cfg(trials=48, chunk=40)
+    cfg2.context = 2
+    b = P.sharded_ber_sweep(cfg2, channel.simulate_trials, device=torch.device("cuda"))
+    for ca, cb in zip(a, b):
+        for pa, pb in zip(ca.points, cb.points):
+            assert (pa.bit_errors, pa.divergence_rate) == (pb.bit_errors, pb.divergence_rate)
