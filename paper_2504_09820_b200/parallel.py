@@ -167,9 +167,11 @@ def sharded_ber_sweep(cfg, simulate, *, counts_fn=None, device=None) -> list:
         for di, curve in enumerate(curves):
             errs = int(c[di, be])
             lo_ci, hi_ci = wilson_interval(errs, total_bits)
+            # NumPy scalars like the reference's (detect.py:264-268), so the
+            # artefact writer formats them identically
             curve.points.append(BERPoint(snr_db=float(cfg.snr_grid[snr_idx]), trials=cfg.trials, bit_errors=errs,
-                                         ber=errs / total_bits, ci_low=lo_ci, ci_high=hi_ci,
-                                         divergence_rate=int(c[di, dv]) / cfg.trials))
+                                         ber=np.int64(errs) / total_bits, ci_low=lo_ci, ci_high=hi_ci,
+                                         divergence_rate=np.int64(c[di, dv]) / cfg.trials))
     return curves
 
 

@@ -180,6 +180,29 @@ def _lmmse():
     return out
 
 
+BER_RUN_CFG = {"kind": "ber", "channel": {"M": 16, "K": 4, "zeta_r": 0.3, "zeta_t": 0.3},
+               "detectors": [{"algorithm": "cg", "iters": 4},
+                             {"algorithm": "fp_bj_cg", "L": 2, "matvec": "fp16", "inner": "fp16", "iters": 4},
+                             {"algorithm": "fp_cg", "matvec": "bfloat16", "inner": "bfloat16", "iters": 5,
+                              "label": "fpcg_bf16"},
+                             {"algorithm": "lmmse"}],
+               "run": {"snr_db": [0.0, 6.0], "trials": 40, "chunk": 16}}
+
+
+def _ber_run():
+    """The reference's BER artefacts (experiments.py:353-384) for a small
+    sweep: ber.csv + ber_plotdata_<detector>.csv, written by its own code."""
+    import tempfile
+    from pathlib import Path
+    from fpmimo.experiments import _run_ber
+    out = {}
+    with tempfile.TemporaryDirectory() as d:
+        files = _run_ber(BER_RUN_CFG, Path(d), 7, 1)
+        for f in files:
+            out[f] = (Path(d) / f).read_text()
+    return out
+
+
 def main():
     for name, (M, K, zeta, snr, T, kw) in CASES.items():
         d = _detector_case(name, M, K, zeta, snr, T, kw)
@@ -190,6 +213,10 @@ def main():
     np.savez_compressed(os.path.join(OUT, "kernel_kats.npz"), **_kernel_kats())
     np.savez_compressed(os.path.join(OUT, "hist_cg.npz"), **_cg_history())
     np.savez_compressed(os.path.join(OUT, "lmmse.npz"), **_lmmse())
+    os.makedirs(os.path.join(OUT, "ber_run"), exist_ok=True)
+    for f, text in _ber_run().items():
+        with open(os.path.join(OUT, "ber_run", f), "w") as fh:
+            fh.write(text)
     # slicer known answers (detect.py:70-84, tests/test_detect.py:55-69)
     vals = np.array([complex(np.nan, 1.0), complex(np.inf, np.inf), complex(-np.inf, -np.inf),
                      -2 / np.sqrt(10), 0.0, 2 / np.sqrt(10), complex(0.3, -0.9), complex(-0.0, 0.0)])
