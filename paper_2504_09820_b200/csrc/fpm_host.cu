@@ -912,12 +912,31 @@ int fpm_detect_host(const double* H, const double* y, const uint8_t* tx_bits, in
   const size_t per = align_up(hB, 256) + align_up(yB, 256) + align_up(tB, 256) + align_up(tB, 256) +
                      align_up(xB, 256) + 2 * align_up(fB, 256) + (bj && Minv_in ? align_up(mB, 256) : 0);
   rc = FPM_OK;
+  // stream-ordered allocations from the device's default pool, kept cached
+  // between calls (cudaMalloc / cudaFree of ~1 GB staging per call cost more
+  // than the transfers they stage)
+  {
+    int dev = 0;
+    cudaMemPool_t pool;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+  }
   for (int s = 0; s < 2; ++s) {
     if (cudaStreamCreateWithFlags(&st[s], cudaStreamNonBlocking) != cudaSuccess) return FPM_ECUDA;
-    if (cudaMalloc(&buf[s], per) != cudaSuccess) rc = FPM_ECUDA;
+    if (cudaMallocAsync(&buf[s], per, st[s]) != cudaSuccess) rc = FPM_ECUDA;
   }
-  if (!rc && cudaMalloc(&dcnt, 2 * FPM_NCOUNTERS * sizeof(int64_t)) != cudaSuccess) rc = FPM_ECUDA;
-  if (!rc) cudaMemset(dcnt, 0, 2 * FPM_NCOUNTERS * sizeof(int64_t));
+  if (!rc && cudaMallocAsync(&dcnt, 2 * FPM_NCOUNTERS * sizeof(int64_t), st[0]) != cudaSuccess) rc = FPM_ECUDA;
+  if (!rc) cudaMemsetAsync(dcnt, 0, 2 * FPM_NCOUNTERS * sizeof(int64_t), st[0]);
+  if (!rc) {  // stream 1 must see the zeroed counters and its buffer
+    cudaEvent_t ev;
+    cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    cudaEventRecord(ev, st[0]);
+    cudaStreamWaitEvent(st[1], ev, 0);
+    cudaEventDestroy(ev);
+  }
   for (int64_t c0 = 0, it = 0; !rc && c0 < T; c0 += chunk, ++it) {
     const int s = (int)(it & 1);
     const int64_t n = std::min<int64_t>(chunk, T - c0);
@@ -976,11 +995,13 @@ int fpm_detect_host(const double* H, const double* y, const uint8_t* tx_bits, in
       for (int i = 0; i < FPM_NCOUNTERS; ++i) counters[i] += hc[i] + hc[FPM_NCOUNTERS + i];
   }
   for (int s = 0; s < 2; ++s) {
+    if (buf[s]) cudaFreeAsync(buf[s], st[s]);
+  }
+  if (dcnt) cudaFreeAsync(dcnt, st[0]);
+  for (int s = 0; s < 2; ++s) {
     cudaStreamSynchronize(st[s]);
-    if (buf[s]) cudaFree(buf[s]);
     cudaStreamDestroy(st[s]);
   }
-  if (dcnt) cudaFree(dcnt);
   if (!rc && cudaGetLastError() != cudaSuccess) rc = FPM_ECUDA;
   return rc;
 }
