@@ -23,6 +23,9 @@
 
 namespace fpm {
 
+#ifndef FPM_WIDE_NC_MAX_RS  // unrolled wide sums only when the CG side keeps >= 256 - this registers
+#define FPM_WIDE_NC_MAX_RS 0
+#endif
 #ifndef FPM_GRAM_PIPE
 #define FPM_GRAM_PIPE 1
 #endif
@@ -71,7 +74,7 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const DetectArgs 
   // compile-time N for the CG sums, except for 16-byte (fp64 / generic)
   // matvec terms under the register split: their unrolled sums do not fit the
   // CG warps' 256 - RS registers, the loop versions do
-  constexpr int kCgNC = (NB > 0 && (RS == 0 || sizeof(typename Ar<K>::C) < 16)) ? 4 * NB : 0;
+  constexpr int kCgNC = (NB > 0 && (RS == 0 || RS <= FPM_WIDE_NC_MAX_RS || sizeof(typename Ar<K>::C) < 16)) ? 4 * NB : 0;
   const int nblk = args.bj ? (N + L - 1) / L : 1;
   const int ldA = NB > 0 ? lda_for(N, (int)sizeof(C)) : args.ldA;
 
@@ -584,6 +587,9 @@ FPM_ROW_UNROLL
   if (tid < FPM_NCOUNTERS && cnt[tid]) atomicAdd(&args.counters[tid], cnt[tid]);
 }
 
+#ifndef FPM_WS_GRAM_REGS_WIDE  // 16-byte matvec terms (fp64 / generic): the CG side needs more
+#define FPM_WS_GRAM_REGS_WIDE 136  // measured: c5 fp64 3.57 M (176) -> 3.95 M det/s
+#endif
 #ifndef FPM_WS_GRAM_REGS
 #define FPM_WS_GRAM_REGS 176
 #endif
@@ -597,7 +603,8 @@ int launch_detect_ws_t(const DetectArgs& a, const WsLayout& sl, int grid, cudaSt
     // N = 64, R = 2: 256 Gram threads = two warp groups and a 512-thread
     // block -> register split between the Gram and the other warp groups
     if (a.ws_gt == 256 && threads == 512 && !std::getenv("FPM_WS_NOSPLIT")) {
-      auto k = fpm_detect_ws_kernel<WK, K, NB, LB, FPM_WS_GRAM_REGS>;
+      constexpr int kRS = sizeof(typename Ar<K>::C) >= 16 ? FPM_WS_GRAM_REGS_WIDE : FPM_WS_GRAM_REGS;
+      auto k = fpm_detect_ws_kernel<WK, K, NB, LB, kRS>;
       if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, a.smem_bytes) != cudaSuccess)
         return FPM_ECUDA;
       k<<<(unsigned)grid, 512, a.smem_bytes, st>>>(b, sl);
