@@ -291,7 +291,10 @@ static void gram_geom(int R, int M, int N, GramGeom& G, int stage_kb = 24) {
 }
 
 static int gram_threads(const GramGeom& G) {
-  int t = G.R * G.nb * G.nb / 2;
+  // one thread per Gram job, and at least one thread per 4 matched-filter
+  // chains (gram_run carries <= 4 chains per thread; small N has more chains
+  // than jobs)
+  const int t = std::max(G.R * G.nb * G.nb / 2, (2 * G.R * G.N + 3) / 4);
   return (t + 31) / 32 * 32;
 }
 
@@ -389,99 +392,104 @@ static bool plan_detect_ws(int M, int N, int L, int bj, int iters, int mvk, int 
   if (std::getenv("FPM_NO_WS")) return false;
   const int Np = (N + 7) / 8 * 8, nb = Np / 4, Cc = nb * (nb / 2 - 1);
   const int limit = max_smem_optin();
-  int best = -1;
-  for (int R = 64; R >= 1; R /= 2) {
+  // the CG group takes the threads left of a 512-thread block (rows beyond
+  // its width loop), so two Gram warps per SM sub-partition (gt = 256) win
+  // over one CG thread per row
+  auto cg_threads = [&](int R, int gt) { return 512 - gt - 32; };
+  // largest R whose thread layout works, falling back to smaller R when the
+  // shared memory does not fit
+  auto try_R = [&](const int R) -> bool {
+    const int Lb = bj ? L : 1;
     const int gt = R * nb * nb / 2;
-    const int ct = (R * N + 31) / 32 * 32 + 32;
-    if (gt > 384 || gt + ct > 512 || gt < 32) continue;
-    if ((R * Cc) % 32 || (R * nb) % 32) continue;
-    if (env_int("FPM_R", 0) && env_int("FPM_R", 0) != R) continue;
-    best = R;
-    break;
-  }
-  if (best < 0) return false;
-  const int R = best;
-  const int Lb = bj ? L : 1;
-  const int gt = R * nb * nb / 2;
-  // two CG groups (alternating hand-off slots) when the Gram side is two full
-  // warp groups: 512 threads = 256 Gram + 32 producer + 128 + 96 CG
-  const int ncg_env = env_int("FPM_WS_NCG", 0);
-  const int stage_list[] = {24, 20, 16, 12, 8, 4};
-  // candidates (CG groups, hand-off slots).  When one CG pass is shorter
-  // than one Gram pass (few sweeps relative to the antenna rows; measured:
-  // c5 fp16 CG 84 K vs Gram 89 K cycles per group) a single CG group on a
-  // single slot keeps up and leaves the most shared memory to the H ring;
-  // otherwise two CG groups on alternating slots, then fallbacks.
-  const bool cg_short = (long)iters * N <= 8L * M && mvk != FK_F64;
-  const int cand_short[4][2] = {{1, 1}, {2, 2}, {1, 2}, {1, 1}};
-  const int cand_long[4][2] = {{2, 2}, {1, 2}, {1, 1}, {1, 1}};
-  const int(*cand)[2] = cg_short ? cand_short : cand_long;
-  const int stage_short[6] = {32, 24, 20, 16, 12, 8};
-  for (int ci = 0; ci < 4; ++ci) {
-    const int ncg = cand[ci][0], nslot = cand[ci][1];
-    if (ncg == 2 && gt != 256) continue;
-    if (ncg_env && ncg != ncg_env) continue;
-    if (env_int("FPM_WS_NSLOT", 0) && nslot != env_int("FPM_WS_NSLOT", 0)) continue;
-    for (int si = 0; si < 6; ++si) {
-      const int stage_kb = env_int("FPM_STAGE_KB", 0) ? env_int("FPM_STAGE_KB", 0)
-                           : (ncg == 1 && nslot == 1 && cg_short ? stage_short[si] : stage_list[si]);
-      if (env_int("FPM_STAGE_KB", 0) && si > 0) break;
-      GramGeom G;
-      gram_geom(R, M, N, G, stage_kb);
-      G.S = std::max(3, G.S);  // the producer refills two chunks behind
-      const int ldA = lda_for(N, mv_bytes(mvk));
-      size_t off = 256;  // mbarriers: full[S], empty[S], ybar, sfull, sempty, ydone [2 each]
-      if ((2 * G.S + 8) * 8 > 256) continue;
-      a.off_union = (int)off;  // H stage ring
-      off = align_up(off + (size_t)G.S * R * G.MC * G.Np * 16, 128);
-      a.off_ys = (int)off;
-      off = align_up(off + (size_t)2 * R * M * 16, 128);
-      sl.at = 0;
-      sl.b = (int)align_up((size_t)R * N * ldA * mv_bytes(mvk), 128);
-      sl.d = (int)align_up(sl.b + (size_t)R * N * 16, 128);
-      sl.bytes = (int)align_up(sl.d + (bj ? (size_t)R * N * Lb * 16 : 0), 128);
-      a.off_slot = (int)off;
-      off = align_up(off + (size_t)nslot * sl.bytes, 128);
-      a.off_bsm = (int)off;  // matched-filter chain accumulators
-      off = align_up(off + (size_t)2 * R * N * 8, 128);
-      // ---- per-CG-group state (replicated ncg times, cg_stride apart) ----
-      const size_t cg0 = off;
-      a.off_minv = (int)off;
-      off = align_up(off + (bj ? (size_t)R * N * Lb * 16 : 0), 128);
-      a.off_vec = (int)off;
-      off = align_up(off + (size_t)8 * R * N * 16, 128);
-      // the inverse's scratch is dead before the CG vectors are initialised
-      if (!bj || Lb <= 8) {
-        a.off_scr2 = a.off_vec;
-      } else {
-        a.off_scr2 = (int)off;
-        off = align_up(off + (size_t)R * N * Lb * 16, 128);
-      }
-      a.off_pmv = (int)off;
-      off = align_up(off + (size_t)R * N * p_bytes(mvk), 128);
-      a.off_tip = (int)off;
-      off = align_up(off + (size_t)4 * R * N * mv_bytes(ipk), 128);
-      a.off_sc = (int)off;
-      off = align_up(off + (size_t)R * 8 * 16, 128);
-      a.off_fl = (int)off;
-      off = align_up(off + (size_t)R * 4 * 4, 128);
-      a.cg_stride = (int)(off - cg0);
-      off += (size_t)(ncg - 1) * a.cg_stride;
-      if ((long)off + 1024 <= limit) {
-        a.G = G;
-        a.ldA = ldA;
-        a.smem_bytes = (int)off;
-        a.ws_gt = gt;
-        a.ws_ct = gt == 256 ? 224 : (R * N + 31) / 32 * 32 + 32;
-        a.ws_ncg = ncg;
-        a.ws_ct0 = ncg == 2 ? 128 : a.ws_ct;
-        a.ws_nslot = nslot;
-        a.ws_order = ncg == 1 ? 1 : 0;  // measured: CG-first for one group, Gram-first for two
-        const long ngroups = (a.T + R - 1) / R;
-        grid = (int)std::min<long>(ngroups, (long)sm_count() * env_int("FPM_CTAS_PER_SM", 1));
-        return true;
+    // two CG groups (alternating hand-off slots) when the Gram side is two full
+    // warp groups: 512 threads = 256 Gram + 32 producer + 128 + 96 CG
+    const int ncg_env = env_int("FPM_WS_NCG", 0);
+    const int stage_list[] = {24, 20, 16, 12, 8, 4};
+    // candidates (CG groups, hand-off slots).  When one CG pass is shorter
+    // than one Gram pass (few sweeps relative to the antenna rows; measured:
+    // c5 fp16 CG 84 K vs Gram 89 K cycles per group) a single CG group on a
+    // single slot keeps up and leaves the most shared memory to the H ring;
+    // otherwise two CG groups on alternating slots, then fallbacks.
+    const bool cg_short = (long)iters * N <= 8L * M && mvk != FK_F64;
+    const int cand_short[4][2] = {{1, 1}, {2, 2}, {1, 2}, {1, 1}};
+    const int cand_long[4][2] = {{2, 2}, {1, 2}, {1, 1}, {1, 1}};
+    const int(*cand)[2] = cg_short ? cand_short : cand_long;
+    const int stage_short[6] = {32, 24, 20, 16, 12, 8};
+    for (int ci = 0; ci < 4; ++ci) {
+      const int ncg = cand[ci][0], nslot = cand[ci][1];
+      if (ncg == 2 && gt != 256) continue;
+      if (ncg_env && ncg != ncg_env) continue;
+      if (env_int("FPM_WS_NSLOT", 0) && nslot != env_int("FPM_WS_NSLOT", 0)) continue;
+      for (int si = 0; si < 6; ++si) {
+        const int stage_kb = env_int("FPM_STAGE_KB", 0) ? env_int("FPM_STAGE_KB", 0)
+                             : (ncg == 1 && nslot == 1 && cg_short ? stage_short[si] : stage_list[si]);
+        if (env_int("FPM_STAGE_KB", 0) && si > 0) break;
+        GramGeom G;
+        gram_geom(R, M, N, G, stage_kb);
+        G.S = std::max(3, G.S);  // the producer refills two chunks behind
+        const int ldA = lda_for(N, mv_bytes(mvk));
+        size_t off = 256;  // mbarriers: full[S], empty[S], ybar, sfull, sempty, ydone [2 each]
+        if ((2 * G.S + 8) * 8 > 256) continue;
+        a.off_union = (int)off;  // H stage ring
+        off = align_up(off + (size_t)G.S * R * G.MC * G.Np * 16, 128);
+        a.off_ys = (int)off;
+        off = align_up(off + (size_t)2 * R * M * 16, 128);
+        sl.at = 0;
+        sl.b = (int)align_up((size_t)R * N * ldA * mv_bytes(mvk), 128);
+        sl.d = (int)align_up(sl.b + (size_t)R * N * 16, 128);
+        sl.bytes = (int)align_up(sl.d + (bj ? (size_t)R * N * Lb * 16 : 0), 128);
+        a.off_slot = (int)off;
+        off = align_up(off + (size_t)nslot * sl.bytes, 128);
+        a.off_bsm = (int)off;  // matched-filter chain accumulators
+        off = align_up(off + (size_t)2 * R * N * 8, 128);
+        // ---- per-CG-group state (replicated ncg times, cg_stride apart) ----
+        const size_t cg0 = off;
+        a.off_minv = (int)off;
+        off = align_up(off + (bj ? (size_t)R * N * Lb * 16 : 0), 128);
+        a.off_vec = (int)off;
+        off = align_up(off + (size_t)8 * R * N * 16, 128);
+        // the inverse's scratch is dead before the CG vectors are initialised
+        if (!bj || Lb <= 8) {
+          a.off_scr2 = a.off_vec;
+        } else {
+          a.off_scr2 = (int)off;
+          off = align_up(off + (size_t)R * N * Lb * 16, 128);
+        }
+        a.off_pmv = (int)off;
+        off = align_up(off + (size_t)R * N * p_bytes(mvk), 128);
+        a.off_tip = (int)off;
+        off = align_up(off + (size_t)4 * R * N * mv_bytes(ipk), 128);
+        a.off_sc = (int)off;
+        off = align_up(off + (size_t)R * 8 * 16, 128);
+        a.off_fl = (int)off;
+        off = align_up(off + (size_t)R * 4 * 4, 128);
+        a.cg_stride = (int)(off - cg0);
+        off += (size_t)(ncg - 1) * a.cg_stride;
+        if ((long)off + 1024 <= limit) {
+          a.G = G;
+          a.ldA = ldA;
+          a.smem_bytes = (int)off;
+          a.ws_gt = gt;
+          a.ws_ct = cg_threads(R, gt);
+          a.ws_ncg = ncg;
+          a.ws_ct0 = ncg == 2 ? 128 : a.ws_ct;
+          a.ws_nslot = nslot;
+          a.ws_order = ncg == 1 ? 1 : 0;  // measured: CG-first for one group, Gram-first for two
+          const long ngroups = (a.T + R - 1) / R;
+          grid = (int)std::min<long>(ngroups, (long)sm_count() * env_int("FPM_CTAS_PER_SM", 1));
+          return true;
+        }
       }
     }
+    return false;
+  };
+  for (int R = 64; R >= 1; R /= 2) {
+    const int gt = R * nb * nb / 2;
+    const int ct = cg_threads(R, gt);
+    if (gt > 384 || ct < 64 || gt < 32) continue;
+    if ((R * Cc) % 32 || (R * nb) % 32) continue;
+    if (env_int("FPM_R", 0) && env_int("FPM_R", 0) != R) continue;
+    if (try_R(R)) return true;
   }
   return false;
 }

@@ -396,3 +396,25 @@ def test_lmmse_non_pd_raises():
     A[1, 2, 2] = -1.0
     with pytest.raises(ContractViolation):
         solve_direct_batch(A, np.ones((2, 4), np.complex128))
+
+
+@pytest.mark.parametrize("M,N", [(16, 8), (24, 8), (32, 16), (64, 32)])
+def test_small_n_all_paths_against_oracle(oracle, M, N, monkeypatch):
+    """Small N (more matched-filter chains than Gram jobs) through the
+    persistent kernel, the fallback fused kernel and the standalone Gram,
+    plain CG fp64 and FP-CG fp16, against the oracle bit for bit."""
+    from paper_2504_09820_b200.detect import DetectorSpec, detect, gram_mf
+    O = oracle
+    T = 40
+    H, y, bits, s2 = O.simulate(M, N, 0.5, 4.0, range(T), 11)
+    A, b = O.gram_mf(H, y, s2)
+    Ag, bg = gram_mf(H, y, s2)
+    assert bits_equal(Ag, A) and bits_equal(bg, b)
+    for no_ws in (False, True):
+        if no_ws:
+            monkeypatch.setenv("FPM_NO_WS", "1")
+        for alg, mv in (("cg", O.FP64), ("fp_cg", O.FP16)):
+            det = DetectorSpec(alg, iters=4, **({} if alg == "cg" else dict(matvec="fp16", inner="fp16")))
+            r = detect(det, H, y, s2, bits)
+            _, _, _, out = O.detect(H, y, s2, alg, 4, None, O.FP64, mv, mv)
+            assert bits_equal(r.x, out.x), (alg, no_ws)

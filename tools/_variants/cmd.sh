@@ -1,4 +1,2 @@
-for v in w128l w120l; do
-  E="FPM_LIB=tools/_variants/lib_$v.so"
-  echo "== $v"; env $E timeout 300 python tools/cfgbench.py --only c5_fp64 2>&1 | tail -1
-done
+python -m pytest tests -m gpu -x -q 2>&1 | tail -25 | grep -v "^$" | head -30
+python tools/cfgbench.py 2>&1 | grep -v "^$"
