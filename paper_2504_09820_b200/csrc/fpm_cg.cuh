@@ -65,12 +65,13 @@ struct CgSmem {
 };
 
 // Owner of the sequential sums of slot g (which = 0: phi/rho1/carry,
-// 1: as_written rho0): past the matvec rows when possible, one warp apart.
-__device__ __forceinline__ int dot_owner(int g, int which, int rows, int nthreads) {
+// 1: as_written rho0).  One warp apart and past the matvec rows when all
+// 2*Rv owners fit that way, else the last 2*Rv threads; distinct threads in
+// both cases (a thread owns at most one chain; 2*Rv <= nthreads).
+__device__ __forceinline__ int dot_owner(int g, int which, int rows, int nthreads, int Rv) {
   const int k = g * 2 + which;
-  const int cand = nthreads - 1 - 32 * k;
-  if (cand >= rows && cand >= 0) return cand;
-  return (nthreads - 1 - k) % nthreads;
+  if (nthreads - 1 - 32 * (2 * Rv - 1) >= rows) return nthreads - 1 - 32 * k;
+  return nthreads - 1 - k;
 }
 
 // 16-byte shared-memory vector loads of consecutive elements: V16<T>::n
@@ -420,8 +421,8 @@ __device__ void cg_group(CgSmem<K>& S, int Rv, int iters, bool bj, bool textbook
   int og = -1, ow = 0;
 #pragma unroll 1
   for (int g = 0; g < Rv; ++g) {
-    if (dot_owner(g, 0, RN, nthreads) == tid) og = g, ow = 0;
-    if (dot_owner(g, 1, RN, nthreads) == tid) og = g, ow = 1;
+    if (dot_owner(g, 0, RN, nthreads, Rv) == tid) og = g, ow = 0;
+    if (dot_owner(g, 1, RN, nthreads, Rv) == tid) og = g, ow = 1;
   }
   // u_IP value of a binary64 (work) value / of a value already on the u_MV grid
   // (native kinds: u_IP == u_MV, so the matvec's rounding of p is reused)

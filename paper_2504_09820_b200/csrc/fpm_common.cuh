@@ -46,6 +46,7 @@ struct DetectArgs {
   int cg_stride;       // bytes between the two CG groups' state regions
   int ws_nslot;        // hand-off slots (2 double-buffered, 1 when two do not fit)
   int debug;  // diagnostic bits (FPM_DEBUG): 1 = WS kernel skips the CG side
+  int composed;  // no fused plan fits: fpm_gram -> fpm_bj_setup -> fpm_cg -> slicer
 };
 
 struct WsLayout;  // fpm_detect_ws.cuh
@@ -64,6 +65,10 @@ struct CgArgs {
   int off_minv, off_vec, off_pmv, off_tip, off_sc, off_fl;
   CgHist h;
   long long* trace;  // nullable: phase clock stamps of CTA 0 (diagnostic)
+  // non-null: A already on the u_MV grid in global memory ((T, N, N), pitch
+  // N, C layout) -- the matrix does not fit shared memory (16-byte matvec
+  // terms at large N); rows are read through L2 every sweep
+  const void* a_glob;
 };
 
 // Launchers (return FPM_* codes).  nb / lb: compile-time specialisation
@@ -83,6 +88,9 @@ FPM_DECLARE_KIND(gen_w)  // everything generic (W != fp64)
 #undef FPM_DECLARE_KIND
 
 void count_launch();
+
+// A -> A rounded to a generic matvec format, C layout (global-A CG mode)
+int launch_round_mv_gen(const double2* A, double2* out, long n, FmtP f, cudaStream_t st);
 
 // LMMSE direct comparator (fpm_lmmse.cu): one CTA per realization
 int launch_lmmse(const double2* A, const double2* b, long T, int N, double2* x, int* nonpd,

@@ -263,8 +263,9 @@ __global__ void __launch_bounds__(256) fpm_cg_kernel(const CgArgs args) {
   S.R = args.R;
   S.N = N;
   S.L = args.bj ? args.L : 1;
-  S.ldA = args.ldA;
-  S.At = reinterpret_cast<C*>(smem);
+  S.ldA = args.a_glob ? N : args.ldA;
+  S.At = args.a_glob ? const_cast<C*>(reinterpret_cast<const C*>(args.a_glob)) + t0 * (long)N * N
+                     : reinterpret_cast<C*>(smem);
   S.minv = reinterpret_cast<double2*>(smem + args.off_minv);
   double2* vec = reinterpret_cast<double2*>(smem + args.off_vec);
   const int RN = args.R * N;
@@ -288,7 +289,7 @@ __global__ void __launch_bounds__(256) fpm_cg_kernel(const CgArgs args) {
   // 8 streaming loads in flight per thread (the copy is HBM-latency bound
   // with one outstanding load per thread)
   const int NN = N * N;
-  {
+  if (!args.a_glob) {
     constexpr int U = 8;
     const double2* Ag = args.A + t0 * (long)NN;
     const int tot = Rv * NN;

@@ -154,6 +154,22 @@ __global__ void fpm_add_counter_kernel(unsigned long long* counters, int idx, un
   atomicAdd(&counters[idx], v);
 }
 
+__global__ void fpm_count_flags_kernel(const int* brk, const int* div, long T, unsigned long long* counters) {
+  unsigned long long nb = 0, nd = 0;
+  for (long t = (long)blockIdx.x * blockDim.x + threadIdx.x; t < T; t += (long)gridDim.x * blockDim.x) {
+    nb += brk[t] >= 0;
+    nd += div[t] >= 0;
+  }
+  for (int off = 16; off; off >>= 1) {
+    nb += __shfl_xor_sync(0xffffffffu, nb, off);
+    nd += __shfl_xor_sync(0xffffffffu, nd, off);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (nb) atomicAdd(&counters[FPM_CNT_BREAKDOWN], nb);
+    if (nd) atomicAdd(&counters[FPM_CNT_DIVERGED], nd);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // FP64 issue-rate probe: independent non-fused DMUL/DADD chains (the only DP
 // ops the bit-exact Gram may use).  Gives the denominator of the fp64
@@ -346,13 +362,13 @@ static bool plan_detect(int M, int N, int L, int bj, int mvk, int ipk, DetectArg
   return false;
 }
 
-static bool plan_cg(int N, int L, int bj, int mvk, int ipk, CgArgs& a, int& smem) {
+static bool plan_cg(int N, int L, int bj, int mvk, int ipk, CgArgs& a, int& smem, bool aglob = false) {
   const int limit = std::min(max_smem_optin(), 110 * 1024);  // aim for >= 2 CTAs / SM
   int R = std::max(1, 256 / N);
   for (; R >= 1; R = (R > 1 ? R / 2 : 0)) {
     const int ldA = lda_for(N, mv_bytes(mvk));
     size_t off = 0;
-    off = align_up(off + (size_t)R * N * ldA * mv_bytes(mvk), 128);
+    if (!aglob) off = align_up(off + (size_t)R * N * ldA * mv_bytes(mvk), 128);
     a.off_minv = (int)off;
     off = align_up(off + (bj ? (size_t)R * N * L * 16 : 0), 128);
     a.off_vec = (int)off;
@@ -754,8 +770,27 @@ int fpm_cg_ex(const double* A, const double* b, const double* Minv, int64_t T, i
     a.h.on = a.h.res || a.h.xn || a.h.al || a.h.be || a.h.conv || a.h.xit || a.h.rit;
   }
   int smem = 0;
-  if (!plan_cg(N, a.L, bj, k.mv, k.ip, a, smem)) return FPM_EUNSUPPORTED;
-  return launch_cg(k, a, smem, (cudaStream_t)stream);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (plan_cg(N, a.L, bj, k.mv, k.ip, a, smem)) return launch_cg(k, a, smem, st);
+  // A at u_MV does not fit shared memory (16-byte terms at large N): keep it
+  // in global memory, pre-rounded (fp64 is already on its own grid)
+  if (mv_bytes(k.mv) != 16 || !plan_cg(N, a.L, bj, k.mv, k.ip, a, smem, true)) return FPM_EUNSUPPORTED;
+  double2* tmp = nullptr;
+  if (k.mv == FK_F64) {
+    a.a_glob = A;
+  } else {
+    const long n = T * (long)N * N;
+    if (cudaMallocAsync(&tmp, (size_t)n * 16, st) != cudaSuccess) return FPM_ECUDA;
+    const int rr = launch_round_mv_gen(reinterpret_cast<const double2*>(A), tmp, n, a.pr.mv, st);
+    if (rr) {
+      cudaFreeAsync(tmp, st);
+      return rr;
+    }
+    a.a_glob = tmp;
+  }
+  const int rl = launch_cg(k, a, smem, st);
+  if (tmp) cudaFreeAsync(tmp, st);
+  return rl;
 }
 
 int fpm_cg(const double* A, const double* b, const double* Minv, int64_t T, int32_t N, int32_t L, int32_t iters,
@@ -840,7 +875,7 @@ static int detect_args(const double* H, const double* y, const uint8_t* tx_bits,
     a = aw;
     return FPM_OK;
   }
-  if (!plan_detect(M, N, a.L, bj, k.mv, k.ip, a, threads)) return FPM_EUNSUPPORTED;
+  if (!plan_detect(M, N, a.L, bj, k.mv, k.ip, a, threads)) a.composed = 1;  // e.g. fp64 matvec at N = 128
   return FPM_OK;
 }
 
@@ -875,6 +910,50 @@ static int run_lmmse(const DetectArgs& a, int M, int N, cudaStream_t st) {
   return cudaGetLastError() == cudaSuccess ? FPM_OK : FPM_ECUDA;
 }
 
+// No fused plan fits (16-byte matvec terms at N = 128): the same detector
+// composed from the standalone kernels, chunk by chunk; identical results.
+static int run_composed(const DetectArgs& a, int M, int N, int algorithm, int L, int iters, const fpm_precision* pp,
+                        int rho_update, cudaStream_t st) {
+  const long T = a.T;
+  const bool bj = algorithm == FPM_ALG_FP_BJ_CG;
+  const long chunk = std::min<long>(T, 2048);
+  double2 *A = nullptr, *b = nullptr, *mv = nullptr;
+  int rc = FPM_OK;
+  if (cudaMallocAsync(&A, (size_t)chunk * N * N * 16, st) != cudaSuccess ||
+      cudaMallocAsync(&b, (size_t)chunk * N * 16, st) != cudaSuccess ||
+      (bj && !a.minv_in && cudaMallocAsync(&mv, (size_t)chunk * N * L * 16, st) != cudaSuccess))
+    rc = FPM_ECUDA;
+  for (long c0 = 0; !rc && c0 < T; c0 += chunk) {
+    const long n = std::min(chunk, T - c0);
+    rc = fpm_gram(reinterpret_cast<const double*>(a.H + c0 * (long)M * N), reinterpret_cast<const double*>(a.y + c0 * M),
+                  n, M, N, a.sigma2, reinterpret_cast<double*>(A), reinterpret_cast<double*>(b), st);
+    const double2* minv = nullptr;
+    if (!rc && bj) {
+      if (a.minv_in) {
+        minv = a.minv_in + c0 * (long)N * L;
+      } else {
+        rc = fpm_bj_setup(reinterpret_cast<const double*>(A), n, N, L, 0, reinterpret_cast<double*>(mv), nullptr, st);
+        minv = mv;
+      }
+    }
+    if (!rc)
+      rc = fpm_cg_ex(reinterpret_cast<const double*>(A), reinterpret_cast<const double*>(b),
+                     reinterpret_cast<const double*>(minv), n, N, bj ? L : 1, iters, pp, rho_update,
+                     reinterpret_cast<double*>(a.x + c0 * N), a.brk + c0, a.div + c0, nullptr, st);
+  }
+  if (A) cudaFreeAsync(A, st);
+  if (b) cudaFreeAsync(b, st);
+  if (mv) cudaFreeAsync(mv, st);
+  if (rc) return rc;
+  const long TN = T * (long)N;
+  fpm_slice_kernel<<<(unsigned)std::min((TN + 255) / 256, 148L * 8), 256, 0, st>>>(a.x, a.tx, TN, a.rx, a.counters,
+                                                                                 a.sl);
+  fpm_count_flags_kernel<<<(unsigned)std::min((T + 255) / 256, 148L * 4), 256, 0, st>>>(a.brk, a.div, T, a.counters);
+  fpm_add_counter_kernel<<<1, 1, 0, st>>>(a.counters, FPM_CNT_TRIALS, (unsigned long long)T);
+  g_launches += 3;
+  return cudaGetLastError() == cudaSuccess ? FPM_OK : FPM_ECUDA;
+}
+
 int fpm_detect(const double* H, const double* y, const uint8_t* tx_bits, int64_t T, int32_t M, int32_t N,
                double sigma2, int32_t algorithm, int32_t L, int32_t iters, const fpm_precision* prec,
                int32_t rho_update, int32_t qam, const double* Minv_in, double* x, int32_t* breakdown_at,
@@ -890,6 +969,11 @@ int fpm_detect(const double* H, const double* y, const uint8_t* tx_bits, int64_t
   if (rc) return rc;
   if (T == 0) return FPM_OK;
   if (algorithm == FPM_ALG_LMMSE) return run_lmmse(a, M, N, (cudaStream_t)stream);
+  if (a.composed) {
+    fpm_precision p64 = {{53, 11, 1}, {53, 11, 1}, {53, 11, 1}};
+    return run_composed(a, M, N, algorithm, L, iters, algorithm == FPM_ALG_CG ? &p64 : prec, rho_update,
+                        (cudaStream_t)stream);
+  }
   if (ws) return launch_detect_ws(k, a, sl, grid, (cudaStream_t)stream);
   return launch_detect(k, a, threads, (cudaStream_t)stream);
 }
@@ -982,6 +1066,9 @@ int fpm_detect_host(const double* H, const double* y, const uint8_t* tx_bits, in
     b.counters = reinterpret_cast<unsigned long long*>(dcnt + s * FPM_NCOUNTERS);
     if (algorithm == FPM_ALG_LMMSE) {
       rc = run_lmmse(b, M, N, st[s]);
+    } else if (a.composed) {
+      fpm_precision p64 = {{53, 11, 1}, {53, 11, 1}, {53, 11, 1}};
+      rc = run_composed(b, M, N, algorithm, L, iters, algorithm == FPM_ALG_CG ? &p64 : prec, rho_update, st[s]);
     } else if (ws) {
       const int grid = (int)std::min<long>((n + a.G.R - 1) / a.G.R, (long)sm_count() * env_int("FPM_CTAS_PER_SM", 1));
       rc = launch_detect_ws(k, b, sl, grid, st[s]);

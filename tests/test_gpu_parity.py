@@ -418,3 +418,84 @@ def test_small_n_all_paths_against_oracle(oracle, M, N, monkeypatch):
             r = detect(det, H, y, s2, bits)
             _, _, _, out = O.detect(H, y, s2, alg, 4, None, O.FP64, mv, mv)
             assert bits_equal(r.x, out.x), (alg, no_ws)
+
+
+SHAPES = [  # (M, N, L) -- N multiples of 4 and not, L dividing N; every kernel geometry
+    (8, 4, 2), (20, 8, 4), (33, 12, 3), (40, 16, 4), (41, 20, 5), (64, 24, 6), (70, 28, 4), (96, 32, 8),
+    (100, 40, 8), (128, 48, 4), (130, 56, 7), (160, 64, 8), (200, 80, 8), (256, 96, 8), (300, 128, 8),
+]
+
+
+@pytest.mark.parametrize("M,N,L", SHAPES)
+def test_shape_sweep_fused_detector_bit_exact(oracle, M, N, L):
+    """Every (M, N, L) geometry class through the fused detector, plain fp16
+    FP-CG and fp16 FP-BJ-CG with injected inverses, against the oracle bit
+    for bit; partial realization groups included (T odd)."""
+    from paper_2504_09820_b200.detect import DetectorSpec, detect
+    O = oracle
+    T = 37
+    H, y, bits, s2 = O.simulate(M, N, 0.4, 8.0, range(T), 5)
+    A, b = O.gram_mf(H, y, s2)
+    mats = O.bj_inverses(A, L)
+    for alg, mt in (("fp_cg", None), ("fp_bj_cg", mats)):
+        det = DetectorSpec(alg, iters=5, L=L if alg == "fp_bj_cg" else None, matvec="fp16", inner="fp16")
+        ref = O.cg_batch(A, b, 5, O.FP64, O.FP16, O.FP16, mt)
+        res = detect(det, H, y, s2, bits, minv=mt, want_bits=True)
+        assert bits_equal(res.x, ref.x), (alg, M, N, L)
+        np.testing.assert_array_equal(res.breakdown_at, ref.breakdown_at)
+        np.testing.assert_array_equal(res.bits, O.demod16(ref.x))
+
+
+@pytest.mark.parametrize("M,N,L", SHAPES[::2])
+@pytest.mark.parametrize("fmt", ["fp64", "fp32", "bfloat16", "p6e4"])
+def test_shape_sweep_formats_gram_and_run_batch(oracle, M, N, L, fmt):
+    """Gram (fpm_gram) and run_batch (fpm_cg) across the geometry classes for
+    every matvec/inner kind (native fp64 / fp32 / bf16 and a generic
+    emulated (6, 4) format), textbook and as-written BJ, bit for bit."""
+    from paper_2504_09820_b200.formats import get_format, make_format
+    from paper_2504_09820_b200.detect import gram_mf
+    from paper_2504_09820_b200.solvers import PrecisionConfig, run_batch
+    O = oracle
+    T = 21
+    H, y, bits, s2 = O.simulate(M, N, 0.4, 8.0, range(T), 9)
+    A, b = O.gram_mf(H, y, s2)
+    Ag, bg = gram_mf(H, y, s2)
+    assert bits_equal(Ag, A) and bits_equal(bg, b)
+    f = make_format(6, 4) if fmt == "p6e4" else get_format(fmt)
+    of = O.Fmt("p6e4", 6, 4) if fmt == "p6e4" else O.REGISTRY[fmt]
+    mats = O.bj_inverses(A, L)
+    for rv in ("as_written", "textbook"):
+        ref = O.cg_batch(A, b, 4, O.FP64, of, of, mats, rho_update=rv)
+        res = run_batch(A, b, 4, PrecisionConfig(matvec=f, inner=f), _pack(mats, N, L), rho_update=rv)
+        assert bits_equal(res.x, ref.x), (fmt, rv)
+        np.testing.assert_array_equal(res.diverged_at, ref.diverged_at)
+
+
+def _pack(mats, N, L):
+    from paper_2504_09820_b200.solvers import BatchBlocks, pack_blocks
+    return BatchBlocks(pack_blocks(mats, N, L), N, L)
+
+
+def test_composed_path_fp64_matvec_at_n128(oracle):
+    """fp64 matvec at N = 128 (c4 shape): A at u_MV does not fit shared
+    memory, so the detector composes fpm_gram -> fpm_bj_setup -> fpm_cg with
+    A read from global memory; bit-exact with injected inverses, identical
+    bits with on-chip ones (tolerance on x)."""
+    from paper_2504_09820_b200.detect import DetectorSpec, detect, detect_host
+    O = oracle
+    M, N, L, T = 256, 128, 8, 6
+    H, y, bits, s2 = O.simulate(M, N, 0.5, 20.0, range(T), 3)
+    A, b = O.gram_mf(H, y, s2)
+    mats = O.bj_inverses(A, L)
+    det = DetectorSpec("fp_bj_cg", iters=4, L=L)
+    ref = O.cg_batch(A, b, 4, O.FP64, O.FP64, O.FP64, mats)
+    r = detect(det, H, y, s2, bits, minv=mats, want_bits=True)
+    assert bits_equal(r.x, ref.x)
+    np.testing.assert_array_equal(r.bits, O.demod16(ref.x))
+    assert r.counters["trials"] == T
+    r2 = detect(det, H, y, s2, bits, want_bits=True)
+    rel = np.linalg.norm(r2.x - ref.x, axis=1) / np.linalg.norm(ref.x, axis=1)
+    assert rel.max() <= 1e-12
+    np.testing.assert_array_equal(r2.bits, r.bits)
+    r3 = detect_host(det, H, y, s2, bits, minv=mats)
+    assert bits_equal(r3.x, ref.x)
