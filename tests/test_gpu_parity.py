@@ -499,3 +499,34 @@ def test_composed_path_fp64_matvec_at_n128(oracle):
     np.testing.assert_array_equal(r2.bits, r.bits)
     r3 = detect_host(det, H, y, s2, bits, minv=mats)
     assert bits_equal(r3.x, ref.x)
+
+
+@pytest.mark.parametrize("case", ["nan_h", "inf_y", "huge", "sigma0", "m_lt_n", "big_m"])
+def test_edge_inputs_against_oracle(oracle, case):
+    """Non-finite and extreme inputs, sigma^2 = 0, M < N, large M: the fused
+    detector reproduces the reference semantics (NaN propagation, divergence
+    and breakdown flags, frozen iterates) bit for bit."""
+    from paper_2504_09820_b200.detect import DetectorSpec, detect
+    O = oracle
+    M, N, T = {"m_lt_n": (6, 8), "big_m": (1000, 16)}.get(case, (24, 8)) + (9,)
+    H, y, bits, s2 = O.simulate(M, N, 0.3, 10.0, range(T), 13)
+    H = H.copy()
+    y = y.copy()
+    if case == "nan_h":
+        H[2, 3, 1] = complex(np.nan, 0.0)
+    elif case == "inf_y":
+        y[4, 0] = complex(np.inf, -1.0)
+    elif case == "huge":
+        H[1] *= 1e5       # fp16 matvec overflow -> divergence
+        y[6] *= 1e-30     # tiny right-hand side
+    elif case == "sigma0":
+        s2 = 0.0
+    for alg, mv in (("fp_cg", O.FP16), ("cg", O.FP64)):
+        det = DetectorSpec(alg, iters=5, **({} if alg == "cg" else dict(matvec="fp16", inner="fp16")))
+        A, b = O.gram_mf(H, y, s2)
+        ref = O.cg_batch(A, b, 5, O.FP64, mv, mv)
+        r = detect(det, H, y, s2, bits, want_bits=True)
+        assert bits_equal(r.x, ref.x), (case, alg)
+        np.testing.assert_array_equal(r.breakdown_at, ref.breakdown_at)
+        np.testing.assert_array_equal(r.diverged_at, ref.diverged_at)
+        np.testing.assert_array_equal(r.bits, O.demod16(ref.x))
