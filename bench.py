@@ -297,6 +297,16 @@ def run_ours(args):
                "path": "fpm_detect_host (C ABI, pinned host buffers, 2-stream H2D/kernel/D2H pipeline)"}
         _ = r
 
+    # the other BASELINE configs through the same fused detector (informational)
+    other = None
+    if rank == 0 and world == 1 and not args.no_configs:
+        if "H" in locals():
+            del H, y, bits, x
+            torch.cuda.empty_cache()
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        import cfgbench
+        other = {name: cfgbench.measure(name, 16384, lib, peak_dp, dev) for name in cfgbench.CFGS}
+
     if rank == 0:
         clocks = clk.summary()
         line = {
@@ -327,6 +337,7 @@ def run_ours(args):
             "clocks": clocks,
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "other_configs": other,
         }
         print(json.dumps(line))
     if world > 1:
@@ -373,6 +384,7 @@ def main():
     ap.add_argument("--cpu-per-worker", dest="cpu_per_worker", type=int, default=2048)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-configs", dest="no_configs", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -883,6 +883,7 @@ static int detect_args(const double* H, const double* y, const uint8_t* tx_bits,
 // solve per chunk, then the slicer / counters; flags are -1 (no iteration).
 static int run_lmmse(const DetectArgs& a, int M, int N, cudaStream_t st) {
   const long T = a.T;
+  std::snprintf(g_last_kernel, sizeof(g_last_kernel), "fpm_gram_kernel+fpm_lmmse_kernel");
   const long chunk = std::min<long>(T, 8192);
   double2 *A = nullptr, *b = nullptr;
   if (cudaMallocAsync(&A, (size_t)chunk * N * N * 16, st) != cudaSuccess) return FPM_ECUDA;
@@ -917,6 +918,7 @@ static int run_composed(const DetectArgs& a, int M, int N, int algorithm, int L,
   const long T = a.T;
   const bool bj = algorithm == FPM_ALG_FP_BJ_CG;
   const long chunk = std::min<long>(T, 2048);
+  std::snprintf(g_last_kernel, sizeof(g_last_kernel), "composed: fpm_gram_kernel+fpm_bj_kernel+fpm_cg_kernel");
   double2 *A = nullptr, *b = nullptr, *mv = nullptr;
   int rc = FPM_OK;
   if (cudaMallocAsync(&A, (size_t)chunk * N * N * 16, st) != cudaSuccess ||

@@ -27,6 +27,39 @@ CFGS = {  # name: (M, N, zeta, snr, qam, detector kwargs)
 }
 
 
+def measure(name, T_req, lib, peak, dev, reps=3):
+    """det/s and FP64 fraction of the fused detector on config `name`."""
+    M, N, zeta, snr, qam, kw = CFGS[name]
+    T = max(1024, min(T_req, (8 << 30) // (M * N * 16)))
+    b = channel.simulate_batch(M, N, zeta, zeta, snr, 0, T, 20261020, qam=qam, device=dev)
+    det = DetectorSpec(**kw)
+    x = torch.empty((T, N), dtype=torch.complex128, device=dev)
+    brk = torch.empty((T,), dtype=torch.int32, device=dev)
+    div = torch.empty((T,), dtype=torch.int32, device=dev)
+    cnt = torch.zeros((8,), dtype=torch.int64, device=dev)
+    ps = _lib.precision_struct(det.precision())
+    L = det.L or 1
+
+    def run():
+        _lib.check(lib.fpm_detect(b["H_est"].data_ptr(), b["y"].data_ptr(), b["bits"].data_ptr(), T, M, N,
+                                  b["sigma_n2"], _lib.FPM_ALG[det.algorithm], L, det.iters, ps, 0, qam, None,
+                                  x.data_ptr(), brk.data_ptr(), div.data_ptr(), None, cnt.data_ptr(), _stream()), name)
+    run()
+    torch.cuda.synchronize()
+    cnt.zero_()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        run()
+    e1.record()
+    e1.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    bps = 4 if qam == 16 else 6
+    fg = 4 * M * N * (N + 1) + 8 * M * N
+    return {"T": T, "ms": round(ms, 3), "det_s": round(T / ms * 1e3), "fp64_frac": round(fg * T / (ms / 1e3) / peak, 3),
+            "kernel": lib.fpm_last_kernel().decode(), "ber": round(int(cnt[0]) / (reps * T * bps * N), 5)}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--T", type=int, default=65536)
@@ -37,39 +70,11 @@ def main():
     _lib.check(lib.fpm_probe_fp64(200000, ctypes.byref(pk)), "probe")
     dev = torch.device("cuda", 0)
     out = {}
-    for name, (M, N, zeta, snr, qam, kw) in CFGS.items():
+    for name in CFGS:
         if a.only and a.only != name:
             continue
-        T = max(1024, min(a.T, (8 << 30) // (M * N * 16)))
-        b = channel.simulate_batch(M, N, zeta, zeta, snr, 0, T, 20261020, qam=qam, device=dev)
-        det = DetectorSpec(**kw)
-        bps = 4 if qam == 16 else 6
-        x = torch.empty((T, N), dtype=torch.complex128, device=dev)
-        brk = torch.empty((T,), dtype=torch.int32, device=dev)
-        div = torch.empty((T,), dtype=torch.int32, device=dev)
-        cnt = torch.zeros((8,), dtype=torch.int64, device=dev)
-        ps = _lib.precision_struct(det.precision())
-        L = det.L or 1
-
-        def run():
-            _lib.check(lib.fpm_detect(b["H_est"].data_ptr(), b["y"].data_ptr(), b["bits"].data_ptr(), T, M, N,
-                                      b["sigma_n2"], _lib.FPM_ALG[det.algorithm], L, det.iters, ps, 0, qam, None,
-                                      x.data_ptr(), brk.data_ptr(), div.data_ptr(), None, cnt.data_ptr(), _stream()),
-                       name)
-        run()
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(3):
-            run()
-        e1.record()
-        e1.synchronize()
-        ms = e0.elapsed_time(e1) / 3
-        fg = 4 * M * N * (N + 1) + 8 * M * N
-        out[name] = {"T": T, "ms": round(ms, 3), "det_s": round(T / ms * 1e3), "fp64_frac": round(fg * T / (ms / 1e3) / pk.value, 3),
-                     "kernel": lib.fpm_last_kernel().decode(), "ber": round(int(cnt[0]) / (4 * T * bps * N), 5)}
+        out[name] = measure(name, a.T, lib, pk.value, dev)
         print(name, json.dumps(out[name]), flush=True)
-        del b, x
 
 
 if __name__ == "__main__":
