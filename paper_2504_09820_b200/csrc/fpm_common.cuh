@@ -69,6 +69,7 @@ struct CgArgs {
   // N, C layout) -- the matrix does not fit shared memory (16-byte matvec
   // terms at large N); rows are read through L2 every sweep
   const void* a_glob;
+  int threads;  // block size (0: 256)
 };
 
 // Launchers (return FPM_* codes).  nb / lb: compile-time specialisation

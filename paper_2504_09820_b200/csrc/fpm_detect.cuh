@@ -250,6 +250,10 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_kernel(const DetectArgs arg
   FPM_STAMP(tr, 15);
 }
 
+#ifndef FPM_CG_LOADS
+#define FPM_CG_LOADS 8
+#endif
+
 template <int WK, int K, int LB, int NC>
 __global__ void __launch_bounds__(256) fpm_cg_kernel(const CgArgs args) {
   extern __shared__ __align__(128) unsigned char smem[];
@@ -290,7 +294,7 @@ __global__ void __launch_bounds__(256) fpm_cg_kernel(const CgArgs args) {
   // with one outstanding load per thread)
   const int NN = N * N;
   if (!args.a_glob) {
-    constexpr int U = 8;
+    constexpr int U = FPM_CG_LOADS;
     const double2* Ag = args.A + t0 * (long)NN;
     const int tot = Rv * NN;
 #pragma unroll 1
@@ -365,7 +369,7 @@ int launch_cg_nc(const CgArgs& a, int smem, cudaStream_t st) {
   auto k = fpm_cg_kernel<WK, K, LB, NC>;
   if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return FPM_ECUDA;
   const long grid = (a.T + a.R - 1) / a.R;
-  k<<<(unsigned)grid, 256, smem, st>>>(a);
+  k<<<(unsigned)grid, a.threads > 0 ? a.threads : 256, smem, st>>>(a);
   count_launch();
   return cudaGetLastError() == cudaSuccess ? FPM_OK : FPM_ECUDA;
 }
