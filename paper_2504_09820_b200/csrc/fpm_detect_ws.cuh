@@ -26,9 +26,6 @@ namespace fpm {
 #ifndef FPM_WIDE_NC_MAX_RS  // unrolled wide sums only when the CG side keeps >= 256 - this registers
 #define FPM_WIDE_NC_MAX_RS 0
 #endif
-#ifndef FPM_GRAM_PIPE
-#define FPM_GRAM_PIPE 1
-#endif
 #ifndef FPM_PIPE_UNROLL_N
 #define FPM_PIPE_UNROLL_N 1
 #endif
@@ -170,7 +167,7 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const DetectArgs 
         const double2* pc = sb + joff + job.c;
         if (args.debug & 4) {
           // diagnostic: Gram math skipped (CG measured without FP64 contention)
-        } else if (active && !job.half && FPM_GRAM_PIPE) {
+        } else if (active && !job.half) {
           // software-pipelined: row mm+1's operands (tile and chain) are in
           // flight while row mm's products run.  The chain runs branch-free
           // (its operands are in-bounds stale data for an idle chain, and the
@@ -222,26 +219,7 @@ FPM_PIPE_UNROLL
             y1 = ny1;
             y2 = ny2;
           }
-        } else if (active && !job.half) {
-FPM_ROW_UNROLL
-          for (int mm = 0; mm < rows; ++mm) {
-            double2 hi[4], hj[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) hi[u] = pa[mm * Np + nb * u];
-#pragma unroll
-            for (int v = 0; v < 4; ++v) hj[v] = pc[mm * Np + nb * v];
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-#pragma unroll
-              for (int v = 0; v < 4; ++v) cmac_conj(acc[u * 4 + v], hi[u], hj[v]);
-            if (chain_ok) {
-              const double2 h = sb[cq_hoff + mm * Np];
-              const double2 yv = ys[cq_yoff + m0 + mm];
-              const double y1 = cq_part ? yv.y : yv.x, y2 = cq_part ? -yv.x : yv.y;
-              ca = __dadd_rn(ca, __dadd_rn(__dmul_rn(h.x, y1), __dmul_rn(h.y, y2)));
-            }
-          }
-        } else if (active && FPM_GRAM_PIPE) {
+        } else if (active) {
           // half-pair job, software-pipelined like the circulant loop above
           const double2* py = sb + joff + job.y + nb * job.yo;
           const double* yrow = reinterpret_cast<const double*>(ys + cq_yoff + m0);
@@ -304,40 +282,6 @@ FPM_PIPE_UNROLL
             hc = nhc;
             y1 = ny1;
             y2 = ny2;
-          }
-        } else if (active) {
-          const double2* py = sb + joff + job.y + nb * job.yo;
-FPM_ROW_UNROLL
-          for (int mm = 0; mm < rows; ++mm) {
-            {
-              double2 hx[4];
-#pragma unroll
-              for (int u = 0; u < 4; ++u) hx[u] = pa[mm * Np + nb * u];
-              int p = 0;
-#pragma unroll
-              for (int u = 0; u < 4; ++u)
-#pragma unroll
-                for (int v = u + 1; v < 4; ++v) cmac_conj(acc[p++], hx[u], hx[v]);
-              acc[14].x = __dadd_rn(acc[14].x, sqmag(hx[0]));
-              acc[14].y = __dadd_rn(acc[14].y, sqmag(hx[1]));
-              acc[15].x = __dadd_rn(acc[15].x, sqmag(hx[2]));
-              acc[15].y = __dadd_rn(acc[15].y, sqmag(hx[3]));
-            }
-            double2 hy[2], hz[4];
-#pragma unroll
-            for (int w = 0; w < 2; ++w) hy[w] = py[mm * Np + nb * w];
-#pragma unroll
-            for (int v = 0; v < 4; ++v) hz[v] = pc[mm * Np + nb * v];
-#pragma unroll
-            for (int w = 0; w < 2; ++w)
-#pragma unroll
-              for (int v = 0; v < 4; ++v) cmac_conj(acc[6 + w * 4 + v], hy[w], hz[v]);
-            if (chain_ok) {
-              const double2 h = sb[cq_hoff + mm * Np];
-              const double2 yv = ys[cq_yoff + m0 + mm];
-              const double y1 = cq_part ? yv.y : yv.x, y2 = cq_part ? -yv.x : yv.y;
-              ca = __dadd_rn(ca, __dadd_rn(__dmul_rn(h.x, y1), __dmul_rn(h.y, y2)));
-            }
           }
         } else if (chain_ok) {  // idle job slot (partial group) that still owns a chain
 #pragma unroll 1
