@@ -72,6 +72,11 @@ enum { FPM_RHO_AS_WRITTEN = 0, FPM_RHO_TEXTBOOK = 1 };
  * "lmmse" is the direct Cholesky comparator (detect.py:230-231) */
 enum { FPM_ALG_LMMSE = 0, FPM_ALG_CG = 1, FPM_ALG_FP_CG = 2, FPM_ALG_FP_BJ_CG = 3 };
 
+/* OR-ed into `algorithm`: FP32 Gram / matched filter (EXTENSION for
+ * BASELINE config c4; the reference has no such knob): H, y rounded once to
+ * binary32, every Gram / MF op in binary32, widened to the fp64 carriers. */
+enum { FPM_FLAG_GRAM_FP32 = 0x100 };
+
 enum {
   FPM_CNT_BIT_ERRORS = 0,
   FPM_CNT_SYMBOL_ERRORS = 1, /* extension: the reference counts bits only */
@@ -90,6 +95,10 @@ int fpm_limits(int32_t* max_n, int32_t* max_l, int32_t* max_m);
 
 int fpm_gram(const double* H, const double* y, int64_t T, int32_t M, int32_t N, double sigma2,
              double* A, double* b, void* stream);
+
+/* FP32-Gram extension of fpm_gram (see FPM_FLAG_GRAM_FP32); same layouts. */
+int fpm_gram32(const double* H, const double* y, int64_t T, int32_t M, int32_t N, double sigma2, double* A,
+               double* b, void* stream);
 
 /* bad_block: optional int32[T], set to the first non-PD block start or -1.
  * Returns FPM_ENOTPD if any block of any realization is not PD. */

@@ -17,11 +17,12 @@ LIB_PATH = os.environ.get("FPM_LIB") or os.path.join(_HERE, "libfpmimo_b200.so")
 FPM_OK, FPM_EINVAL, FPM_ENOTPD, FPM_ECUDA, FPM_EUNSUPPORTED = range(5)
 FPM_RHO = {"as_written": 0, "textbook": 1}
 FPM_ALG = {"lmmse": 0, "cg": 1, "fp_cg": 2, "fp_bj_cg": 3}
+FPM_FLAG_GRAM_FP32 = 0x100
 COUNTERS = ("bit_errors", "symbol_errors", "diverged", "breakdown", "trials", "nonpd")
 NCOUNTERS = 8
 
 # every symbol include/fpmimo_b200.h declares
-EXPORTS = ("fpm_version", "fpm_strerror", "fpm_limits", "fpm_gram", "fpm_bj_setup", "fpm_cg", "fpm_cg_ex", "fpm_lmmse", "fpm_gen_trials",
+EXPORTS = ("fpm_version", "fpm_strerror", "fpm_limits", "fpm_gram", "fpm_bj_setup", "fpm_cg", "fpm_cg_ex", "fpm_lmmse", "fpm_gen_trials", "fpm_gram32",
            "fpm_slice_count", "fpm_detect", "fpm_detect_host", "fpm_launch_count", "fpm_last_kernel", "fpm_probe_fp64",
            "fpm_debug_set_trace")
 
@@ -57,6 +58,7 @@ _SIGS = {
     "fpm_cg_ex": (ctypes.c_int, [_P, _P, _P, _I64, _I32, _I32, _I32, ctypes.POINTER(Precision), _I32,
                                  _P, _P, _P, ctypes.POINTER(CgHistory), _P]),
     "fpm_lmmse": (ctypes.c_int, [_P, _P, _I64, _I32, _P, _P, _P]),
+    "fpm_gram32": (ctypes.c_int, [_P, _P, _I64, _I32, _I32, _D, _P, _P, _P]),
     "fpm_gen_trials": (ctypes.c_int, [ctypes.c_uint64, _I32, _I32, _I64, _I64, _I32, _I32, _I32, _P, _P, _P, _P, _P]),
     "fpm_slice_count": (ctypes.c_int, [_P, _P, _I64, _I32, _I32, _P, _P, _P]),
     "fpm_detect": (ctypes.c_int, [_P, _P, _P, _I64, _I32, _I32, _D, _I32, _I32, _I32,

@@ -47,6 +47,7 @@ struct DetectArgs {
   int ws_nslot;        // hand-off slots (2 double-buffered, 1 when two do not fit)
   int debug;  // diagnostic bits (FPM_DEBUG): 1 = WS kernel skips the CG side
   int composed;  // no fused plan fits: fpm_gram -> fpm_bj_setup -> fpm_cg -> slicer
+  int gram32;    // FPM_FLAG_GRAM_FP32: binary32 Gram (extension), composed path
 };
 
 struct WsLayout;  // fpm_detect_ws.cuh
@@ -89,6 +90,10 @@ FPM_DECLARE_KIND(gen_w)  // everything generic (W != fp64)
 #undef FPM_DECLARE_KIND
 
 void count_launch();
+
+// FP32-Gram extension (fpm_gram32.cu)
+int launch_gram32(const double2* H, const double2* y, long T, int M, int N, double sigma2, double2* A, double2* b,
+                  cudaStream_t st);
 
 // A -> A rounded to a generic matvec format, C layout (global-A CG mode)
 int launch_round_mv_gen(const double2* A, double2* out, long n, FmtP f, cudaStream_t st);

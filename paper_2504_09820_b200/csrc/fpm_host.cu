@@ -804,6 +804,15 @@ int fpm_cg(const double* A, const double* b, const double* Minv, int64_t T, int3
   return fpm_cg_ex(A, b, Minv, T, N, L, iters, prec, rho_update, x, breakdown_at, diverged_at, nullptr, stream);
 }
 
+int fpm_gram32(const double* H, const double* y, int64_t T, int32_t M, int32_t N, double sigma2, double* A,
+               double* b, void* stream) {
+  if (T < 0 || M < 1 || N < 1 || !H || !y || !A || !b) return FPM_EINVAL;
+  if (N > kMaxN || M > kMaxM) return FPM_EUNSUPPORTED;
+  if (T == 0) return FPM_OK;
+  return launch_gram32(reinterpret_cast<const double2*>(H), reinterpret_cast<const double2*>(y), T, M, N, sigma2,
+                       reinterpret_cast<double2*>(A), reinterpret_cast<double2*>(b), (cudaStream_t)stream);
+}
+
 int fpm_lmmse(const double* A, const double* b, int64_t T, int32_t N, double* x, int32_t* nonpd, void* stream) {
   if (T < 0 || N < 1 || !A || !b || !x) return FPM_EINVAL;
   if (N > kMaxN) return FPM_EUNSUPPORTED;
@@ -833,6 +842,8 @@ static int detect_args(const double* H, const double* y, const uint8_t* tx_bits,
                        bool& ws, WsLayout& sl, int& grid) {
   if (T < 0 || M < 1 || N < 1) return FPM_EINVAL;
   if (iters < 1) return FPM_EINVAL;
+  const int gram32 = (algorithm & FPM_FLAG_GRAM_FP32) != 0;
+  algorithm &= ~FPM_FLAG_GRAM_FP32;
   if (rho_update != FPM_RHO_AS_WRITTEN && rho_update != FPM_RHO_TEXTBOOK) return FPM_EINVAL;
   if (qam != 16 && qam != 64) return FPM_EINVAL;
   if (algorithm != FPM_ALG_LMMSE && algorithm != FPM_ALG_CG && algorithm != FPM_ALG_FP_CG &&
@@ -870,8 +881,14 @@ static int detect_args(const double* H, const double* y, const uint8_t* tx_bits,
   a.tl = pick_tl(N);
   a.debug = env_int("FPM_DEBUG", 0);
   k = pick_kinds(*pp);
+  a.gram32 = gram32;
   if (algorithm == FPM_ALG_LMMSE) {  // Gram + Cholesky kernels, no fused plan
     a.G.R = 1;
+    return FPM_OK;
+  }
+  if (gram32) {  // extension: binary32 Gram kernel, then the standalone stages
+    a.G.R = 1;
+    a.composed = 1;
     return FPM_OK;
   }
   DetectArgs aw = a;
@@ -888,7 +905,8 @@ static int detect_args(const double* H, const double* y, const uint8_t* tx_bits,
 // solve per chunk, then the slicer / counters; flags are -1 (no iteration).
 static int run_lmmse(const DetectArgs& a, int M, int N, cudaStream_t st) {
   const long T = a.T;
-  std::snprintf(g_last_kernel, sizeof(g_last_kernel), "fpm_gram_kernel+fpm_lmmse_kernel");
+  std::snprintf(g_last_kernel, sizeof(g_last_kernel), "%s+fpm_lmmse_kernel",
+                a.gram32 ? "fpm_gram32_kernel" : "fpm_gram_kernel");
   const long chunk = std::min<long>(T, 8192);
   double2 *A = nullptr, *b = nullptr;
   if (cudaMallocAsync(&A, (size_t)chunk * N * N * 16, st) != cudaSuccess) return FPM_ECUDA;
@@ -899,8 +917,10 @@ static int run_lmmse(const DetectArgs& a, int M, int N, cudaStream_t st) {
   int rc = FPM_OK;
   for (long c0 = 0; !rc && c0 < T; c0 += chunk) {
     const long n = std::min(chunk, T - c0);
-    rc = fpm_gram(reinterpret_cast<const double*>(a.H + c0 * (long)M * N), reinterpret_cast<const double*>(a.y + c0 * M),
-                  n, M, N, a.sigma2, reinterpret_cast<double*>(A), reinterpret_cast<double*>(b), st);
+    rc = a.gram32 ? launch_gram32(a.H + c0 * (long)M * N, a.y + c0 * M, n, M, N, a.sigma2, A, b, st)
+                  : fpm_gram(reinterpret_cast<const double*>(a.H + c0 * (long)M * N),
+                             reinterpret_cast<const double*>(a.y + c0 * M), n, M, N, a.sigma2,
+                             reinterpret_cast<double*>(A), reinterpret_cast<double*>(b), st);
     if (!rc) rc = launch_lmmse(A, b, n, N, a.x + c0 * N, nullptr, a.counters + FPM_CNT_NONPD, st);
   }
   cudaFreeAsync(A, st);
@@ -923,7 +943,8 @@ static int run_composed(const DetectArgs& a, int M, int N, int algorithm, int L,
   const long T = a.T;
   const bool bj = algorithm == FPM_ALG_FP_BJ_CG;
   const long chunk = std::min<long>(T, 2048);
-  std::snprintf(g_last_kernel, sizeof(g_last_kernel), "composed: fpm_gram_kernel+fpm_bj_kernel+fpm_cg_kernel");
+  std::snprintf(g_last_kernel, sizeof(g_last_kernel), "composed: %s+fpm_bj_kernel+fpm_cg_kernel",
+                a.gram32 ? "fpm_gram32_kernel" : "fpm_gram_kernel");
   double2 *A = nullptr, *b = nullptr, *mv = nullptr;
   int rc = FPM_OK;
   if (cudaMallocAsync(&A, (size_t)chunk * N * N * 16, st) != cudaSuccess ||
@@ -932,8 +953,10 @@ static int run_composed(const DetectArgs& a, int M, int N, int algorithm, int L,
     rc = FPM_ECUDA;
   for (long c0 = 0; !rc && c0 < T; c0 += chunk) {
     const long n = std::min(chunk, T - c0);
-    rc = fpm_gram(reinterpret_cast<const double*>(a.H + c0 * (long)M * N), reinterpret_cast<const double*>(a.y + c0 * M),
-                  n, M, N, a.sigma2, reinterpret_cast<double*>(A), reinterpret_cast<double*>(b), st);
+    rc = a.gram32 ? launch_gram32(a.H + c0 * (long)M * N, a.y + c0 * M, n, M, N, a.sigma2, A, b, st)
+                  : fpm_gram(reinterpret_cast<const double*>(a.H + c0 * (long)M * N),
+                             reinterpret_cast<const double*>(a.y + c0 * M), n, M, N, a.sigma2,
+                             reinterpret_cast<double*>(A), reinterpret_cast<double*>(b), st);
     const double2* minv = nullptr;
     if (!rc && bj) {
       if (a.minv_in) {
@@ -975,6 +998,7 @@ int fpm_detect(const double* H, const double* y, const uint8_t* tx_bits, int64_t
                        breakdown_at, diverged_at, rx_bits, counters, a, k, threads, ws, sl, grid);
   if (rc) return rc;
   if (T == 0) return FPM_OK;
+  algorithm &= ~FPM_FLAG_GRAM_FP32;
   if (algorithm == FPM_ALG_LMMSE) return run_lmmse(a, M, N, (cudaStream_t)stream);
   if (a.composed) {
     fpm_precision p64 = {{53, 11, 1}, {53, 11, 1}, {53, 11, 1}};
@@ -999,6 +1023,7 @@ int fpm_detect_host(const double* H, const double* y, const uint8_t* tx_bits, in
                        breakdown_at, diverged_at, rx_bits, counters, a, k, threads, ws, sl, grid0);
   if (rc) return rc;
   if (T == 0) return FPM_OK;
+  algorithm &= ~FPM_FLAG_GRAM_FP32;  // carried in a.gram32
   const int bps = qam == 64 ? 6 : 4;
   const int bj = algorithm == FPM_ALG_FP_BJ_CG;
   if (chunk <= 0) chunk = std::max<int64_t>(a.G.R, (int64_t)(512LL << 20) / ((int64_t)M * N * 16));

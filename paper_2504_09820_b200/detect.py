@@ -39,8 +39,11 @@ class DetectorSpec:
     rtol: float = 1e-6
     rho_update: str = "as_written"
     label: str | None = None
+    gram: str = "fp64"   # EXTENSION (BASELINE c4 "FP32 Gram"): "fp32" computes the Gram / MF in binary32
 
     def __post_init__(self):
+        if self.gram not in ("fp64", "fp32"):
+            raise ContractViolation(f"unknown Gram precision {self.gram!r}")
         if self.algorithm not in ("lmmse", "cg", "fp_cg", "fp_bj_cg"):
             raise ContractViolation(f"unknown algorithm {self.algorithm!r}")
         if self.algorithm == "fp_bj_cg" and self.L is None:
@@ -63,7 +66,8 @@ class DetectorSpec:
     @classmethod
     def from_reference(cls, det) -> "DetectorSpec":
         return cls(algorithm=det.algorithm, iters=det.iters, L=det.L, work=det.work, matvec=det.matvec,
-                   inner=det.inner, rtol=det.rtol, rho_update=det.rho_update, label=det.label)
+                   inner=det.inner, rtol=det.rtol, rho_update=det.rho_update, label=det.label,
+                   gram=getattr(det, "gram", "fp64"))
 
 
 @dataclass
@@ -79,9 +83,13 @@ def _spec(det) -> DetectorSpec:
     return det if isinstance(det, DetectorSpec) else DetectorSpec.from_reference(det)
 
 
-def gram_mf(H, y, sigma2: float):
+def _alg(det: DetectorSpec) -> int:
+    return _lib.FPM_ALG[det.algorithm] | (_lib.FPM_FLAG_GRAM_FP32 if det.gram == "fp32" else 0)
+
+
+def gram_mf(H, y, sigma2: float, gram: str = "fp64"):
     """A = H^H H (symmetrized) + sigma2 I and b = H^H y, bit-identical to
-    detect.py:215-218."""
+    detect.py:215-218 (gram="fp32": the binary32 extension, fpm_gram32)."""
     torch = _torch()
     host = not _is_torch(H)
     Hd = _to_dev(H, torch.complex128)
@@ -89,8 +97,8 @@ def gram_mf(H, y, sigma2: float):
     T, M, N = Hd.shape
     A = torch.empty((T, N, N), dtype=torch.complex128, device=Hd.device)
     b = torch.empty((T, N), dtype=torch.complex128, device=Hd.device)
-    rc = _lib.load().fpm_gram(Hd.data_ptr(), yd.data_ptr(), T, M, N, float(sigma2), A.data_ptr(), b.data_ptr(),
-                              _stream())
+    fn = _lib.load().fpm_gram32 if gram == "fp32" else _lib.load().fpm_gram
+    rc = fn(Hd.data_ptr(), yd.data_ptr(), T, M, N, float(sigma2), A.data_ptr(), b.data_ptr(), _stream())
     _lib.check(rc, "gram_mf")
     return (A.cpu().numpy(), b.cpu().numpy()) if host else (A, b)
 
@@ -125,7 +133,7 @@ def detect(det, H, y, sigma2: float, tx_bits=None, *, qam: int = 16, minv=None, 
     ps = _lib.precision_struct(det.precision())
     rc = _lib.load().fpm_detect(
         Hd.data_ptr(), yd.data_ptr(), None if txd is None else txd.data_ptr(), T, M, N, float(sigma2),
-        _lib.FPM_ALG[det.algorithm], L, int(det.iters), ps, _lib.FPM_RHO.get(det.rho_update, -1), int(qam),
+        _alg(det), L, int(det.iters), ps, _lib.FPM_RHO.get(det.rho_update, -1), int(qam),
         None if md is None else md.data_ptr(), x.data_ptr(), brk.data_ptr(), div.data_ptr(),
         None if rx is None else rx.data_ptr(), cnt.data_ptr(), _stream())
     _lib.check(rc, "detect")
@@ -164,7 +172,7 @@ def detect_host(det, H, y, sigma2: float, tx_bits=None, *, qam: int = 16, minv=N
     cnt = np.zeros((_lib.NCOUNTERS,), np.int64)
     ps = _lib.precision_struct(det.precision())
     ptr = lambda a: None if a is None else a.ctypes.data  # noqa: E731
-    rc = _lib.load().fpm_detect_host(ptr(H), ptr(y), ptr(tx), T, M, N, float(sigma2), _lib.FPM_ALG[det.algorithm],
+    rc = _lib.load().fpm_detect_host(ptr(H), ptr(y), ptr(tx), T, M, N, float(sigma2), _alg(det),
                                      L, int(det.iters), ps, _lib.FPM_RHO.get(det.rho_update, -1), int(qam),
                                      ptr(mp), ptr(x), ptr(brk), ptr(div), ptr(rx), ptr(cnt), int(chunk))
     _lib.check(rc, "detect_host")

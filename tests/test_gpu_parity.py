@@ -530,3 +530,24 @@ def test_edge_inputs_against_oracle(oracle, case):
         np.testing.assert_array_equal(r.breakdown_at, ref.breakdown_at)
         np.testing.assert_array_equal(r.diverged_at, ref.diverged_at)
         np.testing.assert_array_equal(r.bits, O.demod16(ref.x))
+
+
+@pytest.mark.parametrize("M,N", [(128, 64), (512, 128), (40, 16), (33, 12)])
+def test_fp32_gram_extension(oracle, M, N):
+    """FP32-Gram extension (BASELINE c4; parity unpinned -- no reference knob):
+    the binary32 Gram / matched filter bit-exact against its restatement, and
+    the detector on top of it bit-exact with injected inverses."""
+    from paper_2504_09820_b200.detect import DetectorSpec, detect, gram_mf
+    O = oracle
+    T = 5
+    H, y, bits, s2 = O.simulate(M, N, 0.6, 12.0, range(T), 17)
+    A, b = O.gram_mf_fp32(H, y, s2)
+    Ag, bg = gram_mf(H, y, s2, gram="fp32")
+    assert bits_equal(Ag, A) and bits_equal(bg, b)
+    L = 4
+    mats = O.bj_inverses(A, L)
+    det = DetectorSpec("fp_bj_cg", iters=4, L=L, matvec="fp16", inner="fp16", gram="fp32")
+    ref = O.cg_batch(A, b, 4, O.FP64, O.FP16, O.FP16, mats)
+    r = detect(det, H, y, s2, bits, minv=mats, want_bits=True)
+    assert bits_equal(r.x, ref.x)
+    np.testing.assert_array_equal(r.bits, O.demod16(ref.x))

@@ -156,3 +156,16 @@ def test_lmmse_restatement_matches_reference(oracle):
     for tag in ("c5", "c2"):
         assert bits_equal(oracle.lmmse(g[f"{tag}_A"], g[f"{tag}_b"]), g[f"{tag}_x"])
         np.testing.assert_array_equal(oracle.demod16(g[f"{tag}_x"]), g[f"{tag}_rx_bits"])
+
+
+def test_fp32_gram_extension_is_a_binary32_gram(oracle):
+    """EXTENSION (parity unpinned): the binary32 Gram restatement agrees with
+    the reference Gram to binary32 accuracy and its values lie on the binary32
+    grid."""
+    g = load_golden("c5_bj4_fp16")
+    A32, b32 = oracle.gram_mf_fp32(g["H"], g["y"], float(g["sigma2"]))
+    A, b = g["A"], g["b"]
+    assert np.abs(A32 - A).max() <= 2e-6 * np.abs(A).max()
+    assert np.abs(b32 - b).max() <= 2e-6 * np.abs(b).max()
+    for v in (A32.real, A32.imag, b32.real, b32.imag):
+        assert np.array_equal(v, v.astype(np.float32).astype(np.float64))

@@ -21,6 +21,8 @@ CFGS = {  # name: (M, N, zeta, snr, qam, detector kwargs)
     "c2_bf16": (128, 32, 0.5, 10.0, 16, dict(algorithm="fp_cg", iters=10, matvec="bfloat16", inner="bfloat16")),
     "c3": (256, 64, 0.7, 20.0, 64, dict(algorithm="fp_bj_cg", iters=6, L=4, matvec="fp16", inner="fp16")),
     "c4": (512, 128, 0.8, 25.0, 64, dict(algorithm="fp_bj_cg", iters=8, L=8, matvec="fp16", inner="fp16")),
+    "c4_gram32": (512, 128, 0.8, 25.0, 64, dict(algorithm="fp_bj_cg", iters=8, L=8, matvec="fp16", inner="fp16",
+                                                 gram="fp32")),
     "c5_fp16": (128, 64, 0.5, 15.0, 16, dict(algorithm="fp_bj_cg", iters=8, L=4, matvec="fp16", inner="fp16")),
     "c5_fp64": (128, 64, 0.5, 15.0, 16, dict(algorithm="fp_bj_cg", iters=8, L=4)),
     "c5_lmmse": (128, 64, 0.5, 15.0, 16, dict(algorithm="lmmse")),
@@ -41,8 +43,9 @@ def measure(name, T_req, lib, peak, dev, reps=3):
     L = det.L or 1
 
     def run():
+        alg = _lib.FPM_ALG[det.algorithm] | (_lib.FPM_FLAG_GRAM_FP32 if det.gram == "fp32" else 0)
         _lib.check(lib.fpm_detect(b["H_est"].data_ptr(), b["y"].data_ptr(), b["bits"].data_ptr(), T, M, N,
-                                  b["sigma_n2"], _lib.FPM_ALG[det.algorithm], L, det.iters, ps, 0, qam, None,
+                                  b["sigma_n2"], alg, L, det.iters, ps, 0, qam, None,
                                   x.data_ptr(), brk.data_ptr(), div.data_ptr(), None, cnt.data_ptr(), _stream()), name)
     run()
     torch.cuda.synchronize()
