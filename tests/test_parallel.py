@@ -112,16 +112,19 @@ def test_single_process_sweep_equals_direct_oracle():
             assert curves[di].points[si].divergence_rate == int(cnt[2]) / cfg.trials
 
 
-def test_gloo_world2_sweep_equals_single_process():
+@pytest.mark.parametrize("world", [2, 4])
+def test_gloo_sweep_equals_single_process(world):
+    """SURVEY.md 8(e) invariance: the sharded sweep's counts equal the
+    single-process sweep's at every world size (ragged chunks included)."""
     import torch
-    trials, chunk = 23, 10   # ragged: chunks of 10, 10, 3 split 5/5, 5/5, 2/1
-    outs = _run_world(2, trials, chunk)
+    trials, chunk = 23, 10   # ragged: chunks of 10, 10, 3
+    outs = _run_world(world, trials, chunk)
     single = P.sharded_ber_sweep(_cfg(trials, chunk), _simulate, counts_fn=_oracle_counts,
                                  device=torch.device("cpu"))
     ref = [[(p.bit_errors, p.divergence_rate, p.ci_low, p.ci_high) for p in c.points] for c in single]
     for o in outs:
         assert o[0] == ref                      # every rank holds the global result
-        assert o[1] == [3] * 8                  # 1 + 2
+        assert o[1] == [world * (world + 1) // 2] * 8   # sum of rank + 1 over ranks
     assert outs[0][2] == outs[1][2]
     assert outs[0][2]["trials"] == 9
 
