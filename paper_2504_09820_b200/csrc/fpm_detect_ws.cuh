@@ -546,7 +546,11 @@ int launch_detect_ws_t(const DetectArgs& a, const WsLayout& sl, int grid, cudaSt
   if constexpr (NB == 16) {
     // N = 64, R = 2: 256 Gram threads = two warp groups and a 512-thread
     // block -> register split between the Gram and the other warp groups
-    if (a.ws_gt == 256 && threads == 512 && !std::getenv("FPM_WS_NOSPLIT")) {
+    if (a.ws_gt == 256 && threads <= 512 && !std::getenv("FPM_WS_NOSPLIT")) {
+      // a narrower CG group leaves idle warps in the upper warp groups (they
+      // still take part in the register hand-over); CG-first order needs the
+      // CG group to fill warp groups 0-1 so the Gram starts at warp group 2
+      if (threads < 512) b.ws_order = 0;
       constexpr int kRS = sizeof(typename Ar<K>::C) >= 16 ? FPM_WS_GRAM_REGS_WIDE : FPM_WS_GRAM_REGS;
       auto k = fpm_detect_ws_kernel<WK, K, NB, LB, kRS>;
       if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, a.smem_bytes) != cudaSuccess)

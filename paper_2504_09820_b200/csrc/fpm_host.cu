@@ -491,7 +491,7 @@ static bool plan_detect_ws(int M, int N, int L, int bj, int iters, int mvk, int 
           a.ldA = ldA;
           a.smem_bytes = (int)off;
           a.ws_gt = gt;
-          a.ws_ct = cg_threads(R, gt);
+          a.ws_ct = env_int("FPM_WS_CT", cg_threads(R, gt));
           a.ws_ncg = ncg;
           a.ws_ct0 = ncg == 2 ? 128 : a.ws_ct;
           a.ws_nslot = nslot;
