@@ -48,6 +48,8 @@ struct DetectArgs {
   int debug;  // diagnostic bits (FPM_DEBUG): 1 = WS kernel skips the CG side
   int composed;  // no fused plan fits: fpm_gram -> fpm_bj_setup -> fpm_cg -> slicer
   int gram32;    // FPM_FLAG_GRAM_FP32: binary32 Gram (extension), composed path
+  double2* gram_A;  // non-null: Gram-only mode of the WS kernel (fpm_gram): A, b to HBM
+  double2* gram_b;
 };
 
 struct WsLayout;  // fpm_detect_ws.cuh

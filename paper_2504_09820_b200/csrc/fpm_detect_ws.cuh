@@ -316,6 +316,33 @@ FPM_PIPE_UNROLL
         if ((tid & 31) == 0) mbar_arrive(&empty[s]);
       }
 
+      if (args.gram_A) {
+        // Gram-only mode (fpm_gram): final / mirror entries straight to HBM
+        // in binary64, no hand-off to the CG side
+        if (active) {
+          double2* Agl = args.gram_A + (t0 + job.g) * (long)N * N;
+          gram_entries(
+              job, acc, nb, N, args.sigma2,
+              [&](int i, int jx, double2 vij, double2 vji) {
+                Agl[(long)i * N + jx] = vij;
+                Agl[(long)jx * N + i] = vji;
+              },
+              [&](int i, double2 vii) { Agl[(long)i * N + i] = vii; });
+        }
+        if (kChainInLoop) {
+          if (chain_ok) reinterpret_cast<double*>(args.gram_b + (t0 + cq_g) * N + cq_n)[cq_part] = ca;
+        } else {
+#pragma unroll 1
+          for (int q = tid; q < nchain; q += gt) {
+            const int g = q / (2 * N), e = q - g * 2 * N;
+            const int part = e / N;
+            reinterpret_cast<double*>(args.gram_b + (t0 + g) * N + (e - part * N))[part] = bsm[q];
+          }
+        }
+        gbar.sync();
+        if (tid == 0) mbar_arrive(&ydone[yb]);
+        continue;
+      }
       // ---- hand-off: wait until the CG side has released this slot ----
       if (tr && tid == 0 && j < 8) tr[j * 8 + 1] = clock64();
       if (tr && (tid & 31) == 0 && j == 2) tr[72 + tid / 32] = clock64();
@@ -402,7 +429,7 @@ FPM_PIPE_UNROLL
         issue(gc);
       }
     }
-    } else if (tid >= cbase && tid < cbase + ct) {
+    } else if (tid >= cbase && tid < cbase + ct && !args.gram_A) {
     // ============================ CG warps ============================
     // ws_ncg CG groups; group cgi owns hand-off slot cgi, i.e. realization
     // groups j = cgi, cgi + ncg, ... (two latency-bound solves in flight)

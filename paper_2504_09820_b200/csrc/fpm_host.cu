@@ -566,6 +566,7 @@ static int launch_detect(const Kinds& k, const DetectArgs& a, int threads, cudaS
 static int launch_detect_ws(const Kinds& k, const DetectArgs& a, const WsLayout& sl, int grid, cudaStream_t st) {
   int nb, lb;
   pick_spec(a.G.N, a.L, a.bj, nb, lb);
+  if (a.gram_A && nb == 16) lb = 4;  // Gram-only: any LB; take the N = 64 specialisation
   if (a.G.N != a.G.Np) nb = 0;
   if (std::getenv("FPM_NO_SPEC")) nb = lb = 0;
   note_kernel("fpm_detect_ws_kernel", k, nb, lb);
@@ -666,6 +667,32 @@ int fpm_gram(const double* H, const double* y, int64_t T, int32_t M, int32_t N, 
   if (T < 0 || M < 1 || N < 1 || !H || !y || !A || !b) return FPM_EINVAL;
   if (N > kMaxN || M > kMaxM) return FPM_EUNSUPPORTED;
   if (T == 0) return FPM_OK;
+  {
+    // the persistent warp-specialised kernel in Gram-only mode (its Gram warps
+    // and TMA producer, results straight to HBM) when its layout applies
+    DetectArgs d;
+    std::memset(&d, 0, sizeof(d));
+    d.H = reinterpret_cast<const double2*>(H);
+    d.y = reinterpret_cast<const double2*>(y);
+    d.T = T;
+    d.sigma2 = sigma2;
+    d.L = 1;
+    d.iters = 1;
+    d.gram_A = reinterpret_cast<double2*>(A);
+    d.gram_b = reinterpret_cast<double2*>(b);
+    d.trace = nullptr;
+    const fpm_precision ph = {{53, 11, 1}, {11, 5, 1}, {11, 5, 1}};
+    d.pr.work = make_fmtp(ph.work);
+    d.pr.mv = make_fmtp(ph.matvec);
+    d.pr.ip = make_fmtp(ph.inner);
+    d.sl = make_slicer(16);
+    WsLayout sl;
+    int grid = 0;
+    if (!std::getenv("FPM_GRAM_LEGACY") && plan_detect_ws(M, N, 1, 0, 1, FK_F16, FK_F16, d, sl, grid)) {
+      const Kinds k = {FK_F64, FK_F16, FK_F16};
+      return launch_detect_ws(k, d, sl, grid, (cudaStream_t)stream);
+    }
+  }
   GramArgs a;
   a.H = reinterpret_cast<const double2*>(H);
   a.y = reinterpret_cast<const double2*>(y);
