@@ -31,6 +31,15 @@ namespace fpm {
 #endif
 #define FPM_PIPE_UNROLL FPM_UNROLL_(FPM_PIPE_UNROLL_N)
 
+#ifndef FPM_PRODUCER_SLEEP_NS  // back-off of the producer / CG-side waits (0: spin)
+#define FPM_PRODUCER_SLEEP_NS 0
+#endif
+#ifndef FPM_CG_SLEEP_NS
+#define FPM_CG_SLEEP_NS 0
+#endif
+#define FPM_PWAIT(b, p) (FPM_PRODUCER_SLEEP_NS ? mbar_wait_sleep((b), (p), FPM_PRODUCER_SLEEP_NS) : mbar_wait((b), (p)))
+#define FPM_CWAIT(b, p) (FPM_CG_SLEEP_NS ? mbar_wait_sleep((b), (p), FPM_CG_SLEEP_NS) : mbar_wait((b), (p)))
+
 struct WsLayout {  // byte offsets inside one hand-off slot
   int at, b, d, bytes;
 };
@@ -419,12 +428,12 @@ FPM_PIPE_UNROLL
       fence_proxy_async();
 #pragma unroll 1
       for (long gc = 0; gc < total; ++gc) {
-        if (gc >= G.S) mbar_wait(&empty[gc % G.S], (uint32_t)(((gc - G.S) / G.S) & 1));
+        if (gc >= G.S) FPM_PWAIT(&empty[gc % G.S], (uint32_t)(((gc - G.S) / G.S) & 1));
         if (gc >= 2 * nch && gc % nch == 0) {
           // the y buffer of group jj was last read by group jj-2: wait until
           // that group's Gram is done (its hand-off has been published)
           const int jj = (int)(gc / nch);
-          mbar_wait(&ydone[jj & 1], (uint32_t)(((jj - 2) >> 1) & 1));
+          FPM_PWAIT(&ydone[jj & 1], (uint32_t)(((jj - 2) >> 1) & 1));
         }
         issue(gc);
       }
@@ -474,7 +483,7 @@ FPM_PIPE_UNROLL
       S.At = reinterpret_cast<C*>(sp + sl.at);
       S.b = reinterpret_cast<double2*>(sp + sl.b);
       double2* dS = reinterpret_cast<double2*>(sp + sl.d);
-      mbar_wait(&sfull[slot], (uint32_t)(use & 1));
+      FPM_CWAIT(&sfull[slot], (uint32_t)(use & 1));
       if (tr && lt == 0 && j < 8) tr[j * 8 + 4] = clock64();
 #pragma unroll 1
       for (int g = lt; g < R; g += ctg) S.fl[g * 4] = g < Rv ? 1 : 0;
