@@ -9,7 +9,15 @@
  *                      detect.py:215-218 (A = H^H H sym + s2 I, b = H^H y)
  *   fpm_bj_setup    <- build_blocks_batch, solvers.py:232-253
  *   fpm_cg          <- run_batch, solvers.py:262-393 (x, breakdown_at,
- *                      diverged_at; histories are not produced)
+ *                      diverged_at)
+ *   fpm_cg_ex       <- run_batch with the BatchResult histories,
+ *                      solvers.py:188-204, 306-319, 371-393
+ *   fpm_lmmse       <- _solve_direct_batch, linalg.py:223-231 (the
+ *                      detector "lmmse", detect.py:230-231)
+ *   fpm_gen_trials  <- the draws of simulate_trials, detect.py:189-214,
+ *                      channel.py:138-161, 206-219, rng.py:19-39
+ *                      (distribution level, keyed per-trial streams)
+ *   fpm_gram32      <- EXTENSION: binary32 Gram (BASELINE config c4)
  *   fpm_slice_count <- demodulate_16qam + error sum, detect.py:78-84, :260-262
  *   fpm_detect      <- _detect_batch, detect.py:223-237, fused with the Gram
  *                      of simulate_trials and the slicer/counter of

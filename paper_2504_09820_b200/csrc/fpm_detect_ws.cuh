@@ -162,6 +162,10 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const DetectArgs 
       }
       const double2* ys = ysb + yb * R * G.M;
       mbar_wait(&ybar[yb], (uint32_t)((j >> 1) & 1));
+      // serial mode (debug bit 8): the Gram of group j starts only once the CG
+      // has released the slot of group j - nsl, i.e. no Gram / CG overlap --
+      // faster when both compete for the FP64 pipe (fp64 matvec)
+      if ((args.debug & 8) && j >= nsl && !args.gram_A) mbar_wait(&sempty[slot], (uint32_t)((use - 1) & 1));
       if (tr && tid == 0 && j < 8) tr[j * 8 + 0] = clock64();
 
 #pragma unroll 1
