@@ -62,6 +62,7 @@ struct CgSmem {
   double2* sc;            // R * 8 : 0 alpha, 1 beta, 3 rho0, 4 carry
   int* fl;                // R * 4 : live, nonfinite, breakdown_at, diverged_at
   const CgHist* h = nullptr;  // run_batch histories (standalone CG kernel only)
+  int dbg = 0;                // diagnostic bits (FPM_DEBUG): 16 skip matvec rows, 64 skip owner sums
 };
 
 // Owner of the sequential sums of slot g (which = 0: phi/rho1/carry,
@@ -505,7 +506,8 @@ __device__ void cg_group(CgSmem<K>& S, int Rv, int iters, bool bj, bool textbook
       if (!S.fl[g * 4]) continue;
       if (tr && tid == 0 && it == 2) tr[75] = clock64();
       C wc;
-      if constexpr (NC > 0) wc = mv_row_n<K, NC>(S.At + (g * N + i) * S.ldA, S.pmv + g * N, fm);
+      if (S.dbg & 16) wc = A::rnd(make_double2(1.0, 0.0), fm);
+      else if constexpr (NC > 0) wc = mv_row_n<K, NC>(S.At + (g * N + i) * S.ldA, S.pmv + g * N, fm);
       else wc = mv_row<K>(S.At + (g * N + i) * S.ldA, S.pmv + g * N, N, fm);
       if (tr && tid == 0 && it == 2) tr[76] = clock64() + (h2u(*reinterpret_cast<__half2*>(&wc)) == 12345u);
       S.w[q] = A::wide(wc);
@@ -522,7 +524,7 @@ __device__ void cg_group(CgSmem<K>& S, int Rv, int iters, bool bj, bool textbook
       const int g = og;
       const bool st = tr && g == 0 && it == 2;
       if (st) tr[78] = clock64();
-      const double2 phi = csum(S.tphi + g * N);
+      const double2 phi = (S.dbg & 64) ? make_double2(1.0, 0.0) : csum(S.tphi + g * N);
       if (st) tr[79] = clock64() + (phi.x == 1.234e300);
       const double2 rho0 = rho_fresh ? S.sc[g * 8 + 3] : S.sc[g * 8 + 4];
       S.sc[g * 8 + 3] = rho0;
@@ -599,7 +601,7 @@ __device__ void cg_group(CgSmem<K>& S, int Rv, int iters, bool bj, bool textbook
         S.fl[g * 4] = 0;
         if (H && H->be) H->be[h_at(it - 1, g)] = make_double2(0.0, 0.0);
       } else {
-        const double2 rho1 = csum(S.tr1 + g * N);
+        const double2 rho1 = (S.dbg & 64) ? make_double2(1.0, 0.0) : csum(S.tr1 + g * N);
         const double2 be = wdiv<WK>(rho1, S.sc[g * 8 + 3], fw);
         S.sc[g * 8 + 1] = be;
         S.sc[g * 8 + 4] = rho1;

@@ -170,6 +170,36 @@ __global__ void __launch_bounds__(512, 2) v4(double2* out, int reps) {
   out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+// V5: 4x2 tiles, 512 threads per CTA (16 warps = 4 per SM sub-partition),
+// one CTA per SM, register cap 128 (as the v1 sweep)
+__global__ void __launch_bounds__(512, 1) v5(double2* out, int reps) {
+  __shared__ double2 H[ROWS * NP];
+  for (int i = threadIdx.x; i < ROWS * NP; i += blockDim.x) H[i] = make_double2(1e-3 * i, 2e-3 * (i & 7));
+  __syncthreads();
+  const int t = threadIdx.x % 240;
+  const int d = 1 + (t >> 1) / 16, a = (t >> 1) % 16, c = (a + d) % 16, h = t & 1;
+  double2 acc[8];
+  for (int k = 0; k < 8; ++k) acc[k] = make_double2(0, 0);
+  const double2* pa = H + a;
+  const double2* pc = H + c + NB * 2 * h;
+  for (int r = 0; r < reps; ++r)
+#pragma unroll 2
+    for (int m = 0; m < ROWS; ++m) {
+      double2 hi[4], hj[2];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) hi[u] = pa[m * NP + NB * u];
+#pragma unroll
+      for (int v = 0; v < 2; ++v) hj[v] = pc[m * NP + NB * v];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 2; ++v) cmac(acc[u * 2 + v], hi[u], hj[v]);
+    }
+  double2 s = make_double2(0, 0);
+  for (int k = 0; k < 8; ++k) { s.x += acc[k].x; s.y += acc[k].y; }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 int main() {
   double2* d;
   cudaMalloc(&d, (size_t)148 * 8 * 512 * sizeof(double2));
@@ -189,6 +219,19 @@ int main() {
     cudaEventElapsedTime(&ms, e0, e1);
     double ops = (double)blocks * thr * reps * ROWS * 128.0;
     printf("v1 %3d threads/CTA (1 CTA/SM resident): %6.2f TFLOP/s\n", thr, ops / (ms * 1e-3) / 1e12);
+  }
+  cudaFuncSetAttribute(v5, cudaFuncAttributeMaxDynamicSharedMemorySize, 150 * 1024);
+  for (int thr : {256, 512}) {
+    const int blocks = 148 * 4 * 512 / thr;
+    v5<<<blocks, thr, 150 * 1024>>>(d, reps);
+    cudaEventRecord(e0);
+    v5<<<blocks, thr, 150 * 1024>>>(d, reps);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    double ops = (double)blocks * thr * reps * ROWS * 64.0;
+    printf("v5 (4x2) %3d threads/CTA: %6.2f TFLOP/s\n", thr, ops / (ms * 1e-3) / 1e12);
   }
   return 0;
 }
