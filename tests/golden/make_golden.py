@@ -203,7 +203,40 @@ def _ber_run():
     return out
 
 
+CONV_RUN_CFG = {"kind": "convergence", "channel": {"M": 16, "K": 4, "zeta_r": 0.3, "zeta_t": 0.3},
+                "detectors": [{"algorithm": "cg"},
+                              {"algorithm": "fp_bj_cg", "L": 2, "matvec": "fp16", "inner": "fp16"},
+                              {"algorithm": "fp_cg", "matvec": "bfloat16", "inner": "bfloat16",
+                               "rho_update": "textbook", "label": "fpcg_bf16_tb"},
+                              {"algorithm": "lmmse"}],
+                "run": {"trials": 40, "iters": 6, "snr_db": 10.0, "chunk": 16}}
+
+
+def _conv_run():
+    """The reference's convergence artefacts (experiments.py:281-325):
+    convergence_/trace_<detector>.csv + summary.csv, written by its own code."""
+    import tempfile
+    from pathlib import Path
+    from fpmimo.experiments import _run_convergence
+    out = {}
+    with tempfile.TemporaryDirectory() as d:
+        for f in _run_convergence(CONV_RUN_CFG, Path(d), 7, 1):
+            out[f] = (Path(d) / f).read_text()
+    return out
+
+
+def _write_run(name, files):
+    os.makedirs(os.path.join(OUT, name), exist_ok=True)
+    for f, text in files.items():
+        with open(os.path.join(OUT, name, f), "w") as fh:
+            fh.write(text)
+
+
 def main():
+    if "--runs-only" in sys.argv:
+        _write_run("ber_run", _ber_run())
+        _write_run("conv_run", _conv_run())
+        return
     for name, (M, K, zeta, snr, T, kw) in CASES.items():
         d = _detector_case(name, M, K, zeta, snr, T, kw)
         np.savez_compressed(os.path.join(OUT, f"{name}.npz"), **d)
@@ -213,10 +246,8 @@ def main():
     np.savez_compressed(os.path.join(OUT, "kernel_kats.npz"), **_kernel_kats())
     np.savez_compressed(os.path.join(OUT, "hist_cg.npz"), **_cg_history())
     np.savez_compressed(os.path.join(OUT, "lmmse.npz"), **_lmmse())
-    os.makedirs(os.path.join(OUT, "ber_run"), exist_ok=True)
-    for f, text in _ber_run().items():
-        with open(os.path.join(OUT, "ber_run", f), "w") as fh:
-            fh.write(text)
+    _write_run("ber_run", _ber_run())
+    _write_run("conv_run", _conv_run())
     # slicer known answers (detect.py:70-84, tests/test_detect.py:55-69)
     vals = np.array([complex(np.nan, 1.0), complex(np.inf, np.inf), complex(-np.inf, -np.inf),
                      -2 / np.sqrt(10), 0.0, 2 / np.sqrt(10), complex(0.3, -0.9), complex(-0.0, 0.0)])
