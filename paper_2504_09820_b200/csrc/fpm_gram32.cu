@@ -17,37 +17,74 @@
 
 #include "../../include/fpmimo_b200.h"
 #include "fpm_common.cuh"
+#include "fpm_ptx.cuh"
 
 namespace fpm {
 
-__device__ __forceinline__ void cmac_conj32(float2& acc, float2 hi, float2 hj) {
-  const float pr = __fadd_rn(__fmul_rn(hi.x, hj.x), __fmul_rn(hi.y, hj.y));
-  const float pi = __fsub_rn(__fmul_rn(hi.x, hj.y), __fmul_rn(hi.y, hj.x));
-  acc.x = __fadd_rn(acc.x, pr);
-  acc.y = __fadd_rn(acc.y, pi);
+// Packed binary32 pairs (FMUL2 / FFMA2, f32x2 PTX, sm_100a): two lanes per
+// instruction, each an IEEE binary32 op rounded to nearest.  ptxas contracts
+// even explicit-.rn f32x2 mul/add pairs into FFMA2, so every add is written
+// as fma(x, k, y) with k = (1, 1) or (1, -1) passed in at run time: k is
+// opaque to the compiler, x*k is exact, and the fma rounds once -- the same
+// bits as add.rn / sub.rn, and nothing left to contract.
+typedef unsigned long long f2x;
+__device__ __forceinline__ f2x pk2(float a, float b) {
+  f2x r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
 }
+__device__ __forceinline__ float2 upk2(f2x r) {
+  float2 v;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(r));
+  return v;
+}
+__device__ __forceinline__ f2x mul2(f2x a, f2x b) {
+  f2x d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f2x fma2(f2x a, f2x b, f2x c) {
+  f2x d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+
+// acc += conj(h_i) h_j:  P1 = (hr_i hr_j, hr_i hi_j), P2 = (hi_i hi_j, hi_i hr_j),
+// (pr, pi) = P1 + (1, -1) P2, acc = acc + (pr, pi)
+struct Cj32 {
+  f2x one, pm;  // (1, 1), (1, -1) -- run-time values
+  __device__ __forceinline__ void mac(f2x& acc, float2 hi, float2 hj) const {
+    const f2x p1 = mul2(pk2(hi.x, hi.x), pk2(hj.x, hj.y));
+    const f2x p2 = mul2(pk2(hi.y, hi.y), pk2(hj.y, hj.x));
+    acc = fma2(fma2(p2, pm, p1), one, acc);
+  }
+};
 
 constexpr int kG32Rows = 16;  // antenna rows per staged chunk
 constexpr int kG32Jobs = 2;   // jobs per thread (N = 128: 512 jobs on 256 threads)
 
+template <int NB>  // nb = Np/4 at compile time (0 = run time): immediate-offset operand loads
 __global__ void __launch_bounds__(256) fpm_gram32_kernel(const double2* __restrict__ H, const double2* __restrict__ y,
                                                           long T, int M, int N, double sigma2, double2* __restrict__ A,
-                                                          double2* __restrict__ b) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  const int Np = (N + 7) / 8 * 8, nb = Np / 4;
-  float2* hs = reinterpret_cast<float2*>(smem);          // [kG32Rows][Np]
-  float2* ysm = hs + kG32Rows * Np;                      // [kG32Rows]
+                                                          double2* __restrict__ b, f2x k_one, f2x k_pm) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int Np = NB > 0 ? 4 * NB : (N + 7) / 8 * 8, nb = NB > 0 ? NB : Np / 4;
+  const int raw_bytes = kG32Rows * N * 16 + kG32Rows * 16;  // one binary64 chunk: H rows, then y entries
+  float2* hs = reinterpret_cast<float2*>(smem + 2 * raw_bytes);  // [kG32Rows][Np] binary32
+  float2* ysm = hs + kG32Rows * Np;                             // [kG32Rows]
+  uint64_t* full = reinterpret_cast<uint64_t*>(ysm + kG32Rows);  // one per raw buffer
   const long t = blockIdx.x;
   const int tid = threadIdx.x, nt = blockDim.x;
   const int njobs = nb * (nb / 2 - 1) + nb;
+  const Cj32 cj{k_one, k_pm};
   GramJob job[kG32Jobs];
-  float2 acc[kG32Jobs][16];
+  f2x acc[kG32Jobs][16];
 #pragma unroll
   for (int s = 0; s < kG32Jobs; ++s) {
     const int q = tid + s * nt;
     job[s] = q < njobs ? gram_job(q, 1, nb) : GramJob{-1, 0, 0, 0, 0, 0};
 #pragma unroll
-    for (int k = 0; k < 16; ++k) acc[s][k] = make_float2(0.f, 0.f);
+    for (int k = 0; k < 16; ++k) acc[s][k] = 0ull;
   }
   // matched-filter chains: q in [0, 2N) -> entry n, part (0 re / 1 im)
   const bool chain = tid < 2 * N;
@@ -55,20 +92,39 @@ __global__ void __launch_bounds__(256) fpm_gram32_kernel(const double2* __restri
   float ca = 0.f;
   const double2* Ht = H + t * (long)M * N;
   const double2* yt = y + t * (long)M;
+  const int nch = (M + kG32Rows - 1) / kG32Rows;
+  // chunk c (binary64, as it lies in HBM) -> raw buffer c & 1, one bulk copy each for H and y
+  auto issue = [&](int c) {
+    const int m0 = c * kG32Rows, rows = min(kG32Rows, M - m0);
+    unsigned char* dst = smem + (c & 1) * raw_bytes;
+    mbar_expect_tx(full + (c & 1), (uint32_t)(rows * N * 16 + rows * 16));
+    bulk_g2s(dst, Ht + (long)m0 * N, (uint32_t)(rows * N * 16), full + (c & 1));
+    bulk_g2s(dst + kG32Rows * N * 16, yt + m0, (uint32_t)(rows * 16), full + (c & 1));
+  };
+  if (tid == 0) {
+    mbar_init(full, 1);
+    mbar_init(full + 1, 1);
+    fence_mbar_init();
+    issue(0);
+  }
 #pragma unroll 1
-  for (int m0 = 0; m0 < M; m0 += kG32Rows) {
-    const int rows = min(kG32Rows, M - m0);
-    __syncthreads();
+  for (int c = 0; c < nch; ++c) {
+    const int m0 = c * kG32Rows, rows = min(kG32Rows, M - m0);
+    __syncthreads();  // chunk c-1 accumulated by all: hs free, raw buffer (c+1)&1 long converted
+    if (tid == 0 && c + 1 < nch) issue(c + 1);  // lands while chunk c is converted and accumulated
+    mbar_wait(full + (c & 1), (uint32_t)((c >> 1) & 1));
+    const double2* raw = reinterpret_cast<const double2*>(smem + (c & 1) * raw_bytes);
     for (int q = tid; q < rows * Np; q += nt) {
-      const int r = q / Np, c = q - r * Np;
-      const double2 v = c < N ? Ht[(long)(m0 + r) * N + c] : make_double2(0.0, 0.0);
+      const int r = q / Np, cc = q - r * Np;
+      const double2 v = cc < N ? raw[r * N + cc] : make_double2(0.0, 0.0);
       hs[q] = make_float2(__double2float_rn(v.x), __double2float_rn(v.y));
     }
-    for (int r = tid; r < rows; r += nt) {
-      const double2 v = yt[m0 + r];
-      ysm[r] = make_float2(__double2float_rn(v.x), __double2float_rn(v.y));
+    if (tid < rows) {
+      const double2 v = raw[kG32Rows * N + tid];
+      ysm[tid] = make_float2(__double2float_rn(v.x), __double2float_rn(v.y));
     }
     __syncthreads();
+    (void)m0;
 #pragma unroll
     for (int s = 0; s < kG32Jobs; ++s) {
       const GramJob& jb = job[s];
@@ -85,7 +141,7 @@ __global__ void __launch_bounds__(256) fpm_gram32_kernel(const double2* __restri
 #pragma unroll
           for (int u = 0; u < 4; ++u)
 #pragma unroll
-            for (int v = 0; v < 4; ++v) cmac_conj32(acc[s][u * 4 + v], hi[u], hj[v]);
+            for (int v = 0; v < 4; ++v) cj.mac(acc[s][u * 4 + v], hi[u], hj[v]);
         }
       } else {
 #pragma unroll 1
@@ -102,18 +158,18 @@ __global__ void __launch_bounds__(256) fpm_gram32_kernel(const double2* __restri
 #pragma unroll
           for (int u = 0; u < 4; ++u)
 #pragma unroll
-            for (int v = u + 1; v < 4; ++v) cmac_conj32(acc[s][p++], hx[u], hx[v]);
+            for (int v = u + 1; v < 4; ++v) cj.mac(acc[s][p++], hx[u], hx[v]);
 #pragma unroll
           for (int w = 0; w < 2; ++w)
 #pragma unroll
-            for (int v = 0; v < 4; ++v) cmac_conj32(acc[s][6 + w * 4 + v], hy[w], hz[v]);
-          float dg[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) dg[u] = __fadd_rn(__fmul_rn(hx[u].x, hx[u].x), __fmul_rn(hx[u].y, hx[u].y));
-          acc[s][14].x = __fadd_rn(acc[s][14].x, dg[0]);
-          acc[s][14].y = __fadd_rn(acc[s][14].y, dg[1]);
-          acc[s][15].x = __fadd_rn(acc[s][15].x, dg[2]);
-          acc[s][15].y = __fadd_rn(acc[s][15].y, dg[3]);
+            for (int v = 0; v < 4; ++v) cj.mac(acc[s][6 + w * 4 + v], hy[w], hz[v]);
+          // diagonal: (|h_a|^2, |h_a+nb|^2) and (|h_a+2nb|^2, |h_a+3nb|^2)
+          const f2x q0 = mul2(pk2(hx[0].x, hx[1].x), pk2(hx[0].x, hx[1].x));
+          const f2x q1 = mul2(pk2(hx[0].y, hx[1].y), pk2(hx[0].y, hx[1].y));
+          const f2x q2 = mul2(pk2(hx[2].x, hx[3].x), pk2(hx[2].x, hx[3].x));
+          const f2x q3 = mul2(pk2(hx[2].y, hx[3].y), pk2(hx[2].y, hx[3].y));
+          acc[s][14] = fma2(fma2(q1, cj.one, q0), cj.one, acc[s][14]);
+          acc[s][15] = fma2(fma2(q3, cj.one, q2), cj.one, acc[s][15]);
         }
       }
     }
@@ -131,7 +187,8 @@ __global__ void __launch_bounds__(256) fpm_gram32_kernel(const double2* __restri
   // emit: final / mirror entries in binary32, widened to the fp64 carriers
   const float s2f = __double2float_rn(sigma2);
   double2* At = A + t * (long)N * N;
-  auto put = [&](int i, int j, float2 G) {
+  auto put = [&](int i, int j, f2x Gp) {
+    const float2 G = upk2(Gp);
     At[(long)i * N + j] = make_double2((double)__fadd_rn(G.x, 0.f), (double)__fadd_rn(G.y, 0.f));
     At[(long)j * N + i] = make_double2((double)__fadd_rn(G.x, 0.f), (double)__fsub_rn(0.f, G.y));
   };
@@ -164,7 +221,8 @@ __global__ void __launch_bounds__(256) fpm_gram32_kernel(const double2* __restri
           const int i = jb.y + nb * (jb.yo + w), j = jb.c + nb * v;
           if (i < N && j < N) put(i, j, acc[s][6 + w * 4 + v]);
         }
-      const float dg[4] = {acc[s][14].x, acc[s][14].y, acc[s][15].x, acc[s][15].y};
+      const float2 d01 = upk2(acc[s][14]), d23 = upk2(acc[s][15]);
+      const float dg[4] = {d01.x, d01.y, d23.x, d23.y};
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int i = jb.a + nb * u;
@@ -175,14 +233,27 @@ __global__ void __launch_bounds__(256) fpm_gram32_kernel(const double2* __restri
   if (chain) reinterpret_cast<double*>(b + t * N + cn)[cpart] = (double)ca;
 }
 
+// (1, 1) and (1, -1) as binary32 pairs, lane 0 in the low word
+static const f2x g32_one = 0x3F8000003F800000ull, g32_pm = 0xBF8000003F800000ull;
+
 int launch_gram32(const double2* H, const double2* y, long T, int M, int N, double sigma2, double2* A, double2* b,
                   cudaStream_t st) {
   const int Np = (N + 7) / 8 * 8, nb = Np / 4;
   const int njobs = nb * (nb / 2 - 1) + nb;
   const int threads = std::max(2 * N, std::min(256, (njobs + 31) / 32 * 32));
   if ((njobs + threads - 1) / threads > kG32Jobs || threads > 256) return FPM_EUNSUPPORTED;
-  const int smem = (kG32Rows * Np + kG32Rows) * 8;
-  fpm_gram32_kernel<<<(unsigned)T, threads, smem, st>>>(H, y, T, M, N, sigma2, A, b);
+  const int smem = 2 * (kG32Rows * N * 16 + kG32Rows * 16) + (kG32Rows * Np + kG32Rows) * 8 + 16;
+  if (smem > 48 * 1024) {
+    cudaFuncSetAttribute(fpm_gram32_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(fpm_gram32_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(fpm_gram32_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  }
+  if (nb == 32)
+    fpm_gram32_kernel<32><<<(unsigned)T, threads, smem, st>>>(H, y, T, M, N, sigma2, A, b, g32_one, g32_pm);
+  else if (nb == 16)
+    fpm_gram32_kernel<16><<<(unsigned)T, threads, smem, st>>>(H, y, T, M, N, sigma2, A, b, g32_one, g32_pm);
+  else
+    fpm_gram32_kernel<0><<<(unsigned)T, threads, smem, st>>>(H, y, T, M, N, sigma2, A, b, g32_one, g32_pm);
   count_launch();
   return cudaGetLastError() == cudaSuccess ? FPM_OK : FPM_ECUDA;
 }

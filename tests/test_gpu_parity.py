@@ -551,3 +551,19 @@ def test_fp32_gram_extension(oracle, M, N):
     r = detect(det, H, y, s2, bits, minv=mats, want_bits=True)
     assert bits_equal(r.x, ref.x)
     np.testing.assert_array_equal(r.bits, O.demod16(ref.x))
+
+
+@pytest.mark.parametrize("scale", [1e-20, 3e-23, 3e19])
+def test_fp32_gram_subnormal_and_overflow(oracle, scale):
+    """Packed binary32 Gram (FMUL2 / FFMA2) keeps IEEE subnormals and
+    overflow: products in the binary32 subnormal range (scale 1e-20, 3e-23)
+    and sums past FLT_MAX (3e19: inf entries) match the NumPy float32 restatement bit for
+    bit."""
+    from paper_2504_09820_b200.detect import gram_mf
+    O = oracle
+    H, y, _, s2 = O.simulate(64, 32, 0.5, 10.0, range(3), 23)
+    H, y = H * scale, y * scale
+    with np.errstate(over="ignore", invalid="ignore"):
+        A, b = O.gram_mf_fp32(H, y, s2)
+    Ag, bg = gram_mf(H, y, s2, gram="fp32")
+    assert bits_equal(Ag, A) and bits_equal(bg, b)
