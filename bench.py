@@ -14,8 +14,10 @@ channel model sampled on the GPU; 137 GB of H >> L2, so no flush needed).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-Under torchrun each rank takes a contiguous 1/N of the 2^20 realizations
-(strong scaling); the only collective is the int64 counter all-reduce.
+Under torchrun every rank detects its own c5 batch of 2^20 realizations
+(trials [rank*2^20, (rank+1)*2^20); weak scaling, value = all ranks'
+detections / max-over-ranks time); the only collective is the int64 counter
+all-reduce.
 `--impl reference` times the oracle port of the reference CPU path
 (oracle/fpm_oracle.py) on all host cores.
 """
@@ -195,10 +197,11 @@ def run_ours(args):
                "sample": f"{n} realizations ({args.cpu_per_worker}/worker x {w} processes) of the same "
                          f"workload, oracle/fpm_oracle.py (NumPy port of the reference path), wall {wall:.1f}s"}
 
-    T_total = args.T
-    per = T_total // world
-    t0 = rank * per
-    T = per if rank < world - 1 else T_total - t0
+    # weak scaling: every rank detects its own c5 batch of args.T realizations
+    # (trial indices [rank*T, (rank+1)*T)); no data-path collective
+    T = args.T
+    T_total = T * world
+    t0 = rank * T
     free, total = torch.cuda.mem_get_info(dev)
     need = T * (16 * M * N + 16 * M + 4 * N + 16 * N + 8) + (6 << 30)
     pool = T
@@ -312,13 +315,13 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3), "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": f"f64 work / {args.precision} matvec+inner",
+            "scaling": "weak", "vs_baseline": None, "dtype": f"f64 work / {args.precision} matvec+inner",
             "data": "synthetic: the reference's link model sampled on the GPU (fpm_gen_trials keyed Philox streams; "
                     "Kronecker zeta=0.5, W ~ CN(0,1/M), 16-QAM Gray, AWGN at the reference SNR convention)",
             "config": {"workload": f"c5: FP-BJ-CG L={L}, M={M} x N={N}, zeta={ZETA}, 16-QAM, SNR {SNR_DB} dB, "
-                                   f"{ITERS} iters, batch {T_total} realizations/step",
+                                   f"{ITERS} iters, batch {T} realizations/step per GPU",
                        "precision": {"work": "fp64", "matvec": args.precision, "inner": args.precision},
-                       "batch": T_total, "resident_pool": pool, "l2": "inputs (137 GB) >> L2; no flush",
+                       "batch_per_gpu": T, "global_batch": T_total, "resident_pool": pool, "l2": "inputs (137 GB) >> L2; no flush",
                        "parallelism": f"dp{world} (contiguous realization shards)",
                        "input_gen_s": round(gen_s, 2)},
             "gpu_launches": int(launches),
@@ -362,7 +365,7 @@ def run_reference(args):
     value = sum(n for _, n, _ in vals) / sum(wl for _, _, wl in vals)
     line = {"metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(1e3 * tot / args.steps, 1), "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": f"f64 work / {args.precision} matvec+inner (emulated)",
+            "scaling": "weak", "vs_baseline": None, "dtype": f"f64 work / {args.precision} matvec+inner (emulated)",
             "data": "synthetic (reference generator restated in oracle/)", "impl": "reference",
             "config": {"workload": f"c5: FP-BJ-CG L={L}, M={M} x N={N}, zeta={ZETA}, 16-QAM, SNR {SNR_DB} dB, "
                                    f"{ITERS} iters", "batch_per_step": vals[0][1]},

@@ -37,8 +37,15 @@ namespace fpm {
 #ifndef FPM_CG_SLEEP_NS
 #define FPM_CG_SLEEP_NS 0
 #endif
-#define FPM_PWAIT(b, p) (FPM_PRODUCER_SLEEP_NS ? mbar_wait_sleep((b), (p), FPM_PRODUCER_SLEEP_NS) : mbar_wait((b), (p)))
-#define FPM_CWAIT(b, p) (FPM_CG_SLEEP_NS ? mbar_wait_sleep((b), (p), FPM_CG_SLEEP_NS) : mbar_wait((b), (p)))
+#ifndef FPM_WAIT_HINT_NS  // > 0: producer / CG-side waits suspend in hardware (try_wait hint) instead of polling
+#define FPM_WAIT_HINT_NS 0
+#endif
+#define FPM_PWAIT(b, p)                                                                                       \
+  (FPM_WAIT_HINT_NS ? mbar_wait_suspend((b), (p), FPM_WAIT_HINT_NS)                                          \
+   : FPM_PRODUCER_SLEEP_NS ? mbar_wait_sleep((b), (p), FPM_PRODUCER_SLEEP_NS) : mbar_wait((b), (p)))
+#define FPM_CWAIT(b, p)                                                                                       \
+  (FPM_WAIT_HINT_NS ? mbar_wait_suspend((b), (p), FPM_WAIT_HINT_NS)                                          \
+   : FPM_CG_SLEEP_NS ? mbar_wait_sleep((b), (p), FPM_CG_SLEEP_NS) : mbar_wait((b), (p)))
 
 struct WsLayout {  // byte offsets inside one hand-off slot
   int at, b, d, bytes;
