@@ -79,7 +79,7 @@ def modulate(bits, qam: int = 16):
     bps = 4 if qam == 16 else 6
     if bits.shape[-1] % bps:
         raise ContractViolation(f"bit count must be a multiple of {bps}")
-    g = bits.reshape(*bits.shape[:-1], -1, bps).long()
+    g = bits.reshape(*bits.shape[:-1], bits.shape[-1] // bps, bps).long()
     if qam == 16:
         lv = torch.as_tensor(_LEVEL_OF_PAIR16, dtype=torch.float64, device=bits.device)
         re, im = lv[2 * g[..., 0] + g[..., 1]], lv[2 * g[..., 2] + g[..., 3]]

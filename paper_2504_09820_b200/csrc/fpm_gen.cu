@@ -90,7 +90,8 @@ using namespace fpm;
 extern "C" int fpm_gen_trials(uint64_t seed, int32_t context, int32_t point, int64_t trial0, int64_t T, int32_t M,
                               int32_t N, int32_t nbits, double* W, uint8_t* bits, double* noise, double* csi,
                               void* stream) {
-  if (T < 0 || M < 1 || N < 1 || nbits < 0 || trial0 < 0 || !W || !noise || (nbits && !bits)) return FPM_EINVAL;
+  if (T < 0 || M < 1 || N < 1 || nbits < 0 || trial0 < 0 || (T > 0 && (!W || !noise || (nbits && !bits))))
+    return FPM_EINVAL;
   if (context < 0 || context >= (1 << 12) || point < 0 || point >= (1 << 16)) return FPM_EINVAL;  // rng.py:21-26
   if (T == 0) return FPM_OK;
   const uint32_t k0 = (uint32_t)seed;

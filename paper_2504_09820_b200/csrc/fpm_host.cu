@@ -664,7 +664,7 @@ int fpm_probe_fp64(int64_t iters, double* dp_ops_per_s) {
 
 int fpm_gram(const double* H, const double* y, int64_t T, int32_t M, int32_t N, double sigma2, double* A,
              double* b, void* stream) {
-  if (T < 0 || M < 1 || N < 1 || !H || !y || !A || !b) return FPM_EINVAL;
+  if (T < 0 || M < 1 || N < 1 || (T > 0 && (!H || !y || !A || !b))) return FPM_EINVAL;  // T = 0: empty batch
   if (N > kMaxN || M > kMaxM) return FPM_EUNSUPPORTED;
   if (T == 0) return FPM_OK;
   {
@@ -724,7 +724,7 @@ int fpm_gram(const double* H, const double* y, int64_t T, int32_t M, int32_t N, 
 
 int fpm_bj_setup(const double* A, int64_t T, int32_t N, int32_t L, int32_t allow_ragged, double* Minv,
                  int32_t* bad_block, void* stream) {
-  if (T < 0 || N < 1 || L < 1 || L > N || !A || !Minv) return FPM_EINVAL;
+  if (T < 0 || N < 1 || L < 1 || L > N || (T > 0 && (!A || !Minv))) return FPM_EINVAL;
   if (N % L && !allow_ragged) return FPM_EINVAL;  // solvers.py:240-241
   if (N > kMaxN || L > kMaxL) return FPM_EUNSUPPORTED;
   if (T == 0) return FPM_OK;
@@ -760,7 +760,7 @@ int fpm_bj_setup(const double* A, int64_t T, int32_t N, int32_t L, int32_t allow
 int fpm_cg_ex(const double* A, const double* b, const double* Minv, int64_t T, int32_t N, int32_t L, int32_t iters,
               const fpm_precision* prec, int32_t rho_update, double* x, int32_t* breakdown_at,
               int32_t* diverged_at, const fpm_cg_history* hist, void* stream) {
-  if (T < 0 || N < 1 || !A || !b || !x || !breakdown_at || !diverged_at) return FPM_EINVAL;
+  if (T < 0 || N < 1 || (T > 0 && (!A || !b || !x || !breakdown_at || !diverged_at))) return FPM_EINVAL;
   if (iters < 1) return FPM_EINVAL;                                                   // solvers.py:282-283
   if (rho_update != FPM_RHO_AS_WRITTEN && rho_update != FPM_RHO_TEXTBOOK) return FPM_EINVAL;  // :280-281
   int rc = check_prec(prec);
@@ -833,7 +833,7 @@ int fpm_cg(const double* A, const double* b, const double* Minv, int64_t T, int3
 
 int fpm_gram32(const double* H, const double* y, int64_t T, int32_t M, int32_t N, double sigma2, double* A,
                double* b, void* stream) {
-  if (T < 0 || M < 1 || N < 1 || !H || !y || !A || !b) return FPM_EINVAL;
+  if (T < 0 || M < 1 || N < 1 || (T > 0 && (!H || !y || !A || !b))) return FPM_EINVAL;  // T = 0: empty batch
   if (N > kMaxN || M > kMaxM) return FPM_EUNSUPPORTED;
   if (T == 0) return FPM_OK;
   return launch_gram32(reinterpret_cast<const double2*>(H), reinterpret_cast<const double2*>(y), T, M, N, sigma2,
@@ -841,7 +841,7 @@ int fpm_gram32(const double* H, const double* y, int64_t T, int32_t M, int32_t N
 }
 
 int fpm_lmmse(const double* A, const double* b, int64_t T, int32_t N, double* x, int32_t* nonpd, void* stream) {
-  if (T < 0 || N < 1 || !A || !b || !x) return FPM_EINVAL;
+  if (T < 0 || N < 1 || (T > 0 && (!A || !b || !x))) return FPM_EINVAL;
   if (N > kMaxN) return FPM_EUNSUPPORTED;
   if (T == 0) return FPM_OK;
   return launch_lmmse(reinterpret_cast<const double2*>(A), reinterpret_cast<const double2*>(b), T, N,
@@ -850,7 +850,7 @@ int fpm_lmmse(const double* A, const double* b, int64_t T, int32_t N, double* x,
 
 int fpm_slice_count(const double* x, const uint8_t* tx_bits, int64_t T, int32_t N, int32_t qam,
                     uint8_t* rx_bits, int64_t* counters, void* stream) {
-  if (T < 0 || N < 1 || !x || !counters || (qam != 16 && qam != 64)) return FPM_EINVAL;
+  if (T < 0 || N < 1 || !counters || (T > 0 && !x) || (qam != 16 && qam != 64)) return FPM_EINVAL;
   if (T == 0) return FPM_OK;
   const long TN = T * (long)N;
   const int tpb = 256;
@@ -1015,7 +1015,7 @@ int fpm_detect(const double* H, const double* y, const uint8_t* tx_bits, int64_t
                double sigma2, int32_t algorithm, int32_t L, int32_t iters, const fpm_precision* prec,
                int32_t rho_update, int32_t qam, const double* Minv_in, double* x, int32_t* breakdown_at,
                int32_t* diverged_at, uint8_t* rx_bits, int64_t* counters, void* stream) {
-  if (!H || !y || !x || !breakdown_at || !diverged_at || !counters) return FPM_EINVAL;
+  if (!counters || (T > 0 && (!H || !y || !x || !breakdown_at || !diverged_at))) return FPM_EINVAL;
   DetectArgs a;
   Kinds k;
   int threads = 0, grid = 0;
@@ -1040,7 +1040,7 @@ int fpm_detect_host(const double* H, const double* y, const uint8_t* tx_bits, in
                     double sigma2, int32_t algorithm, int32_t L, int32_t iters, const fpm_precision* prec,
                     int32_t rho_update, int32_t qam, const double* Minv_in, double* x, int32_t* breakdown_at,
                     int32_t* diverged_at, uint8_t* rx_bits, int64_t* counters, int64_t chunk) {
-  if (!H || !y || !x || !breakdown_at || !diverged_at || !counters) return FPM_EINVAL;
+  if (!counters || (T > 0 && (!H || !y || !x || !breakdown_at || !diverged_at))) return FPM_EINVAL;
   DetectArgs a;
   Kinds k;
   int threads = 0, grid0 = 0;

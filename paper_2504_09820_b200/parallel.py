@@ -184,7 +184,8 @@ def counters_from_arrays(rx_bits, tx_bits, diverged, breakdown, bits_per_symbol:
     out = np.zeros(_lib.NCOUNTERS, np.int64)
     diff = rx != tx
     out[_lib.COUNTERS.index("bit_errors")] = int(diff.sum())
-    out[_lib.COUNTERS.index("symbol_errors")] = int(diff.reshape(T, -1, bits_per_symbol).any(-1).sum())
+    sym = diff.reshape(T, diff.shape[-1] // bits_per_symbol, bits_per_symbol)
+    out[_lib.COUNTERS.index("symbol_errors")] = int(sym.any(-1).sum())
     out[_lib.COUNTERS.index("diverged")] = int((np.asarray(diverged) >= 0).sum())
     out[_lib.COUNTERS.index("breakdown")] = int((np.asarray(breakdown) >= 0).sum())
     out[_lib.COUNTERS.index("trials")] = T

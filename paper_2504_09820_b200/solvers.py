@@ -105,7 +105,7 @@ def pack_blocks(mats, N: int, L: int):
     out = np.zeros((T, N * L), np.complex128)
     for k, m in enumerate(mats):
         Lk = m.shape[-1]
-        out[:, k * L * L:k * L * L + Lk * Lk] = np.asarray(m, np.complex128).reshape(T, -1)
+        out[:, k * L * L:k * L * L + Lk * Lk] = np.asarray(m, np.complex128).reshape(T, Lk * Lk)
     return out
 
 

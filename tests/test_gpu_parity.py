@@ -567,3 +567,36 @@ def test_fp32_gram_subnormal_and_overflow(oracle, scale):
         A, b = O.gram_mf_fp32(H, y, s2)
     Ag, bg = gram_mf(H, y, s2, gram="fp32")
     assert bits_equal(Ag, A) and bits_equal(bg, b)
+
+
+@pytest.mark.gpu
+def test_empty_batches_match_reference_shapes():
+    """T = 0 through every boundary call returns the reference's empty
+    shapes (run_batch / build_blocks_batch / _solve_direct_batch accept an
+    empty batch, solvers.py:262-393, linalg.py:223-231) and launches nothing
+    that faults."""
+    from paper_2504_09820_b200.detect import DetectorSpec, detect, gram_mf
+    from paper_2504_09820_b200.solvers import PrecisionConfig, build_blocks_batch, run_batch, solve_direct_batch
+    A = np.zeros((0, 8, 8), np.complex128)
+    b = np.zeros((0, 8), np.complex128)
+    r = run_batch(A, b, 3)
+    assert r.x.shape == (0, 8) and r.diverged_at.shape == (0,) and r.breakdown_at.shape == (0,)
+    assert r.residual_norms.shape == (4, 0) and r.iterate_norms.shape == (4, 0) and r.alphas.shape == (3, 0)
+    assert r.converged_at.shape == (0,)
+    bl = build_blocks_batch(A, 4)
+    assert [m.shape for m in bl.mats] == [(0, 4, 4), (0, 4, 4)]
+    r = run_batch(A, b, 3, PrecisionConfig.uniform("fp16"), blocks=bl, x_ref=b, record_gaps=True, record_iterates=True)
+    assert r.x.shape == (0, 8) and r.residual_gaps.shape == (4, 0) and r.iterates.shape == (4, 0, 8)
+    assert solve_direct_batch(A, b).shape == (0, 8)
+    H = np.zeros((0, 16, 8), np.complex128)
+    y = np.zeros((0, 16), np.complex128)
+    Ag, bg = gram_mf(H, y, 0.1)
+    assert Ag.shape == (0, 8, 8) and bg.shape == (0, 8)
+    for alg in ("fp_bj_cg", "lmmse"):
+        det = DetectorSpec(alg, iters=4, L=4, matvec="fp16", inner="fp16") if alg != "lmmse" else DetectorSpec(alg)
+        res = detect(det, H, y, 0.1, np.zeros((0, 32), np.uint8), want_bits=True)
+        assert res.x.shape == (0, 8) and res.bits.shape == (0, 32)
+        assert int(res.counters["trials"]) == 0 and int(res.counters["bit_errors"]) == 0
+    from paper_2504_09820_b200 import channel
+    b0 = channel.simulate_batch(16, 8, 0.5, 0.5, 10.0, 0, 0, 7)
+    assert b0["H"].shape == (0, 16, 8) and b0["bits"].shape == (0, 32) and b0["y"].shape == (0, 16)
