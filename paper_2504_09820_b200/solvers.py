@@ -228,11 +228,18 @@ def run_batch(A, b, max_iters: int, prec: PrecisionConfig | None = None, blocks=
     minv = None
     L = 1
     if blocks is not None:
+        # a preconditioner built for another system size or batch is a
+        # contract violation (solvers.py:222-225 apply, tests/test_solvers.py:284-290)
         if isinstance(blocks, BatchBlocks):
             L, packed = blocks.L, blocks.packed
+            if blocks.N != N or packed.shape[0] != T:
+                raise ContractViolation(f"block-Jacobi blocks are for n={blocks.N}, T={packed.shape[0]}; "
+                                        f"system has n={N}, T={T}")
         else:
             mats = blocks.mats
             L = mats[0].shape[-1]
+            if sum(m.shape[-1] for m in mats) != N or any(m.shape[0] != T for m in mats):
+                raise ContractViolation(f"block-Jacobi blocks do not partition n={N} over T={T} systems")
             packed = pack_blocks([np.asarray(m) for m in mats], N, L)
         minv = _to_dev(packed, torch.complex128)
     dev = bd.device
