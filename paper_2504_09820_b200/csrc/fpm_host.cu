@@ -1079,6 +1079,28 @@ int fpm_detect_host(const double* H, const double* y, const uint8_t* tx_bits, in
     if (cudaStreamCreateWithFlags(&st[s], cudaStreamNonBlocking) != cudaSuccess) return FPM_ECUDA;
     if (cudaMallocAsync(&buf[s], per, st[s]) != cudaSuccess) rc = FPM_ECUDA;
   }
+  // Outputs: straight to the caller's buffers per chunk when they are pinned;
+  // otherwise (pageable NumPy arrays) a copy into pageable memory would block
+  // the host between chunks and serialise the H2D stream behind every
+  // kernel, so the outputs stay on the device and go back in one copy at the end.
+  auto pinned = [](const void* q) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, q) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+  };
+  const bool direct = pinned(x) && pinned(breakdown_at) && pinned(diverged_at) && (!rx_bits || pinned(rx_bits));
+  unsigned char* obuf = nullptr;
+  const size_t oxB = (size_t)T * N * 16, ofB = (size_t)T * 4, orB = rx_bits ? (size_t)T * bps * N : 0;
+  if (!rc && !direct &&
+      cudaMallocAsync(&obuf, align_up(oxB, 256) + 2 * align_up(ofB, 256) + align_up(orB, 256), st[0]) != cudaSuccess)
+    rc = FPM_ECUDA;
+  double* ox = (double*)obuf;
+  int32_t* obk = obuf ? (int32_t*)(obuf + align_up(oxB, 256)) : nullptr;
+  int32_t* odv = obuf ? (int32_t*)(obuf + align_up(oxB, 256) + align_up(ofB, 256)) : nullptr;
+  uint8_t* orx = obuf ? obuf + align_up(oxB, 256) + 2 * align_up(ofB, 256) : nullptr;
   if (!rc && cudaMallocAsync(&dcnt, 2 * FPM_NCOUNTERS * sizeof(int64_t), st[0]) != cudaSuccess) rc = FPM_ECUDA;
   if (!rc) cudaMemsetAsync(dcnt, 0, 2 * FPM_NCOUNTERS * sizeof(int64_t), st[0]);
   if (!rc) {  // stream 1 must see the zeroed counters and its buffer
@@ -1118,10 +1140,10 @@ int fpm_detect_host(const double* H, const double* y, const uint8_t* tx_bits, in
     b.tx = tx_bits ? dtx : nullptr;
     b.T = n;
     b.minv_in = (const double2*)dm;
-    b.x = (double2*)dx;
-    b.brk = dbk;
-    b.div = ddv;
-    b.rx = rx_bits ? drx : nullptr;
+    b.x = (double2*)(direct ? dx : ox + c0 * (int64_t)N * 2);
+    b.brk = direct ? dbk : obk + c0;
+    b.div = direct ? ddv : odv + c0;
+    b.rx = rx_bits ? (direct ? drx : orx + c0 * bps * N) : nullptr;
     b.counters = reinterpret_cast<unsigned long long*>(dcnt + s * FPM_NCOUNTERS);
     if (algorithm == FPM_ALG_LMMSE) {
       rc = run_lmmse(b, M, N, st[s]);
@@ -1135,16 +1157,25 @@ int fpm_detect_host(const double* H, const double* y, const uint8_t* tx_bits, in
       rc = launch_detect(k, b, threads, st[s]);
     }
     if (rc) break;
-    cudaMemcpyAsync(x + c0 * (int64_t)N * 2, dx, (size_t)n * N * 16, cudaMemcpyDeviceToHost, st[s]);
-    cudaMemcpyAsync(breakdown_at + c0, dbk, (size_t)n * 4, cudaMemcpyDeviceToHost, st[s]);
-    cudaMemcpyAsync(diverged_at + c0, ddv, (size_t)n * 4, cudaMemcpyDeviceToHost, st[s]);
-    if (rx_bits) cudaMemcpyAsync(rx_bits + c0 * bps * N, drx, (size_t)n * bps * N, cudaMemcpyDeviceToHost, st[s]);
+    if (direct) {
+      cudaMemcpyAsync(x + c0 * (int64_t)N * 2, dx, (size_t)n * N * 16, cudaMemcpyDeviceToHost, st[s]);
+      cudaMemcpyAsync(breakdown_at + c0, dbk, (size_t)n * 4, cudaMemcpyDeviceToHost, st[s]);
+      cudaMemcpyAsync(diverged_at + c0, ddv, (size_t)n * 4, cudaMemcpyDeviceToHost, st[s]);
+      if (rx_bits) cudaMemcpyAsync(rx_bits + c0 * bps * N, drx, (size_t)n * bps * N, cudaMemcpyDeviceToHost, st[s]);
+    }
   }
   int64_t hc[2 * FPM_NCOUNTERS] = {0};
   if (!rc) {
     for (int s = 0; s < 2; ++s)
       if (cudaStreamSynchronize(st[s]) != cudaSuccess) rc = FPM_ECUDA;
     if (!rc && cudaMemcpy(hc, dcnt, sizeof(hc), cudaMemcpyDeviceToHost) != cudaSuccess) rc = FPM_ECUDA;
+    if (!rc && obuf) {
+      if (cudaMemcpy(x, ox, oxB, cudaMemcpyDeviceToHost) != cudaSuccess ||
+          cudaMemcpy(breakdown_at, obk, ofB, cudaMemcpyDeviceToHost) != cudaSuccess ||
+          cudaMemcpy(diverged_at, odv, ofB, cudaMemcpyDeviceToHost) != cudaSuccess ||
+          (rx_bits && cudaMemcpy(rx_bits, orx, orB, cudaMemcpyDeviceToHost) != cudaSuccess))
+        rc = FPM_ECUDA;
+    }
     if (!rc)
       for (int i = 0; i < FPM_NCOUNTERS; ++i) counters[i] += hc[i] + hc[FPM_NCOUNTERS + i];
   }
@@ -1152,6 +1183,7 @@ int fpm_detect_host(const double* H, const double* y, const uint8_t* tx_bits, in
     if (buf[s]) cudaFreeAsync(buf[s], st[s]);
   }
   if (dcnt) cudaFreeAsync(dcnt, st[0]);
+  if (obuf) cudaFreeAsync(obuf, st[0]);
   for (int s = 0; s < 2; ++s) {
     cudaStreamSynchronize(st[s]);
     cudaStreamDestroy(st[s]);

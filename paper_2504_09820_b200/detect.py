@@ -149,6 +149,16 @@ def detect(det, H, y, sigma2: float, tx_bits=None, *, qam: int = 16, minv=None, 
     return DetectResult(x, brk, div, rx, cdict)
 
 
+_NP2TORCH = {np.dtype(np.complex128): "complex128", np.dtype(np.int32): "int32", np.dtype(np.uint8): "uint8"}
+
+
+def _pinned_empty(shape, dtype):
+    """NumPy view of a page-locked host tensor (keeps the tensor alive)."""
+    torch = _torch()
+    t = torch.empty(shape, dtype=getattr(torch, _NP2TORCH[np.dtype(dtype)]), pin_memory=True)
+    return t.numpy()
+
+
 def detect_host(det, H, y, sigma2: float, tx_bits=None, *, qam: int = 16, minv=None, want_bits=False,
                 chunk: int = 0) -> DetectResult:
     """Same as `detect` on HOST NumPy buffers through the library's own
@@ -165,10 +175,13 @@ def detect_host(det, H, y, sigma2: float, tx_bits=None, *, qam: int = 16, minv=N
     if det.algorithm == "fp_bj_cg" and minv is not None:
         mp = np.ascontiguousarray(pack_blocks(minv, N, L) if isinstance(minv, (list, tuple)) else minv,
                                   np.complex128)
-    x = np.empty((T, N), np.complex128)
-    brk = np.empty((T,), np.int32)
-    div = np.empty((T,), np.int32)
-    rx = np.empty((T, bps * N), np.uint8) if want_bits else None
+    # outputs in page-locked memory from torch's caching host allocator (cheap
+    # after the first call), so the library copies them back chunk by chunk
+    # under the H2D stream instead of once at the end into pageable memory
+    x = _pinned_empty((T, N), np.complex128)
+    brk = _pinned_empty((T,), np.int32)
+    div = _pinned_empty((T,), np.int32)
+    rx = _pinned_empty((T, bps * N), np.uint8) if want_bits else None
     cnt = np.zeros((_lib.NCOUNTERS,), np.int64)
     ps = _lib.precision_struct(det.precision())
     ptr = lambda a: None if a is None else a.ctypes.data  # noqa: E731
