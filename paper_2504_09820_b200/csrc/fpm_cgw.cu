@@ -1,0 +1,388 @@
+// Warp-per-realization (BJ-)CG: the run_batch boundary's fast path
+// (solvers.py:262-393, same arithmetic contract as cg_group in fpm_cg.cuh).
+//
+// One warp owns one realization for its whole life: it streams the
+// realization's complex128 A from HBM (coalesced 16-byte loads, many in
+// flight), rounds it ONCE to u_MV into its private shared-memory matrix
+// (formats.py:110-146 via cvt.rn / native ops, linalg.py:60-61), then runs
+// every sweep with warp-synchronous steps only (__syncwarp, no CTA barriers):
+//
+//   * lane l owns rows l, l+32, ... (RPL = N/32 rows): x, r, p, w and its
+//     block-Jacobi inverse rows live in registers;
+//   * a matvec row is one left-to-right chain in its lane (linalg.py:65-68);
+//   * a dot product u^H v: every lane forms the product terms of its rows,
+//     writes them to shared memory, and then EVERY lane runs the same
+//     left-to-right chain over all N terms (broadcast loads,
+//     linalg.py:94-95), so the scalar is warp-uniform with no broadcast step
+//     and the freeze / stall / breakdown decisions are warp-uniform branches;
+//   * alpha, beta: NumPy's Smith division in binary64 (solvers.py:256-259).
+//
+// Freeze semantics (solvers.py:342-357) become an early exit of the warp.
+// CTAs are one warp, so the block scheduler refills an SM as soon as any
+// realization finishes and loading (HBM latency) overlaps other warps' sweeps.
+// Work format fp64 and u_MV == u_IP native (fp64 / fp32 / fp16 / bf16), N in
+// {32, 64}, plain CG or block-Jacobi with N % L == 0; everything else (and the
+// run_batch histories) runs fpm_cg_kernel.
+#include "../../include/fpmimo_b200.h"
+#include "fpm_common.cuh"
+
+
+namespace fpm {
+
+#ifndef FPM_CGW_FUSE_RHO0
+#define FPM_CGW_FUSE_RHO0 0
+#endif
+#ifndef FPM_CGW_LOADS
+#define FPM_CGW_LOADS 16
+#endif
+
+// Per-realization shared-memory region.  A is unpadded (N*N entries at
+// u_MV) with an XOR swizzle on its 16-byte units, unit u of row i stored at
+// u ^ (i & 7): the 8 rows one LDS.128 quarter-warp phase reads fall on 8
+// distinct bank groups.  Scratch after A: the prepared p, the rho0 / rho1
+// term buffer (live ranges [p update, matvec] and [r update, rho1] are
+// disjoint, so one buffer), the phi terms and the binary64 r that z = M r
+// reads.  N = 64 fp16: 18,432 B (12 warps / SM).
+template <int K, int NC, int LB>
+struct CgwLayout {
+  typedef typename Ar<K>::C C;
+  typedef typename Ar<K>::P P;
+  static constexpr int EPU = 16 / (int)sizeof(C);  // entries per 16-byte unit
+  static constexpr int UPR = NC / EPU;             // units per row (>= 8)
+  static_assert(UPR % 8 == 0, "swizzle needs >= 8 units per row");
+  static constexpr int a_bytes = NC * NC * (int)sizeof(C);
+  static constexpr int off_pmv = a_bytes;
+  static constexpr int off_t0 = off_pmv + NC * (int)sizeof(P);
+  static constexpr int off_t1 = off_t0 + NC * (int)sizeof(C);
+  static constexpr int off_t2 = off_t0;
+  static constexpr int off_rv = (off_t1 + NC * (int)sizeof(C) + 15) / 16 * 16;
+  static constexpr int bytes = off_rv + (LB > 0 ? NC * 16 : 0);
+  // element offset of A(i, k)
+  static __device__ __forceinline__ int at(int i, int k) {
+    return (i * UPR + ((k / EPU) ^ (i & 7))) * EPU + k % EPU;
+  }
+};
+
+// w_i = sum_k A(i,k) p_k (matvec_fp, linalg.py:45-69) for the lane's RPL
+// rows -- one left-to-right chain per row -- and, in the same loop, the
+// optional left-to-right sum of the terms `ct` (the rho0 = r^H p chain of
+// as-written BJ, dot_fp's accumulation linalg.py:94-95): RPL + 1 independent
+// chains interleaved block by block.  The prepared p block is shared by the
+// rows.
+template <int K, int NC, int RPL, int LPR, bool CHAIN>
+__device__ __forceinline__ void mv_rows(const typename Ar<K>::C* At, const typename Ar<K>::P* pv,
+                                        const typename Ar<K>::C* ct, int lane, typename Ar<K>::C (&out)[RPL],
+                                        double2& csum, const FmtP& f, const FmtP& fi) {
+  typedef Ar<K> A;
+  typedef typename A::C C;
+  typedef typename A::P P;
+  constexpr int B = V16<C>::n;  // entries per 16-byte unit (= per block)
+  constexpr int NB = NC / B;
+  static_assert(B == 16 / (int)sizeof(C), "one 16-byte unit per block");
+  const C* row[RPL];
+  int sw[RPL];
+#pragma unroll
+  for (int j = 0; j < RPL; ++j) {
+    const int i = lane + LPR * j;
+    row[j] = At + i * NC;
+    sw[j] = i & 7;
+  }
+  C s[RPL], c;
+#pragma unroll
+  for (int kb = 0; kb < NB; ++kb) {
+    P p[B];
+    ld_blk<B>(pv + kb * B, p);
+    C cc[B];
+    if constexpr (CHAIN) ld_blk<B>(ct + kb * B, cc);
+#pragma unroll
+    for (int j = 0; j < RPL; ++j) {
+      C a[B];
+      ld_blk<B>(row[j] + (kb ^ sw[j]) * B, a);
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        const C t = A::mulp(a[u], p[u], f);
+        s[j] = (kb + u == 0) ? t : A::add(s[j], t, f);
+      }
+    }
+    if constexpr (CHAIN) {
+#pragma unroll
+      for (int u = 0; u < B; ++u) c = (kb + u == 0) ? cc[u] : A::add(c, cc[u], fi);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < RPL; ++j) out[j] = A::asmc(s[j]);
+  if constexpr (CHAIN) csum = A::wide(A::asmc(c));
+}
+
+// left-to-right sum of the NC terms in shared memory (dot_fp's
+// accumulation, linalg.py:94-95), run identically by every lane
+template <int K, int NC>
+__device__ __forceinline__ double2 wsum(const typename Ar<K>::C* t, const FmtP& f) {
+  typedef Ar<K> A;
+  typedef typename A::C C;
+  constexpr int B = V16<C>::n;
+  constexpr int NB = NC / B;
+  C s;
+#pragma unroll
+  for (int kb = 0; kb < NB; ++kb) {
+    C v[B];
+    ld_blk<B>(t + kb * B, v);
+#pragma unroll
+    for (int u = 0; u < B; ++u) s = (kb + u == 0) ? v[u] : A::add(s, v[u], f);
+  }
+  return A::wide(A::asmc(s));
+}
+
+// z_i = sum_l Minv(i, l) r_(block start + l) at u_W = fp64 (_BatchBlocks.apply,
+// solvers.py:222-225 -> matvec_fp at u_W), r from shared memory
+template <int LB>
+__device__ __forceinline__ double2 bj_z(const double2 (&m)[LB], const double2* rv, int s0) {
+  typedef Ar<FK_F64> W;
+  const FmtP f{};
+  double2 s = W::mul(m[0], rv[s0], f);
+#pragma unroll
+  for (int l = 1; l < LB; ++l) s = W::add(s, W::mul(m[l], rv[s0 + l], f), f);
+  return assemble(s.x, s.y);
+}
+
+// One warp (= one CTA) per realization; the block scheduler refills an SM as
+// soon as any realization finishes, so one warp's HBM load phase overlaps the
+// other resident warps' sweeps.  (A persistent grid that bulk-prefetches each
+// warp's next A into L2 -- cp.async.bulk.prefetch.L2 -- measured slower at c5
+// fp16, 48.3 M vs 51.7 M/s: one fewer resident warp per SM, and the
+// L2-sourced load phase still took ~11 K cycles.)
+template <int K, int NC, int LB>
+__global__ void __launch_bounds__(32) fpm_cgw_kernel(const CgArgs args) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  typedef Ar<K> A;
+  typedef typename A::C C;
+  typedef typename A::P P;
+  typedef CgwLayout<K, NC, LB> Lay;
+  constexpr int RPL = NC / 32;  // rows per lane
+  constexpr bool BJ = LB > 0;
+  constexpr int NN = NC * NC;
+  const int l = threadIdx.x;
+  const FmtP& fm = args.pr.mv;
+  const FmtP& fi = args.pr.ip;
+  const FmtP fw{};  // work = binary64 (identity rounding)
+  C* At = reinterpret_cast<C*>(smem);
+  P* pmv = reinterpret_cast<P*>(smem + Lay::off_pmv);
+  C* tb0 = reinterpret_cast<C*>(smem + Lay::off_t0);  // rho0 = r^H p terms (as_written BJ)
+  C* tb1 = reinterpret_cast<C*>(smem + Lay::off_t1);  // phi = p^H w terms
+  C* tb2 = reinterpret_cast<C*>(smem + Lay::off_t2);  // rho1 / carry terms (tb0's storage)
+  double2* rv = reinterpret_cast<double2*>(smem + Lay::off_rv);
+  const bool rho_fresh = BJ && !args.textbook;  // as_written: rho0 = r^H p every sweep
+  {
+    const long t = blockIdx.x;
+    long long* trc = args.trace ? args.trace + 4 * t : nullptr;  // diagnostic per-realization clocks
+    if (trc && l == 0) {
+      unsigned sm;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+      trc[0] = clock64();
+      trc[3] = sm;
+    }
+    // ---- A (complex128, row-major) -> At at u_MV, one rounding per entry ----
+    {
+      constexpr int U = FPM_CGW_LOADS;
+      const double2* Ag = args.A + t * NN;
+      __syncwarp();  // the previous realization's reads of At are done
+#pragma unroll 1
+      for (int q0 = l; q0 < NN; q0 += 32 * U) {
+        double2 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (q0 + 32 * u < NN) v[u] = __ldcs(Ag + q0 + 32 * u);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int q = q0 + 32 * u;
+          if (q < NN) At[Lay::at(q / NC, q % NC)] = A::rnd(v[u], fm);
+        }
+      }
+    }
+    double2 x[RPL], r[RPL], p[RPL];
+    C pm[RPL];
+    double2 m[RPL][LB > 0 ? LB : 1];
+#pragma unroll
+    for (int j = 0; j < RPL; ++j) {
+      const int i = l + 32 * j;
+      x[j] = make_double2(0.0, 0.0);
+      r[j] = args.b[t * NC + i];  // run_batch copies b (solvers.py:297-298)
+      if constexpr (BJ) {
+#pragma unroll
+        for (int k = 0; k < LB; ++k) m[j][k] = args.minv[(t * NC + i) * LB + k];  // row i of its block
+      }
+    }
+    if (trc) {
+      __syncwarp();
+      if (l == 0) trc[1] = clock64();
+    }
+    // ---- init (solvers.py:297-328): p = M r | r; carry = r^H r | r^H p ----
+    if constexpr (BJ) {
+#pragma unroll
+      for (int j = 0; j < RPL; ++j) rv[l + 32 * j] = r[j];
+      __syncwarp();
+    }
+#pragma unroll
+    for (int j = 0; j < RPL; ++j) {
+      const int i = l + 32 * j;
+      if constexpr (BJ) p[j] = bj_z<LB>(m[j], rv, i - i % LB);
+      else p[j] = r[j];
+    }
+#pragma unroll
+    for (int j = 0; j < RPL; ++j) {
+      const int i = l + 32 * j;
+      pm[j] = A::rnd(p[j], fm);
+      pmv[i] = A::prep(pm[j]);
+      const C ri = A::rnd(r[j], fi);
+      // as_written BJ: rho0 terms (tb0); otherwise the carry's terms (tb2, same storage)
+      tb0[i] = A::mulc(ri, (BJ && (args.textbook || rho_fresh)) ? pm[j] : ri, fi);
+    }
+    __syncwarp();
+    double2 carry = make_double2(0.0, 0.0);
+    if (!rho_fresh) carry = wsum<K, NC>(tb2, fi);
+    int brk = -1, dvg = -1;
+    long long* ph = (trc && t == 0 && l == 0) ? args.trace + 4 * args.T : nullptr;  // phase clocks, realization 0
+#define CGW_ST(k, dep)                                                             \
+  do {                                                                             \
+    if (ph) ph[(it - 1) * 10 + (k)] = clock64() + ((dep) == 1.2345e300 ? 1 : 0);   \
+  } while (0)
+
+#pragma unroll 1
+    for (int it = 1; it <= args.iters; ++it) {
+      // ---- w = A p (u_MV) ; rho0 (as_written BJ, same loop) ; phi = p^H w (u_IP) ----
+      C wc[RPL];
+      double2 rho0 = carry;
+#if FPM_CGW_FUSE_RHO0
+      if (rho_fresh) mv_rows<K, NC, RPL, 32, true>(At, pmv, tb0, l, wc, rho0, fm, fi);
+      else mv_rows<K, NC, RPL, 32, false>(At, pmv, tb0, l, wc, rho0, fm, fi);
+#else
+      mv_rows<K, NC, RPL, 32, false>(At, pmv, tb0, l, wc, rho0, fm, fi);
+      if (rho_fresh) rho0 = wsum<K, NC>(tb0, fi);
+#endif
+      CGW_ST(0, A::wide(wc[RPL - 1]).x);
+      CGW_ST(1, rho0.x);
+#pragma unroll
+      for (int j = 0; j < RPL; ++j) tb1[l + 32 * j] = A::mulc(pm[j], wc[j], fi);
+      __syncwarp();
+      const double2 phi = wsum<K, NC>(tb1, fi);
+      CGW_ST(2, phi.x);
+      // stall / breakdown freeze the realization (solvers.py:342-345)
+      const bool stall = (rho0.x == 0.0) && (rho0.y == 0.0);
+      if (!stall && phi.x <= 0.0) brk = it;
+      if (stall || phi.x <= 0.0) break;
+      const double2 al = wdiv<FK_F64>(rho0, phi, fw);
+      CGW_ST(3, al.x);
+      const double2 nal = make_double2(-al.x, -al.y);
+      // ---- x, r updates at u_W; non-finite -> diverged (solvers.py:346-354) ----
+      double2 xn[RPL], rn[RPL];
+      bool bad = false;
+#pragma unroll
+      for (int j = 0; j < RPL; ++j) {
+        xn[j] = axpy1<FK_F64>(al, p[j], x[j], fw);
+        rn[j] = axpy1<FK_F64>(nal, A::wide(wc[j]), r[j], fw);
+        bad |= !(finite2(xn[j]) && finite2(rn[j]));
+      }
+      if (__any_sync(0xffffffffu, bad)) {
+        dvg = it;
+        break;
+      }
+#pragma unroll
+      for (int j = 0; j < RPL; ++j) {
+        x[j] = xn[j];
+        r[j] = rn[j];
+      }
+      CGW_ST(4, r[RPL - 1].x);
+      // ---- z = M r ; rho1 = r^H z | r^H r ; beta = rho1 / rho0 ----
+      double2 z[RPL];
+      if constexpr (BJ) {
+#pragma unroll
+        for (int j = 0; j < RPL; ++j) rv[l + 32 * j] = r[j];
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < RPL; ++j) {
+          const int i = l + 32 * j;
+          z[j] = bj_z<LB>(m[j], rv, i - i % LB);
+        }
+      }
+      CGW_ST(5, BJ ? z[RPL - 1].x : r[0].x);
+      C ri[RPL];
+#pragma unroll
+      for (int j = 0; j < RPL; ++j) {
+        ri[j] = A::rnd(r[j], fi);
+        tb2[l + 32 * j] = A::mulc(ri[j], BJ ? A::rnd(z[j], fi) : ri[j], fi);
+      }
+      __syncwarp();
+      const double2 rho1 = wsum<K, NC>(tb2, fi);
+      CGW_ST(6, rho1.x);
+      const double2 be = wdiv<FK_F64>(rho1, rho0, fw);
+      CGW_ST(7, be.x);
+      carry = rho1;
+      __syncwarp();  // every lane's rho1 chain has read tb2 (= tb0's storage)
+      // ---- p = (z | r) + beta p ; prepared p and next rho0 terms ----
+#pragma unroll
+      for (int j = 0; j < RPL; ++j) {
+        const int i = l + 32 * j;
+        p[j] = axpy1<FK_F64>(be, p[j], BJ ? z[j] : r[j], fw);
+        pm[j] = A::rnd(p[j], fm);
+        pmv[i] = A::prep(pm[j]);
+        if (rho_fresh) tb0[i] = A::mulc(ri[j], pm[j], fi);
+      }
+      __syncwarp();
+      CGW_ST(8, p[RPL - 1].x);
+    }
+#undef CGW_ST
+    if (trc && l == 0) trc[2] = clock64();
+#pragma unroll
+    for (int j = 0; j < RPL; ++j) args.x[t * NC + l + 32 * j] = x[j];
+    if (l == 0) {
+      args.brk[t] = brk;
+      args.div[t] = dvg;
+    }
+  }
+}
+
+// One realization per warp.  (Two realizations per warp -- a half-warp each -- was measured slower at c5
+// fp16: 35.9 M vs 51.7 M/s, half the warps per SM and twice the serial load
+// phase per warp.)
+template <int K, int NC, int LB>
+static int launch_cgw_t(const CgArgs& a, cudaStream_t st) {
+  auto k = fpm_cgw_kernel<K, NC, LB>;
+  constexpr int smem = CgwLayout<K, NC, LB>::bytes;
+  if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return FPM_ECUDA;
+  k<<<(unsigned)a.T, 32, smem, st>>>(a);
+  count_launch();
+  return cudaGetLastError() == cudaSuccess ? FPM_OK : FPM_ECUDA;
+}
+
+template <int K, int NC>
+static int launch_cgw_n(const CgArgs& a, cudaStream_t st) {
+  if (!a.bj) return launch_cgw_t<K, NC, 0>(a, st);
+  switch (a.L) {
+    case 1: return launch_cgw_t<K, NC, 1>(a, st);
+    case 2: return launch_cgw_t<K, NC, 2>(a, st);
+    case 4: return launch_cgw_t<K, NC, 4>(a, st);
+    case 8: return NC == 32 ? launch_cgw_t<K, NC, 8>(a, st) : FPM_EUNSUPPORTED;
+    default: return FPM_EUNSUPPORTED;
+  }
+}
+
+template <int K>
+static int launch_cgw_k(const CgArgs& a, cudaStream_t st) {
+  if (a.N == 64) return launch_cgw_n<K, 64>(a, st);
+  if (a.N == 32) return launch_cgw_n<K, 32>(a, st);
+  return FPM_EUNSUPPORTED;
+}
+
+// FPM_EUNSUPPORTED: no warp-CG instance for this (kind, N, L); the caller
+// runs fpm_cg_kernel instead
+int launch_cgw(int mv_kind, const CgArgs& a, cudaStream_t st) {
+  switch (mv_kind) {
+    case FK_F64: return launch_cgw_k<FK_F64>(a, st);
+    case FK_F32: return launch_cgw_k<FK_F32>(a, st);
+    case FK_F16: return launch_cgw_k<FK_F16>(a, st);
+    case FK_BF16: return launch_cgw_k<FK_BF16>(a, st);
+    default: return FPM_EUNSUPPORTED;
+  }
+}
+
+}  // namespace fpm

@@ -93,6 +93,10 @@ FPM_DECLARE_KIND(gen_w)  // everything generic (W != fp64)
 
 void count_launch();
 
+// warp-per-realization CG (fpm_cgw.cu); FPM_EUNSUPPORTED when it has no
+// instance for the configuration
+int launch_cgw(int mv_kind, const CgArgs& a, cudaStream_t st);
+
 // FP32-Gram extension (fpm_gram32.cu)
 int launch_gram32(const double2* H, const double2* y, long T, int M, int N, double sigma2, double2* A, double2* b,
                   cudaStream_t st);

@@ -530,7 +530,7 @@ static void pick_spec(int N, int L, int bj, int& nb, int& lb) {
   if (bj && nb && (nb % L)) nb = 0;
 }
 
-static thread_local char g_last_kernel[96] = "";  // per calling thread (re-entrant)
+static thread_local char g_last_kernel[128] = "";  // per calling thread (re-entrant)
 
 static const char* kind_name(int k) {
   switch (k) {
@@ -582,6 +582,7 @@ static int launch_detect_ws(const Kinds& k, const DetectArgs& a, const WsLayout&
 
 static int launch_cg(const Kinds& k, const CgArgs& a, int smem, cudaStream_t st) {
   const int lb = (a.bj && a.N % a.L == 0 && !std::getenv("FPM_NO_SPEC")) ? a.L : 0;
+  note_kernel("fpm_cg_kernel", k, a.N == 64 ? 16 : 0, lb);
   if (k.w == FK_GEN) return launch_cg_gen_w(a, smem, 0, st);
   switch (k.mv) {
     case FK_F64: return launch_cg_f64(a, smem, lb, st);
@@ -803,6 +804,17 @@ int fpm_cg_ex(const double* A, const double* b, const double* Minv, int64_t T, i
   }
   int smem = 0;
   cudaStream_t st = (cudaStream_t)stream;
+  // warp-per-realization fast path (fpm_cgw.cu): fp64 work, native u_MV == u_IP,
+  // no histories; FPM_NO_CGW forces fpm_cg_kernel (A/B and parity tests)
+  if (!a.h.on && k.w == FK_F64 && k.mv == k.ip && k.mv != FK_GEN && !std::getenv("FPM_NO_CGW") &&
+      !std::getenv("FPM_FORCE_GENERIC") && (!bj || N % L == 0)) {
+    const int rw = launch_cgw(k.mv, a, st);
+    if (rw != FPM_EUNSUPPORTED) {
+      std::snprintf(g_last_kernel, sizeof(g_last_kernel), "fpm_cgw_kernel<mv=%s,N=%d,L=%d>", kind_name(k.mv), N,
+                    bj ? L : 0);
+      return rw;
+    }
+  }
   if (plan_cg(N, a.L, bj, k.mv, k.ip, a, smem)) return launch_cg(k, a, smem, st);
   // A at u_MV does not fit shared memory (16-byte terms at large N): keep it
   // in global memory, pre-rounded (fp64 is already on its own grid)
@@ -970,8 +982,6 @@ static int run_composed(const DetectArgs& a, int M, int N, int algorithm, int L,
   const long T = a.T;
   const bool bj = algorithm == FPM_ALG_FP_BJ_CG;
   const long chunk = std::min<long>(T, 2048);
-  std::snprintf(g_last_kernel, sizeof(g_last_kernel), "composed: %s+fpm_bj_kernel+fpm_cg_kernel",
-                a.gram32 ? "fpm_gram32_kernel" : "fpm_gram_kernel");
   double2 *A = nullptr, *b = nullptr, *mv = nullptr;
   int rc = FPM_OK;
   if (cudaMallocAsync(&A, (size_t)chunk * N * N * 16, st) != cudaSuccess ||
@@ -1001,6 +1011,12 @@ static int run_composed(const DetectArgs& a, int M, int N, int algorithm, int L,
   if (A) cudaFreeAsync(A, st);
   if (b) cudaFreeAsync(b, st);
   if (mv) cudaFreeAsync(mv, st);
+  {
+    char cg[96];
+    std::snprintf(cg, sizeof(cg), "%s", g_last_kernel);  // the CG kernel fpm_cg_ex picked
+    std::snprintf(g_last_kernel, sizeof(g_last_kernel), "composed: %s+fpm_bj_kernel+%.48s",
+                  a.gram32 ? "fpm_gram32_kernel" : "fpm_gram_kernel", cg);
+  }
   if (rc) return rc;
   const long TN = T * (long)N;
   fpm_slice_kernel<<<(unsigned)std::min((TN + 255) / 256, 148L * 8), 256, 0, st>>>(a.x, a.tx, TN, a.rx, a.counters,

@@ -1,0 +1,121 @@
+"""Warp-per-realization CG (csrc/fpm_cgw.cu) through the C ABI `fpm_cg`:
+bit-exact against the oracle's run_batch restatement (solvers.py:262-393)
+for every native matvec/inner kind, N in {32, 64}, plain CG and block-Jacobi
+L in {1, 2, 4, 8}, both rho updates, the freeze flags (stall / breakdown /
+divergence), and bit-identical to the CTA-lockstep fpm_cg_kernel at batch
+sizes the oracle would take minutes on."""
+
+import ctypes
+
+import numpy as np
+import pytest
+
+from conftest import bits_equal
+
+pytestmark = pytest.mark.gpu
+
+KINDS = {"fp64": (53, 11), "fp32": (24, 8), "fp16": (11, 5), "bfloat16": (8, 8)}
+
+
+def _cg_capi(A, b, minv, L, iters, fmt, rho_update, env=None, monkeypatch=None):
+    """fpm_cg (no histories) on device copies; returns x, brk, div, kernel."""
+    import torch
+    from paper_2504_09820_b200 import _lib
+    from paper_2504_09820_b200.solvers import _stream
+    lib = _lib.load()
+    dev = torch.device("cuda", 0)
+    T, N = b.shape
+    Ad = torch.from_numpy(np.ascontiguousarray(A, np.complex128)).to(dev)
+    bd = torch.from_numpy(np.ascontiguousarray(b, np.complex128)).to(dev)
+    md = None if minv is None else torch.from_numpy(np.ascontiguousarray(minv, np.complex128)).to(dev)
+    x = torch.empty((T, N), dtype=torch.complex128, device=dev)
+    brk = torch.empty(T, dtype=torch.int32, device=dev)
+    div = torch.empty(T, dtype=torch.int32, device=dev)
+    sig, ex = KINDS[fmt]
+    ps = _lib.Precision(_lib.Format(53, 11, 1), _lib.Format(sig, ex, 1), _lib.Format(sig, ex, 1))
+    rc = lib.fpm_cg(Ad.data_ptr(), bd.data_ptr(), None if md is None else md.data_ptr(), T, N, L if md is not None else 1,
+                    iters, ctypes.byref(ps), 0 if rho_update == "as_written" else 1, x.data_ptr(), brk.data_ptr(),
+                    div.data_ptr(), _stream())
+    _lib.check(rc, "fpm_cg")
+    torch.cuda.synchronize()
+    kern = lib.fpm_last_kernel().decode()
+    return x.cpu().numpy(), brk.cpu().numpy(), div.cpu().numpy(), kern
+
+
+def _pack(mats, N, L):
+    from paper_2504_09820_b200.solvers import pack_blocks
+    return pack_blocks(mats, N, L)
+
+
+def _system(O, M, N, T, seed, snr=10.0):
+    H, y, _, s2 = O.simulate(M, N, 0.5, snr, range(T), seed)
+    return O.gram_mf(H, y, s2)
+
+
+@pytest.mark.parametrize("fmt", list(KINDS))
+@pytest.mark.parametrize("N", [32, 64])
+def test_cgw_matches_oracle(oracle, fmt, N):
+    O = oracle
+    T = 7
+    A, b = _system(O, 2 * N, N, T, 31 + N)
+    of = O.REGISTRY[fmt]
+    for L in (0, 1, 2, 4, 8):
+        mats = O.bj_inverses(A, L) if L else None
+        for rv in ("as_written", "textbook"):
+            if L == 0 and rv == "textbook":
+                continue
+            ref = O.cg_batch(A, b, 6, O.FP64, of, of, mats, rho_update=rv)
+            x, brk, div, kern = _cg_capi(A, b, _pack(mats, N, L) if L else None, L, 6, fmt, rv)
+            if not (L == 8 and N == 64):
+                assert kern.startswith("fpm_cgw_kernel"), kern
+            assert bits_equal(x, ref.x), (fmt, N, L, rv)
+            np.testing.assert_array_equal(brk, ref.breakdown_at)
+            np.testing.assert_array_equal(div, ref.diverged_at)
+
+
+@pytest.mark.parametrize("fmt", ["fp64", "fp16", "bfloat16"])
+def test_cgw_freeze_flags(oracle, fmt):
+    """Stall (b = 0), breakdown (negative definite A), divergence (fp16
+    overflow of the matvec / a NaN entry) and healthy lanes side by side."""
+    O = oracle
+    N, T = 32, 6
+    A0, b = _system(O, 64, N, T, 5)
+    A = A0.copy()
+    b = b.copy()
+    b[1] = 0.0                                   # stall at sweep 1
+    A[2] = -A[2]                                 # Re(phi) < 0: breakdown at sweep 1
+    A[3] *= 1e6                                  # fp16 / bf16 matvec overflow
+    b[3] *= 1e6
+    A[4, 3, 5] = np.nan                          # non-finite update
+    for L in (0, 4):
+        mats = O.bj_inverses(A0, L) if L else None  # preconditioner of the clean systems
+        of = O.REGISTRY[fmt]
+        ref = O.cg_batch(A, b, 6, O.FP64, of, of, mats)
+        x, brk, div, kern = _cg_capi(A, b, _pack(mats, N, L) if L else None, L, 6, fmt, "as_written")
+        assert kern.startswith("fpm_cgw_kernel"), kern
+        assert bits_equal(x, ref.x), (fmt, L)
+        np.testing.assert_array_equal(brk, ref.breakdown_at)
+        np.testing.assert_array_equal(div, ref.diverged_at)
+
+
+@pytest.mark.parametrize("fmt,L", [("fp16", 4), ("bfloat16", 0), ("fp64", 4), ("fp32", 2)])
+def test_cgw_equals_lockstep_kernel_at_scale(oracle, monkeypatch, fmt, L):
+    """The warp kernel and the CTA-lockstep kernel (FPM_NO_CGW) give the same
+    bits on a 4096-realization c5-shaped batch."""
+    O = oracle
+    N, T = 64, 4096
+    rng = np.random.default_rng(7)
+    Hh = (rng.standard_normal((T, 128, N)) + 1j * rng.standard_normal((T, 128, N))) / np.sqrt(256)
+    s = (rng.integers(0, 2, (T, N)) * 2 - 1 + 1j * (rng.integers(0, 2, (T, N)) * 2 - 1)) / np.sqrt(2)
+    y = np.einsum("tmn,tn->tm", Hh, s) + 0.05 * (rng.standard_normal((T, 128)) + 1j * rng.standard_normal((T, 128)))
+    from paper_2504_09820_b200.detect import gram_mf
+    from paper_2504_09820_b200.solvers import build_blocks_batch
+    A, b = gram_mf(Hh, y, 0.005)
+    minv = build_blocks_batch(A, L).packed if L else None
+    x1, b1, d1, k1 = _cg_capi(A, b, minv, L, 8, fmt, "as_written")
+    monkeypatch.setenv("FPM_NO_CGW", "1")
+    x2, b2, d2, k2 = _cg_capi(A, b, minv, L, 8, fmt, "as_written")
+    assert k1.startswith("fpm_cgw_kernel") and not k2.startswith("fpm_cgw_kernel"), (k1, k2)
+    assert bits_equal(x1, x2)
+    np.testing.assert_array_equal(b1, b2)
+    np.testing.assert_array_equal(d1, d2)

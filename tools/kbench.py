@@ -50,6 +50,7 @@ def main():
     ap.add_argument("--trace", action="store_true")
     ap.add_argument("--wstrace", action="store_true")
     ap.add_argument("--cgtrace", action="store_true")
+    ap.add_argument("--cgwtrace", action="store_true")
     a = ap.parse_args()
     bench.M, bench.N, bench.L = a.M, a.N, a.L
     M, N, L, T = a.M, a.N, a.L, a.T
@@ -121,6 +122,37 @@ def main():
         o["B_detail_it2"] = [c[78] - c[1 + 6], c[79] - c[78], c[80] - c[79], c[1 + 6 + 1] - c[80]]
         o["C_detail_it2"] = [c[71] - c[70], c[72] - c[71], c[73] - c[72], c[74] - c[73], c[1 + 6 + 2] - c[74]]
         out["cg_trace"] = o
+    if a.cgwtrace:  # warp CG: per-realization load / compute clocks and SM residency
+        gram()
+        bj()
+        tr = torch.zeros(T * 4 + 256, dtype=torch.int64, device=dev)
+        lib.fpm_debug_set_trace(tr.data_ptr())
+        cg()
+        torch.cuda.synchronize()
+        lib.fpm_debug_set_trace(None)
+        ph = tr[T * 4:].cpu().tolist()
+        t4 = tr[:T * 4].view(T, 4).cpu()
+        load = (t4[:, 1] - t4[:, 0]).double()
+        comp = (t4[:, 2] - t4[:, 1]).double()
+        res = []
+        for sm in range(148):
+            sel = t4[:, 3] == sm
+            if sel.any():
+                span = (t4[sel, 2].max() - t4[sel, 0].min()).item()
+                res.append(((t4[sel, 2] - t4[sel, 0]).double().sum() / span).item())
+        out["cgw_trace"] = {"load_cyc": load.mean().item(), "compute_cyc": comp.mean().item(),
+                            "resident_per_sm": sum(res) / len(res), "compute_per_sweep": comp.mean().item() / bench.ITERS}
+        names = ["matvec", "rho0", "phi", "alpha", "x,r", "z", "rho1", "beta", "p"]
+        sweeps = []
+        for it in range(1, bench.ITERS):  # sweep it+1 relative to the end of sweep it
+            prev = ph[(it - 1) * 10 + 8]
+            row = {}
+            for k, nm in enumerate(names):
+                v = ph[it * 10 + k]
+                row[nm] = v - prev
+                prev = v
+            sweeps.append(row)
+        out["cgw_phases_r0"] = sweeps[:3]
     if a.wstrace:
         tr = torch.zeros(160, dtype=torch.int64, device=dev)
         lib.fpm_debug_set_trace(tr.data_ptr())
