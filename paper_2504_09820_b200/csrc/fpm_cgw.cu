@@ -25,12 +25,18 @@
 // run_batch histories) runs fpm_cg_kernel.
 #include "../../include/fpmimo_b200.h"
 #include "fpm_common.cuh"
+#include "fpm_ptx.cuh"
+
+#include <cstdlib>
 
 
 namespace fpm {
 
 #ifndef FPM_CGW_FUSE_RHO0
 #define FPM_CGW_FUSE_RHO0 0
+#endif
+#ifndef FPM_CGW_PREFETCH
+#define FPM_CGW_PREFETCH 1
 #endif
 #ifndef FPM_CGW_LOADS
 #define FPM_CGW_LOADS 16
@@ -145,35 +151,164 @@ __device__ __forceinline__ double2 bj_z(const double2 (&m)[LB], const double2* r
   return assemble(s.x, s.y);
 }
 
+// ---- tensor memory (TMEM) as the matrix store -----------------------------
+// 32x32b shapes: lane l of the warp reads / writes TMEM lane (32 * (warp % 4)
+// + l), consecutive 32-bit columns.  tcgen05.ld / st complete asynchronously;
+// tm_wait_ld / tm_wait_st wait for all of this thread's outstanding ones, and
+// tm_launder makes the loaded registers' consumers depend on the wait (the
+// compiler sees the ld's outputs as defined at the ld itself).
+__device__ __forceinline__ void tm_ld8(uint32_t (&v)[8], uint32_t taddr) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+               : "r"(taddr));
+}
+__device__ __forceinline__ void tm_st16(uint32_t taddr, const uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
+__device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tm_launder(uint32_t (&v)[8]) {
+  asm volatile("" : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]), "+r"(v[7]));
+}
+
+// w = A p for rows l and l+32 with A in TMEM (row l: columns [0, 64), row
+// l+32: [64, 128), one 32-bit u_MV complex per column): 8-column blocks, the
+// next block's tcgen05.ld in flight while this block's products and sums run.
+template <int K>
+__device__ __forceinline__ void mv_rows_tm(uint32_t ta, const typename Ar<K>::P* pv, typename Ar<K>::C (&out)[2],
+                                           const FmtP& f) {
+  typedef Ar<K> A;
+  typedef typename A::C C;
+  typedef typename A::P P;
+  static_assert(sizeof(C) == 4, "TMEM matvec: 32-bit complex entries");
+  uint32_t ra[2][2][8];
+  tm_ld8(ra[0][0], ta);
+  tm_ld8(ra[0][1], ta + 64);
+  tm_wait_ld();
+  tm_launder(ra[0][0]);
+  tm_launder(ra[0][1]);
+  C s[2];
+#pragma unroll
+  for (int kb = 0; kb < 8; ++kb) {
+    const int cur = kb & 1;
+    if (kb < 7) {
+      tm_ld8(ra[cur ^ 1][0], ta + 8 * (kb + 1));
+      tm_ld8(ra[cur ^ 1][1], ta + 64 + 8 * (kb + 1));
+    }
+    P p[8];
+    ld_blk<8>(pv + 8 * kb, p);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        uint32_t w = ra[cur][j][u];
+        const C t = A::mulp(*reinterpret_cast<C*>(&w), p[u], f);
+        s[j] = (kb + u == 0) ? t : A::add(s[j], t, f);
+      }
+    }
+    if (kb < 7) {
+      tm_wait_ld();
+      tm_launder(ra[cur ^ 1][0]);
+      tm_launder(ra[cur ^ 1][1]);
+    }
+  }
+  out[0] = A::asmc(s[0]);
+  out[1] = A::asmc(s[1]);
+}
+
+// z_i from block-inverse rows in shared memory (TMEM kernel; LB = 4): row i's
+// entry k at unit (k + (i >> 1)) % 4 of the row, so 8 lanes reading 8
+// consecutive rows' entry k hit 8 distinct bank groups
+template <int LB>
+__device__ __forceinline__ double2 bj_z_s(const double2* ms, int i, const double2* rv, int s0) {
+  static_assert(LB == 4, "shared-memory block rows: L = 4");
+  typedef Ar<FK_F64> W;
+  const FmtP f{};
+  const double2* mr = ms + i * LB;
+  const int o = i >> 1;
+  double2 s = W::mul(mr[o & 3], rv[s0], f);
+#pragma unroll
+  for (int k = 1; k < LB; ++k) s = W::add(s, W::mul(mr[(k + o) & 3], rv[s0 + k], f), f);
+  return assemble(s.x, s.y);
+}
+
 // One warp (= one CTA) per realization; the block scheduler refills an SM as
 // soon as any realization finishes, so one warp's HBM load phase overlaps the
 // other resident warps' sweeps.  (A persistent grid that bulk-prefetches each
 // warp's next A into L2 -- cp.async.bulk.prefetch.L2 -- measured slower at c5
 // fp16, 48.3 M vs 51.7 M/s: one fewer resident warp per SM, and the
 // L2-sourced load phase still took ~11 K cycles.)
-template <int K, int NC, int LB>
-__global__ void __launch_bounds__(32) fpm_cgw_kernel(const CgArgs args) {
+// TM = false: one warp per CTA, A at u_MV in shared memory (CgwLayout).
+// TM = true (N = 64, 32-bit u_MV entries, L in {0, 4}; opt-in, see
+// launch_cgw_t): four warps per CTA,
+// each warp's A in its TMEM lane quarter (128 columns per CTA), the
+// block-inverse rows in shared memory: the shared-memory footprint drops from
+// 18 KB to 6 KB per realization, so registers, not shared memory, bound the
+// resident warps (16 per SM at <= 128 registers).
+template <int K, int NC, int LB, bool TM>
+struct CgwTmLayout {
+  typedef typename Ar<K>::C C;
+  typedef typename Ar<K>::P P;
+  static constexpr int off_pmv = 0;
+  static constexpr int off_t0 = off_pmv + NC * (int)sizeof(P);
+  static constexpr int off_t1 = off_t0 + NC * (int)sizeof(C);
+  static constexpr int off_t2 = off_t0;
+  static constexpr int off_rv = (off_t1 + NC * (int)sizeof(C) + 15) / 16 * 16;
+  static constexpr int off_ms = off_rv + (LB > 0 ? NC * 16 : 0);
+  static constexpr int bytes_ = off_ms + NC * LB * 16;
+  static constexpr int stage = NC * 16 * 4;  // 16-column staging tile (aliases rv / ms)
+  static constexpr int bytes = off_rv + stage > bytes_ ? off_rv + stage : bytes_;
+  static constexpr int head = 128;  // TMEM address slot
+  static constexpr int cta_bytes = head + 4 * bytes;
+};
+
+template <int K, int NC, int LB, bool TM>
+__global__ void __launch_bounds__(TM ? 128 : 32, TM ? 4 : 1) fpm_cgw_kernel(const CgArgs args) {
   extern __shared__ __align__(128) unsigned char smem[];
   typedef Ar<K> A;
   typedef typename A::C C;
   typedef typename A::P P;
   typedef CgwLayout<K, NC, LB> Lay;
+  typedef CgwTmLayout<K, NC, LB, TM> TLay;
   constexpr int RPL = NC / 32;  // rows per lane
   constexpr bool BJ = LB > 0;
   constexpr int NN = NC * NC;
-  const int l = threadIdx.x;
+  static_assert(!TM || (NC == 64 && sizeof(C) == 4 && (LB == 0 || LB == 4)), "TMEM variant: N = 64, 32-bit u_MV");
+  const int l = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const long t = TM ? (long)blockIdx.x * 4 + wid : (long)blockIdx.x;
+  const bool valid = t < args.T;
   const FmtP& fm = args.pr.mv;
   const FmtP& fi = args.pr.ip;
   const FmtP fw{};  // work = binary64 (identity rounding)
+  unsigned char* base = TM ? smem + TLay::head + wid * TLay::bytes : smem;
   C* At = reinterpret_cast<C*>(smem);
-  P* pmv = reinterpret_cast<P*>(smem + Lay::off_pmv);
-  C* tb0 = reinterpret_cast<C*>(smem + Lay::off_t0);  // rho0 = r^H p terms (as_written BJ)
-  C* tb1 = reinterpret_cast<C*>(smem + Lay::off_t1);  // phi = p^H w terms
-  C* tb2 = reinterpret_cast<C*>(smem + Lay::off_t2);  // rho1 / carry terms (tb0's storage)
-  double2* rv = reinterpret_cast<double2*>(smem + Lay::off_rv);
+  P* pmv = reinterpret_cast<P*>(base + (TM ? TLay::off_pmv : Lay::off_pmv));
+  C* tb0 = reinterpret_cast<C*>(base + (TM ? TLay::off_t0 : Lay::off_t0));  // rho0 = r^H p terms (as_written BJ)
+  C* tb1 = reinterpret_cast<C*>(base + (TM ? TLay::off_t1 : Lay::off_t1));  // phi = p^H w terms
+  C* tb2 = reinterpret_cast<C*>(base + (TM ? TLay::off_t2 : Lay::off_t2));  // rho1 / carry terms (tb0's storage)
+  double2* rv = reinterpret_cast<double2*>(base + (TM ? TLay::off_rv : Lay::off_rv));
+  double2* ms = reinterpret_cast<double2*>(base + TLay::off_ms);  // TM: block-inverse rows
   const bool rho_fresh = BJ && !args.textbook;  // as_written: rho0 = r^H p every sweep
-  {
-    const long t = blockIdx.x;
+  uint32_t ta = 0;  // TM: this warp's TMEM base (lane quarter wid, 128 columns)
+  if constexpr (TM) {
+    uint32_t* slot = reinterpret_cast<uint32_t*>(smem);
+    if (wid == 0) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(smem_u32(slot))
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    ta = *slot + ((uint32_t)(32 * wid) << 16);
+  }
+
+  if (valid) {
     long long* trc = args.trace ? args.trace + 4 * t : nullptr;  // diagnostic per-realization clocks
     if (trc && l == 0) {
       unsigned sm;
@@ -181,11 +316,61 @@ __global__ void __launch_bounds__(32) fpm_cgw_kernel(const CgArgs args) {
       trc[0] = clock64();
       trc[3] = sm;
     }
-    // ---- A (complex128, row-major) -> At at u_MV, one rounding per entry ----
-    {
+    // ---- A (complex128, row-major) -> u_MV, one rounding per entry ----
+    // One bulk L2 prefetch of the whole matrix first: HBM sees all of this
+    // realization's bytes requested at once (memory-level parallelism without
+    // registers), the loads below then mostly wait on L2, not on HBM.
+#if FPM_CGW_PREFETCH
+    if (l == 0)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(args.A + t * NN), "r"(NN * 16) : "memory");
+#endif
+    if constexpr (TM) {
+      // 16-column chunks of all 64 rows: coalesced loads (two 256-byte row
+      // segments per warp load), rounded into a shared-memory staging tile
+      // (16-byte unit v of row i at v ^ ((i >> 1) & 3): conflict-free both
+      // ways), then lane l moves rows l and l+32 into its TMEM lane.  The
+      // staging tile aliases rv / ms, which are first written after this.
+      constexpr int U = FPM_CGW_LOADS;
+      uint32_t* stg = reinterpret_cast<uint32_t*>(base + TLay::off_rv);
+      const double2* Ag = args.A + t * NN;
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+#pragma unroll 1
+        for (int q0 = l; q0 < 1024; q0 += 32 * U) {
+          double2 v[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int q = q0 + 32 * u;
+            v[u] = __ldcs(Ag + (q >> 4) * NC + 16 * c + (q & 15));
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int q = q0 + 32 * u, i = q >> 4, k = q & 15;
+            const C h = A::rnd(v[u], fm);
+            stg[i * 16 + ((((k >> 2) ^ (i >> 1)) & 3) << 2) + (k & 3)] = *reinterpret_cast<const uint32_t*>(&h);
+          }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int i = l + 32 * j;
+          uint32_t u[16];
+#pragma unroll
+          for (int w4 = 0; w4 < 4; ++w4) {
+            const uint4 q = *reinterpret_cast<const uint4*>(stg + i * 16 + (((w4 ^ (i >> 1)) & 3) << 2));
+            u[4 * w4] = q.x;
+            u[4 * w4 + 1] = q.y;
+            u[4 * w4 + 2] = q.z;
+            u[4 * w4 + 3] = q.w;
+          }
+          tm_st16(ta + 64 * j + 16 * c, u);
+        }
+        __syncwarp();
+      }
+      tm_wait_st();
+    } else {
       constexpr int U = FPM_CGW_LOADS;
       const double2* Ag = args.A + t * NN;
-      __syncwarp();  // the previous realization's reads of At are done
 #pragma unroll 1
       for (int q0 = l; q0 < NN; q0 += 32 * U) {
         double2 v[U];
@@ -201,17 +386,27 @@ __global__ void __launch_bounds__(32) fpm_cgw_kernel(const CgArgs args) {
     }
     double2 x[RPL], r[RPL], p[RPL];
     C pm[RPL];
-    double2 m[RPL][LB > 0 ? LB : 1];
+    double2 m[RPL][(LB > 0 && !TM) ? LB : 1];
 #pragma unroll
     for (int j = 0; j < RPL; ++j) {
       const int i = l + 32 * j;
       x[j] = make_double2(0.0, 0.0);
       r[j] = args.b[t * NC + i];  // run_batch copies b (solvers.py:297-298)
-      if constexpr (BJ) {
+      if constexpr (BJ && !TM) {
 #pragma unroll
         for (int k = 0; k < LB; ++k) m[j][k] = args.minv[(t * NC + i) * LB + k];  // row i of its block
       }
+      if constexpr (BJ && TM) {
+#pragma unroll
+        for (int k = 0; k < LB; ++k) ms[i * LB + ((k + (i >> 1)) & 3)] = args.minv[(t * NC + i) * LB + k];
+      }
     }
+    auto zrow = [&](int j) -> double2 {
+      const int i = l + 32 * j;
+      if constexpr (TM && BJ) return bj_z_s<LB>(ms, i, rv, i - i % LB);
+      else if constexpr (!TM) return bj_z<(LB > 0 ? LB : 1)>(m[j], rv, i - i % (LB > 0 ? LB : 1));
+      else return rv[i];  // unused (plain CG)
+    };
     if (trc) {
       __syncwarp();
       if (l == 0) trc[1] = clock64();
@@ -224,8 +419,7 @@ __global__ void __launch_bounds__(32) fpm_cgw_kernel(const CgArgs args) {
     }
 #pragma unroll
     for (int j = 0; j < RPL; ++j) {
-      const int i = l + 32 * j;
-      if constexpr (BJ) p[j] = bj_z<LB>(m[j], rv, i - i % LB);
+      if constexpr (BJ) p[j] = zrow(j);
       else p[j] = r[j];
     }
 #pragma unroll
@@ -249,16 +443,21 @@ __global__ void __launch_bounds__(32) fpm_cgw_kernel(const CgArgs args) {
 
 #pragma unroll 1
     for (int it = 1; it <= args.iters; ++it) {
-      // ---- w = A p (u_MV) ; rho0 (as_written BJ, same loop) ; phi = p^H w (u_IP) ----
+      // ---- w = A p (u_MV) ; rho0 (as_written BJ) ; phi = p^H w (u_IP) ----
       C wc[RPL];
       double2 rho0 = carry;
+      if constexpr (TM) {
+        mv_rows_tm<K>(ta, pmv, wc, fm);
+      } else {
 #if FPM_CGW_FUSE_RHO0
-      if (rho_fresh) mv_rows<K, NC, RPL, 32, true>(At, pmv, tb0, l, wc, rho0, fm, fi);
-      else mv_rows<K, NC, RPL, 32, false>(At, pmv, tb0, l, wc, rho0, fm, fi);
-#else
-      mv_rows<K, NC, RPL, 32, false>(At, pmv, tb0, l, wc, rho0, fm, fi);
-      if (rho_fresh) rho0 = wsum<K, NC>(tb0, fi);
+        if (rho_fresh) mv_rows<K, NC, RPL, 32, true>(At, pmv, tb0, l, wc, rho0, fm, fi);
+        else
 #endif
+          mv_rows<K, NC, RPL, 32, false>(At, pmv, tb0, l, wc, rho0, fm, fi);
+      }
+      if (!FPM_CGW_FUSE_RHO0 || TM) {
+        if (rho_fresh) rho0 = wsum<K, NC>(tb0, fi);
+      }
       CGW_ST(0, A::wide(wc[RPL - 1]).x);
       CGW_ST(1, rho0.x);
 #pragma unroll
@@ -299,10 +498,7 @@ __global__ void __launch_bounds__(32) fpm_cgw_kernel(const CgArgs args) {
         for (int j = 0; j < RPL; ++j) rv[l + 32 * j] = r[j];
         __syncwarp();
 #pragma unroll
-        for (int j = 0; j < RPL; ++j) {
-          const int i = l + 32 * j;
-          z[j] = bj_z<LB>(m[j], rv, i - i % LB);
-        }
+        for (int j = 0; j < RPL; ++j) z[j] = zrow(j);
       }
       CGW_ST(5, BJ ? z[RPL - 1].x : r[0].x);
       C ri[RPL];
@@ -339,6 +535,14 @@ __global__ void __launch_bounds__(32) fpm_cgw_kernel(const CgArgs args) {
       args.div[t] = dvg;
     }
   }
+  if constexpr (TM) {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (wid == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(ta) : "memory");
+    }
+  }
 }
 
 // One realization per warp.  (Two realizations per warp -- a half-warp each -- was measured slower at c5
@@ -346,7 +550,24 @@ __global__ void __launch_bounds__(32) fpm_cgw_kernel(const CgArgs args) {
 // phase per warp.)
 template <int K, int NC, int LB>
 static int launch_cgw_t(const CgArgs& a, cudaStream_t st) {
-  auto k = fpm_cgw_kernel<K, NC, LB>;
+  constexpr bool tm_ok = NC == 64 && sizeof(typename Ar<K>::C) == 4 && (LB == 0 || LB == 4);
+  if constexpr (tm_ok) {
+    // opt-in (FPM_CGW_TMEM=1): measured slower than the shared-memory kernel
+    // at c5 fp16 (50.4 M vs 55.5 M det/s): 15 resident warps instead of 12,
+    // but the transposing load phase is twice as long and the sweeps slow
+    // down under the extra contention
+    const char* e = std::getenv("FPM_CGW_TMEM");
+    if (e && e[0] == '1') {
+      auto k = fpm_cgw_kernel<K, NC, LB, true>;
+      constexpr int smem = CgwTmLayout<K, NC, LB, true>::cta_bytes;
+      if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+        return FPM_ECUDA;
+      k<<<(unsigned)((a.T + 3) / 4), 128, smem, st>>>(a);
+      count_launch();
+      return cudaGetLastError() == cudaSuccess ? FPM_OK : FPM_ECUDA;
+    }
+  }
+  auto k = fpm_cgw_kernel<K, NC, LB, false>;
   constexpr int smem = CgwLayout<K, NC, LB>::bytes;
   if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return FPM_ECUDA;
   k<<<(unsigned)a.T, 32, smem, st>>>(a);

@@ -119,3 +119,22 @@ def test_cgw_equals_lockstep_kernel_at_scale(oracle, monkeypatch, fmt, L):
     assert bits_equal(x1, x2)
     np.testing.assert_array_equal(b1, b2)
     np.testing.assert_array_equal(d1, d2)
+
+
+@pytest.mark.parametrize("fmt", ["fp16", "bfloat16"])
+def test_cgw_tmem_variant_matches_oracle(oracle, monkeypatch, fmt):
+    """The opt-in TMEM variant (FPM_CGW_TMEM=1: A in tensor memory, four
+    warps per CTA) gives the oracle's bits, including a partial last CTA."""
+    O = oracle
+    T, N = 7, 64
+    A, b = _system(O, 128, N, T, 77)
+    of = O.REGISTRY[fmt]
+    monkeypatch.setenv("FPM_CGW_TMEM", "1")
+    for L in (0, 4):
+        mats = O.bj_inverses(A, L) if L else None
+        for rv in (("as_written", "textbook") if L else ("as_written",)):
+            ref = O.cg_batch(A, b, 6, O.FP64, of, of, mats, rho_update=rv)
+            x, brk, div, kern = _cg_capi(A, b, _pack(mats, N, L) if L else None, L, 6, fmt, rv)
+            assert bits_equal(x, ref.x), (fmt, L, rv)
+            np.testing.assert_array_equal(brk, ref.breakdown_at)
+            np.testing.assert_array_equal(div, ref.diverged_at)
