@@ -310,6 +310,10 @@ def run_ours(args):
         import cfgbench
         other = {name: cfgbench.measure(name, 16384, lib, peak_dp, dev) for name in cfgbench.CFGS}
 
+    cgk = None
+    if rank == 0 and world == 1 and not args.no_configs:
+        cgk = cg_kernel_line(lib, dev, ps, args.precision)
+
     if rank == 0:
         clocks = clk.summary()
         line = {
@@ -336,15 +340,75 @@ def run_ours(args):
                          "work_per_unit": f"F_gram = 4MN(N+1)+8MN = {f_gram()} non-fused fp64 ops/detection",
                          "peak_source": "fpm_probe_fp64 (measured non-fused DMUL/DADD rate, this GPU)",
                          "hbm": {"achieved_gbs": round(io_bytes() * min(pool, T) / (kernel_ms / 1e3) / 1e9, 1),
-                                 "peak_gbs": 6554.9, "bytes_per_unit": io_bytes()}},
+                                 "peak_gbs": hbm_peak_gbs()[0], "bytes_per_unit": io_bytes()}},
             "clocks": clocks,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "other_configs": other,
+            "cg_kernel": cgk,
         }
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
+
+
+def hbm_peak_gbs():
+    """Measured copy bandwidth of this pool's B200s (MEASURED_PEAKS.json,
+    driver-written) or, without it, the previously measured 6554.9 GB/s."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs"
+    except (OSError, KeyError, ValueError):
+        return 6554.9, "fallback: 6554.9 GB/s measured on an earlier box of this pool"
+
+
+def cg_kernel_line(lib, dev, ps, precision, T=131072, reps=5):
+    """North-star kernel (b) at the run_batch C ABI (fpm_cg): the batched
+    (BJ-)CG from complex128 A, b and block inverses resident in HBM (c5 shape,
+    A / b from fpm_gram, inverses from fpm_bj_setup on generated channels),
+    timed with CUDA events on the launching stream.  HBM roofline: B_cg =
+    16 N^2 + 16 N (2 + L) + 8 bytes per realization (A, b, Minv, x read /
+    written once; flags), against the measured copy bandwidth."""
+    import torch
+    from paper_2504_09820_b200 import _lib
+    H, y, _ = gen_inputs(T, 0, dev, trial0=0)
+    A = torch.empty((T, N, N), dtype=torch.complex128, device=dev)
+    b = torch.empty((T, N), dtype=torch.complex128, device=dev)
+    mv = torch.empty((T, N * L), dtype=torch.complex128, device=dev)
+    x = torch.empty((T, N), dtype=torch.complex128, device=dev)
+    brk = torch.empty((T,), dtype=torch.int32, device=dev)
+    div = torch.empty((T,), dtype=torch.int32, device=dev)
+    from paper_2504_09820_b200.solvers import _stream
+    st = _stream()
+    _lib.check(lib.fpm_gram(H.data_ptr(), y.data_ptr(), T, M, N, SIGMA2, A.data_ptr(), b.data_ptr(), st), "gram")
+    _lib.check(lib.fpm_bj_setup(A.data_ptr(), T, N, L, 0, mv.data_ptr(), None, st), "bj")
+    del H, y
+    s = torch.cuda.current_stream()  # st is its handle
+
+    def cg():
+        _lib.check(lib.fpm_cg(A.data_ptr(), b.data_ptr(), mv.data_ptr(), T, N, L, ITERS, ps, 0, x.data_ptr(),
+                              brk.data_ptr(), div.data_ptr(), st), "fpm_cg")
+
+    cg()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    for _ in range(reps):
+        cg()
+    e1.record(s)
+    e1.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    bpu = 16 * N * N + 16 * N * (2 + L) + 8
+    gbs = bpu * T / (ms / 1e3) / 1e9
+    pk, pks = hbm_peak_gbs()
+    kname = lib.fpm_last_kernel().decode()
+    del A, b, mv, x
+    torch.cuda.empty_cache()
+    return {"boundary": "fpm_cg (run_batch C ABI), complex128 A / b / Minv resident in HBM",
+            "kernel": kname, "T": T, "precision": {"work": "fp64", "matvec": precision, "inner": precision},
+            "ms": round(ms, 3), "det_s": round(T / (ms / 1e3), 1),
+            "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": pk, "unit": "GB/s",
+                         "frac": round(gbs / pk, 4), "bytes_per_unit": bpu, "peak_source": pks}}
 
 
 def run_reference(args):
