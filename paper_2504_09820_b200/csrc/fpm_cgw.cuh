@@ -23,6 +23,7 @@
 // Work format fp64 and u_MV == u_IP native (fp64 / fp32 / fp16 / bf16), N in
 // {32, 64}, plain CG or block-Jacobi with N % L == 0; everything else (and the
 // run_batch histories) runs fpm_cg_kernel.
+#pragma once
 #include "../../include/fpmimo_b200.h"
 #include "fpm_common.cuh"
 #include "fpm_ptx.cuh"
@@ -243,6 +244,42 @@ __device__ __forceinline__ double2 bj_z_s(const double2* ms, int i, const double
 // warp's next A into L2 -- cp.async.bulk.prefetch.L2 -- measured slower at c5
 // fp16, 48.3 M vs 51.7 M/s: one fewer resident warp per SM, and the
 // L2-sourced load phase still took ~11 K cycles.)
+// norm2 (linalg.py:122-134) of the realization's vector held two rows per
+// lane: scale = max |v_k| (NaN-propagating; 1 if not a finite positive
+// number), scale * sqrt(sum (|v_k| / scale)^2), inf if any |v_k| is inf.  The
+// sum runs as a warp tree (NumPy's pairwise sum and the lockstep kernel's
+// sequential sum differ from it, and from each other, in the last bits only).
+template <int RPL>
+__device__ __forceinline__ double cgw_norm2(const double2 (&v)[RPL]) {
+  double h[RPL], scale = 0.0;
+  bool nan = false, inf = false;
+#pragma unroll
+  for (int j = 0; j < RPL; ++j) {
+    h[j] = hypot(v[j].x, v[j].y);
+    nan |= isnan(h[j]);
+    inf |= isinf(h[j]);
+    scale = h[j] > scale ? h[j] : scale;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const double u = __shfl_xor_sync(0xffffffffu, scale, o);
+    scale = u > scale ? u : scale;
+  }
+  nan = __any_sync(0xffffffffu, nan);
+  inf = __any_sync(0xffffffffu, inf);
+  if (nan || !isfinite(scale) || !(scale > 0.0)) scale = 1.0;
+  double s = 0.0;
+#pragma unroll
+  for (int j = 0; j < RPL; ++j) {
+    const double q = __ddiv_rn(h[j], scale);
+    s = __dadd_rn(s, __dmul_rn(q, q));
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, o));
+  const double out = __dmul_rn(scale, __dsqrt_rn(s));
+  return inf ? __longlong_as_double(0x7ff0000000000000LL) : out;
+}
+
 // TM = false: one warp per CTA, A at u_MV in shared memory (CgwLayout).
 // TM = true (N = 64, 32-bit u_MV entries, L in {0, 4}; opt-in, see
 // launch_cgw_t): four warps per CTA,
@@ -267,7 +304,7 @@ struct CgwTmLayout {
   static constexpr int cta_bytes = head + 4 * bytes;
 };
 
-template <int K, int NC, int LB, bool TM>
+template <int K, int NC, int LB, bool TM, bool HIST>
 __global__ void __launch_bounds__(TM ? 128 : 32, TM ? 4 : 1) fpm_cgw_kernel(const CgArgs args) {
   extern __shared__ __align__(128) unsigned char smem[];
   typedef Ar<K> A;
@@ -435,6 +472,44 @@ __global__ void __launch_bounds__(TM ? 128 : 32, TM ? 4 : 1) fpm_cgw_kernel(cons
     double2 carry = make_double2(0.0, 0.0);
     if (!rho_fresh) carry = wsum<K, NC>(tb2, fi);
     int brk = -1, dvg = -1;
+    // ---- run_batch histories (solvers.py:306-319, 369-381); fpm_cg_ex only ----
+    const CgHist& Hh = args.h;
+    constexpr bool hist = HIST;  // compiled out of the plain fpm_cg kernel (registers)
+    const bool hnorm = hist && (Hh.res || Hh.xn || Hh.conv);
+    double h_bn = 0.0, h_res = 0.0, h_xn = 0.0;
+    int h_conv = -1, last = args.iters;
+    auto h_rows = [&](int i) {  // iterates / residual vectors of sweep i
+#pragma unroll
+      for (int j = 0; j < RPL; ++j) {
+        const long o = ((long)i * Hh.T + t) * NC + l + 32 * j;
+        if (Hh.xit) Hh.xit[o] = x[j];
+        if (Hh.rit) Hh.rit[o] = r[j];
+      }
+    };
+    auto h_norms = [&](int i, bool fresh) {  // res_hist[i], xn_hist[i] (solvers.py:373-374)
+      if (!hnorm) return;
+      if (fresh) {
+        h_res = cgw_norm2<RPL>(r);
+        h_xn = i ? cgw_norm2<RPL>(x) : 0.0;
+        if (i == 0) h_bn = h_res;
+      }
+      // converged_at: first sweep whose (possibly frozen) residual is small
+      if (i > 0 && h_conv < 0 && h_res <= Hh.rtol * fmax(h_bn, 1e-300)) h_conv = i;
+      if (l == 0) {
+        if (Hh.res) Hh.res[(long)i * Hh.T + t] = h_res;
+        if (Hh.xn) Hh.xn[(long)i * Hh.T + t] = h_xn;
+      }
+    };
+    auto h_ab = [&](int i, double2 al, double2 be) {  // alphas / betas[i - 1] (solvers.py:371)
+      if (hist && l == 0) {
+        if (Hh.al) Hh.al[(long)(i - 1) * Hh.T + t] = al;
+        if (Hh.be) Hh.be[(long)(i - 1) * Hh.T + t] = be;
+      }
+    };
+    if (hist) {
+      h_norms(0, true);
+      h_rows(0);
+    }
     long long* ph = (trc && t == 0 && l == 0) ? args.trace + 4 * args.T : nullptr;  // phase clocks, realization 0
 #define CGW_ST(k, dep)                                                             \
   do {                                                                             \
@@ -468,7 +543,12 @@ __global__ void __launch_bounds__(TM ? 128 : 32, TM ? 4 : 1) fpm_cgw_kernel(cons
       // stall / breakdown freeze the realization (solvers.py:342-345)
       const bool stall = (rho0.x == 0.0) && (rho0.y == 0.0);
       if (!stall && phi.x <= 0.0) brk = it;
-      if (stall || phi.x <= 0.0) break;
+      if (stall || phi.x <= 0.0) {
+        // alphas records alpha where the lane broke down, 0 on a stall
+        if (hist) h_ab(it, stall ? make_double2(0.0, 0.0) : wdiv<FK_F64>(rho0, phi, fw), make_double2(0.0, 0.0));
+        last = it - 1;
+        break;
+      }
       const double2 al = wdiv<FK_F64>(rho0, phi, fw);
       CGW_ST(3, al.x);
       const double2 nal = make_double2(-al.x, -al.y);
@@ -483,6 +563,8 @@ __global__ void __launch_bounds__(TM ? 128 : 32, TM ? 4 : 1) fpm_cgw_kernel(cons
       }
       if (__any_sync(0xffffffffu, bad)) {
         dvg = it;
+        if (hist) h_ab(it, al, make_double2(0.0, 0.0));
+        last = it - 1;
         break;
       }
 #pragma unroll
@@ -525,8 +607,25 @@ __global__ void __launch_bounds__(TM ? 128 : 32, TM ? 4 : 1) fpm_cgw_kernel(cons
       }
       __syncwarp();
       CGW_ST(8, p[RPL - 1].x);
+      if (hist) {
+        h_ab(it, al, be);
+        h_norms(it, true);
+        h_rows(it);
+      }
     }
 #undef CGW_ST
+    if (hist) {
+      // frozen before the last sweep: the remaining sweeps record the frozen
+      // state (unchanged norms and vectors; zero alphas / betas after the
+      // freezing sweep, whose alpha was recorded above)
+#pragma unroll 1
+      for (int i = last + 1; i <= args.iters; ++i) {
+        if (i > last + 1) h_ab(i, make_double2(0.0, 0.0), make_double2(0.0, 0.0));
+        h_norms(i, false);
+        h_rows(i);
+      }
+      if (Hh.conv && l == 0) Hh.conv[t] = h_conv;
+    }
     if (trc && l == 0) trc[2] = clock64();
 #pragma unroll
     for (int j = 0; j < RPL; ++j) args.x[t * NC + l + 32 * j] = x[j];
@@ -548,8 +647,19 @@ __global__ void __launch_bounds__(TM ? 128 : 32, TM ? 4 : 1) fpm_cgw_kernel(cons
 // One realization per warp.  (Two realizations per warp -- a half-warp each -- was measured slower at c5
 // fp16: 35.9 M vs 51.7 M/s, half the warps per SM and twice the serial load
 // phase per warp.)
+template <int K, int NC, int LB, bool TM, bool HIST>
+inline int launch_cgw_k2(const CgArgs& a, cudaStream_t st) {
+  auto k = fpm_cgw_kernel<K, NC, LB, TM, HIST>;
+  constexpr int smem = TM ? CgwTmLayout<K, NC, LB, true>::cta_bytes : CgwLayout<K, NC, LB>::bytes;
+  if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return FPM_ECUDA;
+  if (TM) k<<<(unsigned)((a.T + 3) / 4), 128, smem, st>>>(a);
+  else k<<<(unsigned)a.T, 32, smem, st>>>(a);
+  count_launch();
+  return cudaGetLastError() == cudaSuccess ? FPM_OK : FPM_ECUDA;
+}
+
 template <int K, int NC, int LB>
-static int launch_cgw_t(const CgArgs& a, cudaStream_t st) {
+inline int launch_cgw_t(const CgArgs& a, cudaStream_t st) {
   constexpr bool tm_ok = NC == 64 && sizeof(typename Ar<K>::C) == 4 && (LB == 0 || LB == 4);
   if constexpr (tm_ok) {
     // opt-in (FPM_CGW_TMEM=1): measured slower than the shared-memory kernel
@@ -557,26 +667,13 @@ static int launch_cgw_t(const CgArgs& a, cudaStream_t st) {
     // but the transposing load phase is twice as long and the sweeps slow
     // down under the extra contention
     const char* e = std::getenv("FPM_CGW_TMEM");
-    if (e && e[0] == '1') {
-      auto k = fpm_cgw_kernel<K, NC, LB, true>;
-      constexpr int smem = CgwTmLayout<K, NC, LB, true>::cta_bytes;
-      if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
-        return FPM_ECUDA;
-      k<<<(unsigned)((a.T + 3) / 4), 128, smem, st>>>(a);
-      count_launch();
-      return cudaGetLastError() == cudaSuccess ? FPM_OK : FPM_ECUDA;
-    }
+    if (e && e[0] == '1' && !a.h.on) return launch_cgw_k2<K, NC, LB, true, false>(a, st);
   }
-  auto k = fpm_cgw_kernel<K, NC, LB, false>;
-  constexpr int smem = CgwLayout<K, NC, LB>::bytes;
-  if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return FPM_ECUDA;
-  k<<<(unsigned)a.T, 32, smem, st>>>(a);
-  count_launch();
-  return cudaGetLastError() == cudaSuccess ? FPM_OK : FPM_ECUDA;
+  return a.h.on ? launch_cgw_k2<K, NC, LB, false, true>(a, st) : launch_cgw_k2<K, NC, LB, false, false>(a, st);
 }
 
 template <int K, int NC>
-static int launch_cgw_n(const CgArgs& a, cudaStream_t st) {
+inline int launch_cgw_n(const CgArgs& a, cudaStream_t st) {
   if (!a.bj) return launch_cgw_t<K, NC, 0>(a, st);
   switch (a.L) {
     case 1: return launch_cgw_t<K, NC, 1>(a, st);
@@ -588,22 +685,10 @@ static int launch_cgw_n(const CgArgs& a, cudaStream_t st) {
 }
 
 template <int K>
-static int launch_cgw_k(const CgArgs& a, cudaStream_t st) {
+inline int launch_cgw_k(const CgArgs& a, cudaStream_t st) {
   if (a.N == 64) return launch_cgw_n<K, 64>(a, st);
   if (a.N == 32) return launch_cgw_n<K, 32>(a, st);
   return FPM_EUNSUPPORTED;
-}
-
-// FPM_EUNSUPPORTED: no warp-CG instance for this (kind, N, L); the caller
-// runs fpm_cg_kernel instead
-int launch_cgw(int mv_kind, const CgArgs& a, cudaStream_t st) {
-  switch (mv_kind) {
-    case FK_F64: return launch_cgw_k<FK_F64>(a, st);
-    case FK_F32: return launch_cgw_k<FK_F32>(a, st);
-    case FK_F16: return launch_cgw_k<FK_F16>(a, st);
-    case FK_BF16: return launch_cgw_k<FK_BF16>(a, st);
-    default: return FPM_EUNSUPPORTED;
-  }
 }
 
 }  // namespace fpm

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "../../include/fpmimo_b200.h"
 #include "fpm_arith.cuh"
 #include "fpm_cg.cuh"
 #include "fpm_gram.cuh"
@@ -93,9 +94,21 @@ FPM_DECLARE_KIND(gen_w)  // everything generic (W != fp64)
 
 void count_launch();
 
-// warp-per-realization CG (fpm_cgw.cu); FPM_EUNSUPPORTED when it has no
-// instance for the configuration
-int launch_cgw(int mv_kind, const CgArgs& a, cudaStream_t st);
+// warp-per-realization CG (fpm_cgw.cuh, one unit per kind: fpm_cgw_<kind>.cu);
+// FPM_EUNSUPPORTED when it has no instance for the configuration
+int launch_cgw_f64(const CgArgs& a, cudaStream_t st);
+int launch_cgw_f32(const CgArgs& a, cudaStream_t st);
+int launch_cgw_f16(const CgArgs& a, cudaStream_t st);
+int launch_cgw_bf16(const CgArgs& a, cudaStream_t st);
+inline int launch_cgw(int mv_kind, const CgArgs& a, cudaStream_t st) {
+  switch (mv_kind) {
+    case FK_F64: return launch_cgw_f64(a, st);
+    case FK_F32: return launch_cgw_f32(a, st);
+    case FK_F16: return launch_cgw_f16(a, st);
+    case FK_BF16: return launch_cgw_bf16(a, st);
+    default: return FPM_EUNSUPPORTED;
+  }
+}
 
 // FP32-Gram extension (fpm_gram32.cu)
 int launch_gram32(const double2* H, const double2* y, long T, int M, int N, double sigma2, double2* A, double2* b,

@@ -804,9 +804,9 @@ int fpm_cg_ex(const double* A, const double* b, const double* Minv, int64_t T, i
   }
   int smem = 0;
   cudaStream_t st = (cudaStream_t)stream;
-  // warp-per-realization fast path (fpm_cgw.cu): fp64 work, native u_MV == u_IP,
-  // no histories; FPM_NO_CGW forces fpm_cg_kernel (A/B and parity tests)
-  if (!a.h.on && k.w == FK_F64 && k.mv == k.ip && k.mv != FK_GEN && !std::getenv("FPM_NO_CGW") &&
+  // warp-per-realization fast path (fpm_cgw.cu): fp64 work, native u_MV == u_IP;
+  // FPM_NO_CGW forces fpm_cg_kernel (A/B and parity tests)
+  if (k.w == FK_F64 && k.mv == k.ip && k.mv != FK_GEN && !std::getenv("FPM_NO_CGW") &&
       !std::getenv("FPM_FORCE_GENERIC") && (!bj || N % L == 0)) {
     const int rw = launch_cgw(k.mv, a, st);
     if (rw != FPM_EUNSUPPORTED) {

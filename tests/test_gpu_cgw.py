@@ -138,3 +138,32 @@ def test_cgw_tmem_variant_matches_oracle(oracle, monkeypatch, fmt):
             assert bits_equal(x, ref.x), (fmt, L, rv)
             np.testing.assert_array_equal(brk, ref.breakdown_at)
             np.testing.assert_array_equal(div, ref.diverged_at)
+
+
+@pytest.mark.parametrize("fmt,N,L", [("fp16", 64, 4), ("bfloat16", 32, 0), ("fp64", 64, 4), ("fp32", 32, 2)])
+def test_cgw_run_batch_histories(oracle, fmt, N, L):
+    """The Python run_batch mirror (solvers.py:262-393; it always requests the
+    norm histories) on the warp kernel: every BatchResult field against the
+    oracle's run_batch restatement, with stall / breakdown / divergence lanes
+    so the frozen-sweep recording is exercised."""
+    from paper_2504_09820_b200 import _lib
+    from paper_2504_09820_b200.formats import get_format
+    from paper_2504_09820_b200.solvers import BatchBlocks, PrecisionConfig, run_batch
+    from test_gpu_parity import HIST_NORMS, _check_history
+    O = oracle
+    T = 6
+    A0, b = _system(O, 2 * N, N, T, 11 + N)
+    A, b = A0.copy(), b.copy()
+    b[1] = 0.0          # stall at sweep 1
+    A[2] = -A[2]        # breakdown at sweep 1
+    A[4, 3, 5] = np.nan  # non-finite update
+    mats = O.bj_inverses(A0, L) if L else None
+    of = O.REGISTRY[fmt]
+    f = get_format(fmt)
+    want = O.cg_batch(A, b, 6, O.FP64, of, of, mats, rtol=1e-3, record=True)
+    res = run_batch(A, b, 6, PrecisionConfig(matvec=f, inner=f), BatchBlocks(_pack(mats, N, L), N, L) if L else None,
+                    rtol=1e-3, record_iterates=True, record_residual_vectors=True)
+    assert _lib.load().fpm_last_kernel().decode().startswith("fpm_cgw_kernel")
+    _check_history(res, {k: getattr(want, k) for k in
+                         ("x", "breakdown_at", "diverged_at", "alphas", "betas", "converged_at", "iterates",
+                          "residual_vectors") + HIST_NORMS}, f"{fmt}-{N}-{L}")

@@ -84,6 +84,18 @@ def main():
         _lib.check(lib.fpm_cg(A.data_ptr(), b.data_ptr(), mv.data_ptr(), T, N, L, bench.ITERS, ps, 0, x.data_ptr(),
                               brk.data_ptr(), div.data_ptr(), st), "cg")
 
+    def cgx():  # run_batch boundary with the histories the Python mirror always requests
+        _lib.check(lib.fpm_cg_ex(A.data_ptr(), b.data_ptr(), mv.data_ptr(), T, N, L, bench.ITERS, ps, 0,
+                                 x.data_ptr(), brk.data_ptr(), div.data_ptr(), ctypes.byref(hist), st), "cg_ex")
+
+    hres = torch.empty((bench.ITERS + 1, T), dtype=torch.float64, device=dev)
+    hxn = torch.empty_like(hres)
+    hal = torch.empty((bench.ITERS, T), dtype=torch.complex128, device=dev)
+    hbe = torch.empty_like(hal)
+    hconv = torch.empty((T,), dtype=torch.int32, device=dev)
+    hist = _lib.CgHistory(hres.data_ptr(), hxn.data_ptr(), hal.data_ptr(), hbe.data_ptr(), hconv.data_ptr(),
+                          1e-6, None, None)
+
     def fused():
         _lib.check(lib.fpm_detect(H.data_ptr(), y.data_ptr(), bits.data_ptr(), T, M, N, bench.SIGMA2, 3, L,
                                   bench.ITERS, ps, 0, 16, None, x.data_ptr(), brk.data_ptr(), div.data_ptr(), None,
@@ -99,6 +111,11 @@ def main():
         byts = 16 * N * N + 16 * N * (2 + L) + 8
         out["cg"] = {"ms": ms, "det_s": T / ms * 1e3, "hbm_gbs": byts * T / (ms / 1e3) / 1e9,
                      "hbm_frac": byts * T / (ms / 1e3) / 6554.9e9}
+    if a.only == "cgx":
+        gram()
+        bj()
+        ms = timeit(cgx, a.reps)
+        out["cg_hist"] = {"ms": ms, "det_s": T / ms * 1e3, "kernel": lib.fpm_last_kernel().decode()}
     if a.cgtrace:  # standalone CG kernel, CTA 0 phase stamps (one wave: 1 CTA per SM)
         gram()
         bj()
