@@ -21,8 +21,8 @@
 // CTAs are one warp, so the block scheduler refills an SM as soon as any
 // realization finishes and loading (HBM latency) overlaps other warps' sweeps.
 // Work format fp64 and u_MV == u_IP native (fp64 / fp32 / fp16 / bf16), N in
-// {32, 64}, plain CG or block-Jacobi with N % L == 0; everything else (and the
-// run_batch histories) runs fpm_cg_kernel.
+// {32, 64}, plain CG or block-Jacobi with L in {1, 2, 4, 8} (with or without
+// the run_batch histories); everything else runs fpm_cg_kernel.
 #pragma once
 #include "../../include/fpmimo_b200.h"
 #include "fpm_common.cuh"
@@ -63,7 +63,10 @@ struct CgwLayout {
   static constexpr int off_t1 = off_t0 + NC * (int)sizeof(C);
   static constexpr int off_t2 = off_t0;
   static constexpr int off_rv = (off_t1 + NC * (int)sizeof(C) + 15) / 16 * 16;
-  static constexpr int bytes = off_rv + (LB > 0 ? NC * 16 : 0);
+  // block-inverse rows: registers unless a lane would hold more than 8
+  static constexpr bool MS = (NC / 32) * LB > 8;
+  static constexpr int off_ms = off_rv + (LB > 0 ? NC * 16 : 0);
+  static constexpr int bytes = off_ms + (MS ? NC * LB * 16 : 0);
   // element offset of A(i, k)
   static __device__ __forceinline__ int at(int i, int k) {
     return (i * UPR + ((k / EPU) ^ (i & 7))) * EPU + k % EPU;
@@ -222,19 +225,27 @@ __device__ __forceinline__ void mv_rows_tm(uint32_t ta, const typename Ar<K>::P*
   out[1] = A::asmc(s[1]);
 }
 
-// z_i from block-inverse rows in shared memory (TMEM kernel; LB = 4): row i's
-// entry k at unit (k + (i >> 1)) % 4 of the row, so 8 lanes reading 8
-// consecutive rows' entry k hit 8 distinct bank groups
+// Block-inverse rows in shared memory (when they do not fit in registers:
+// RPL * L > 8, and in the TMEM variant): row i's entry k at unit
+// ms_unit(i, k) of its L-unit row, so 8 lanes reading 8 consecutive rows'
+// entry k hit 8 distinct 16-byte bank groups.
+template <int LB>
+__device__ __forceinline__ int ms_unit(int i, int k) {
+  if constexpr (LB >= 8) return (k + i) & (LB - 1);
+  else if constexpr (LB == 4) return (k + (i >> 1)) & 3;
+  else if constexpr (LB == 2) return (k + (i >> 2)) & 1;
+  else return 0;
+}
+
 template <int LB>
 __device__ __forceinline__ double2 bj_z_s(const double2* ms, int i, const double2* rv, int s0) {
-  static_assert(LB == 4, "shared-memory block rows: L = 4");
+  static_assert((LB & (LB - 1)) == 0, "power-of-two block size");
   typedef Ar<FK_F64> W;
   const FmtP f{};
   const double2* mr = ms + i * LB;
-  const int o = i >> 1;
-  double2 s = W::mul(mr[o & 3], rv[s0], f);
+  double2 s = W::mul(mr[ms_unit<LB>(i, 0)], rv[s0], f);
 #pragma unroll
-  for (int k = 1; k < LB; ++k) s = W::add(s, W::mul(mr[(k + o) & 3], rv[s0 + k], f), f);
+  for (int k = 1; k < LB; ++k) s = W::add(s, W::mul(mr[ms_unit<LB>(i, k)], rv[s0 + k], f), f);
   return assemble(s.x, s.y);
 }
 
@@ -329,7 +340,8 @@ __global__ void __launch_bounds__(TM ? 128 : 32, TM ? 4 : 1) fpm_cgw_kernel(cons
   C* tb1 = reinterpret_cast<C*>(base + (TM ? TLay::off_t1 : Lay::off_t1));  // phi = p^H w terms
   C* tb2 = reinterpret_cast<C*>(base + (TM ? TLay::off_t2 : Lay::off_t2));  // rho1 / carry terms (tb0's storage)
   double2* rv = reinterpret_cast<double2*>(base + (TM ? TLay::off_rv : Lay::off_rv));
-  double2* ms = reinterpret_cast<double2*>(base + TLay::off_ms);  // TM: block-inverse rows
+  constexpr bool MS = TM || Lay::MS;  // block-inverse rows in shared memory
+  double2* ms = reinterpret_cast<double2*>(base + (TM ? TLay::off_ms : Lay::off_ms));
   const bool rho_fresh = BJ && !args.textbook;  // as_written: rho0 = r^H p every sweep
   uint32_t ta = 0;  // TM: this warp's TMEM base (lane quarter wid, 128 columns)
   if constexpr (TM) {
@@ -423,25 +435,25 @@ __global__ void __launch_bounds__(TM ? 128 : 32, TM ? 4 : 1) fpm_cgw_kernel(cons
     }
     double2 x[RPL], r[RPL], p[RPL];
     C pm[RPL];
-    double2 m[RPL][(LB > 0 && !TM) ? LB : 1];
+    double2 m[RPL][(LB > 0 && !MS) ? LB : 1];
 #pragma unroll
     for (int j = 0; j < RPL; ++j) {
       const int i = l + 32 * j;
       x[j] = make_double2(0.0, 0.0);
       r[j] = args.b[t * NC + i];  // run_batch copies b (solvers.py:297-298)
-      if constexpr (BJ && !TM) {
+      if constexpr (BJ && !MS) {
 #pragma unroll
         for (int k = 0; k < LB; ++k) m[j][k] = args.minv[(t * NC + i) * LB + k];  // row i of its block
       }
-      if constexpr (BJ && TM) {
+      if constexpr (BJ && MS) {
 #pragma unroll
-        for (int k = 0; k < LB; ++k) ms[i * LB + ((k + (i >> 1)) & 3)] = args.minv[(t * NC + i) * LB + k];
+        for (int k = 0; k < LB; ++k) ms[i * LB + ms_unit<LB>(i, k)] = args.minv[(t * NC + i) * LB + k];
       }
     }
     auto zrow = [&](int j) -> double2 {
       const int i = l + 32 * j;
-      if constexpr (TM && BJ) return bj_z_s<LB>(ms, i, rv, i - i % LB);
-      else if constexpr (!TM) return bj_z<(LB > 0 ? LB : 1)>(m[j], rv, i - i % (LB > 0 ? LB : 1));
+      if constexpr (MS && BJ) return bj_z_s<LB>(ms, i, rv, i - i % LB);
+      else if constexpr (!MS) return bj_z<(LB > 0 ? LB : 1)>(m[j], rv, i - i % (LB > 0 ? LB : 1));
       else return rv[i];  // unused (plain CG)
     };
     if (trc) {
@@ -679,7 +691,7 @@ inline int launch_cgw_n(const CgArgs& a, cudaStream_t st) {
     case 1: return launch_cgw_t<K, NC, 1>(a, st);
     case 2: return launch_cgw_t<K, NC, 2>(a, st);
     case 4: return launch_cgw_t<K, NC, 4>(a, st);
-    case 8: return NC == 32 ? launch_cgw_t<K, NC, 8>(a, st) : FPM_EUNSUPPORTED;
+    case 8: return launch_cgw_t<K, NC, 8>(a, st);
     default: return FPM_EUNSUPPORTED;
   }
 }
@@ -688,6 +700,9 @@ template <int K>
 inline int launch_cgw_k(const CgArgs& a, cudaStream_t st) {
   if (a.N == 64) return launch_cgw_n<K, 64>(a, st);
   if (a.N == 32) return launch_cgw_n<K, 32>(a, st);
+  // N = 128 stays on the CTA-lockstep kernel: with 64 KB of fp16 A per warp
+  // only two warps fit per SM and each lane chains four rows; measured at c4
+  // (fp16, L = 8) 23.4 ms vs 20.8 ms per 8192 realizations
   return FPM_EUNSUPPORTED;
 }
 
