@@ -113,7 +113,12 @@ int fpm_gram32(const double* H, const double* y, int64_t T, int32_t M, int32_t N
 int fpm_bj_setup(const double* A, int64_t T, int32_t N, int32_t L, int32_t allow_ragged, double* Minv,
                  int32_t* bad_block, void* stream);
 
-/* Minv == NULL -> plain FP-CG, else FP-BJ-CG with block size L. */
+/* Minv == NULL -> plain FP-CG, else FP-BJ-CG with block size L.  Minv is
+ * (T, N*L) complex128: block k row-major at k*L*L (solvers.py:207-229
+ * _BatchBlocks.mats packed).  Kernel: one warp per realization
+ * (fpm_cgw_kernel) for fp64 work, native u_MV == u_IP, N in {32, 64} and L in
+ * {1, 2, 4, 8}; the CTA-lockstep fpm_cg_kernel otherwise.  Same bits either
+ * way. */
 int fpm_cg(const double* A, const double* b, const double* Minv, int64_t T, int32_t N, int32_t L,
            int32_t iters, const fpm_precision* prec, int32_t rho_update, double* x, int32_t* breakdown_at,
            int32_t* diverged_at, void* stream);
