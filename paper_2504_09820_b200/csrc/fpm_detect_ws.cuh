@@ -31,6 +31,10 @@ namespace fpm {
 #endif
 #define FPM_PIPE_UNROLL FPM_UNROLL_(FPM_PIPE_UNROLL_N)
 
+#ifndef FPM_PRODUCER_LANES  // threads of the producer warp issuing bulk copies (1 or 32)
+#define FPM_PRODUCER_LANES 32
+#endif
+constexpr int kProducerLanes = FPM_PRODUCER_LANES;
 #ifndef FPM_PRODUCER_SLEEP_NS  // back-off of the producer / CG-side waits (0: spin)
 #define FPM_PRODUCER_SLEEP_NS 300  // measured: evens out the producer warp's SM sub-partition (+0.7 %)
 #endif
@@ -421,7 +425,12 @@ FPM_PIPE_UNROLL
     if constexpr (RS > 0) reg_dealloc<256 - RS>();
     if (tid >= pbase && tid < pbase + 32) {
     // ========================= producer warp ==========================
-    if (tid == pbase) {
+    // the whole warp issues (many realizations per group at small N: one bulk
+    // copy per realization and stage, spread over the lanes); lane 0 posts the
+    // expected bytes, every lane waits on the ring barriers
+    const int pl = tid - pbase;
+    const int pn = kProducerLanes;
+    if (pl < pn) {
       // issue global chunk gc (group gc/nch, local chunk gc%nch) into its stage
       auto issue = [&](long gc) {
         const int jj = (int)(gc / nch), c = (int)(gc - (long)jj * nch);
@@ -429,12 +438,13 @@ FPM_PIPE_UNROLL
         const int Rv = (int)min((long)R, args.T - t0);
         if (c == 0) {  // this group's y rides with its first chunk
           double2* yd = ysb + (jj & 1) * R * G.M;
-          mbar_expect_tx(&ybar[jj & 1], (uint32_t)Rv * (uint32_t)G.M * 16u);
-          for (int g = 0; g < Rv; ++g)
+          if (pl == 0) mbar_expect_tx(&ybar[jj & 1], (uint32_t)Rv * (uint32_t)G.M * 16u);
+          if (pn > 1) __syncwarp();
+          for (int g = pl; g < Rv; g += pn)
             bulk_g2s(yd + g * G.M, args.y + (t0 + g) * (long)G.M, G.M * 16u, &ybar[jj & 1]);
         }
         const int s = (int)(gc % G.S);
-        gram_issue(args.H, t0, Rv, G, c, stages + s * stage_elems, &full[s]);
+        gram_issue(args.H, t0, Rv, G, c, stages + s * stage_elems, &full[s], pl, pn);
       };
       fence_proxy_async();
 #pragma unroll 1

@@ -112,13 +112,18 @@ struct GramGeom {
 };
 
 // Issue the bulk copies of chunk `c` (rows c*MC ..) for every valid slot.
+// lane / nlanes: the copies of one stage are issued by nlanes threads of one
+// warp (the realizations' row blocks are separate bulk copies); lane 0 posts
+// the stage's expected bytes first.  nlanes > 1 must be a whole warp.
 __device__ __forceinline__ void gram_issue(const double2* H, long t0, int Rv, const GramGeom& G,
-                                           int chunk, double2* stage_buf, uint64_t* bar) {
+                                           int chunk, double2* stage_buf, uint64_t* bar, int lane = 0,
+                                           int nlanes = 1) {
   const int m0 = chunk * G.MC;
   const int rows = min(G.MC, G.M - m0);
   const uint32_t rowb = (uint32_t)G.N * 16u;
-  mbar_expect_tx(bar, (uint32_t)Rv * (uint32_t)rows * rowb);
-  for (int g = 0; g < Rv; ++g) {
+  if (lane == 0) mbar_expect_tx(bar, (uint32_t)Rv * (uint32_t)rows * rowb);
+  if (nlanes > 1) __syncwarp();
+  for (int g = lane; g < Rv; g += nlanes) {
     const double2* src = H + ((t0 + g) * (long)G.M + m0) * (long)G.N;
     double2* dst = stage_buf + (long)g * G.MC * G.Np;
     if (G.N == G.Np) {
