@@ -181,10 +181,12 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
-        dist.init_process_group("nccl")
+    # bind the rank's GPU before NCCL initialises (barriers / all-reduces then
+    # use this device, one rank per GPU)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
     lib = _lib.load()
     det = DetectorSpec("fp_bj_cg", iters=ITERS, L=L, matvec=args.precision, inner=args.precision)
     ps = _lib.precision_struct(det.precision())

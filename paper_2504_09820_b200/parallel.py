@@ -56,11 +56,14 @@ def init(backend: str | None = None):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     backend = backend or ("nccl" if torch.cuda.is_available() else "gloo")
-    if world > 1 and not dist.is_initialized():
-        dist.init_process_group(backend)
     dev = torch.device("cuda", local) if backend == "nccl" else torch.device("cpu")
-    if dev.type == "cuda":
+    if dev.type == "cuda":  # bind the rank's GPU before NCCL initialises
         torch.cuda.set_device(dev)
+    if world > 1 and not dist.is_initialized():
+        if dev.type == "cuda":
+            dist.init_process_group(backend, device_id=dev)
+        else:
+            dist.init_process_group(backend)
     rank = dist.get_rank() if dist.is_initialized() else 0
     return rank, world, dev
 
