@@ -39,6 +39,16 @@ namespace fpm {
 #ifndef FPM_CGW_PREFETCH
 #define FPM_CGW_PREFETCH 1
 #endif
+// alpha / beta: NumPy's Smith division at u_W = binary64 (the rounding to
+// u_W is the identity).  Inline for 32-bit u_MV (c5 fp16 55.6 -> 56.5 M/s);
+// the shared __noinline__ wdiv for 16-byte u_MV, whose kernels are
+// register-bound (inline measured 13.5 -> 13.1 M/s at fp64).
+template <int K>
+__device__ __forceinline__ double2 cgw_div(double2 n, double2 d) {
+  if constexpr (sizeof(typename Ar<K>::C) >= 16) return wdiv<FK_F64>(n, d, FmtP{});
+  else return cdiv(n, d);
+}
+#define CGW_DIV(n, d) cgw_div<K>((n), (d))
 #ifndef FPM_CGW_LOADS
 #define FPM_CGW_LOADS 16
 #endif
@@ -557,11 +567,11 @@ __global__ void __launch_bounds__(TM ? 128 : 32, TM ? 4 : 1) fpm_cgw_kernel(cons
       if (!stall && phi.x <= 0.0) brk = it;
       if (stall || phi.x <= 0.0) {
         // alphas records alpha where the lane broke down, 0 on a stall
-        if (hist) h_ab(it, stall ? make_double2(0.0, 0.0) : wdiv<FK_F64>(rho0, phi, fw), make_double2(0.0, 0.0));
+        if (hist) h_ab(it, stall ? make_double2(0.0, 0.0) : CGW_DIV(rho0, phi), make_double2(0.0, 0.0));
         last = it - 1;
         break;
       }
-      const double2 al = wdiv<FK_F64>(rho0, phi, fw);
+      const double2 al = CGW_DIV(rho0, phi);
       CGW_ST(3, al.x);
       const double2 nal = make_double2(-al.x, -al.y);
       // ---- x, r updates at u_W; non-finite -> diverged (solvers.py:346-354) ----
@@ -604,7 +614,7 @@ __global__ void __launch_bounds__(TM ? 128 : 32, TM ? 4 : 1) fpm_cgw_kernel(cons
       __syncwarp();
       const double2 rho1 = wsum<K, NC>(tb2, fi);
       CGW_ST(6, rho1.x);
-      const double2 be = wdiv<FK_F64>(rho1, rho0, fw);
+      const double2 be = CGW_DIV(rho1, rho0);
       CGW_ST(7, be.x);
       carry = rho1;
       __syncwarp();  // every lane's rho1 chain has read tb2 (= tb0's storage)
