@@ -28,6 +28,9 @@
  * Conventions
  *   - complex128 arrays are interleaved (re, im) doubles, C-contiguous,
  *     exactly NumPy's layout: H (T, M, N), y (T, M), A (T, N, N), b/x (T, N).
+ *     Device complex128 arrays must be 16-byte aligned (NumPy / torch
+ *     allocations are); the device entry points return FPM_EINVAL otherwise
+ *     (fpm_detect_host copies host arrays and accepts any alignment).
  *   - Block-Jacobi inverses ("Minv") are packed per realization with a fixed
  *     stride of N*L complex entries: block k (size Lk = min(L, N - kL)) is the
  *     row-major Lk x Lk matrix starting at entry k*L*L.

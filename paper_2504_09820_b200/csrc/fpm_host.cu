@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <initializer_list>
 #include <atomic>
 #include <cmath>
 #include <cstdint>
@@ -593,6 +594,15 @@ static int launch_cg(const Kinds& k, const CgArgs& a, int smem, cudaStream_t st)
   }
 }
 
+// complex128 device arrays are read / written as 16-byte vectors: a pointer
+// off 16-byte alignment would fault on the device (a sticky CUDA error), so
+// the entry points reject it up front (FPM_EINVAL).  NULL passes.
+static bool al16_all(std::initializer_list<const void*> ps) {
+  for (const void* p : ps)
+    if (reinterpret_cast<uintptr_t>(p) & 15) return false;
+  return true;
+}
+
 static int check_prec(const fpm_precision* p) {
   if (!p) return FPM_EINVAL;
   if (!valid_format(p->work) || !valid_format(p->matvec) || !valid_format(p->inner)) return FPM_EINVAL;
@@ -666,6 +676,7 @@ int fpm_probe_fp64(int64_t iters, double* dp_ops_per_s) {
 int fpm_gram(const double* H, const double* y, int64_t T, int32_t M, int32_t N, double sigma2, double* A,
              double* b, void* stream) {
   if (T < 0 || M < 1 || N < 1 || (T > 0 && (!H || !y || !A || !b))) return FPM_EINVAL;  // T = 0: empty batch
+  if (!al16_all({H, y, A, b})) return FPM_EINVAL;
   if (N > kMaxN || M > kMaxM) return FPM_EUNSUPPORTED;
   if (T == 0) return FPM_OK;
   {
@@ -726,6 +737,7 @@ int fpm_gram(const double* H, const double* y, int64_t T, int32_t M, int32_t N, 
 int fpm_bj_setup(const double* A, int64_t T, int32_t N, int32_t L, int32_t allow_ragged, double* Minv,
                  int32_t* bad_block, void* stream) {
   if (T < 0 || N < 1 || L < 1 || L > N || (T > 0 && (!A || !Minv))) return FPM_EINVAL;
+  if (!al16_all({A, Minv})) return FPM_EINVAL;
   if (N % L && !allow_ragged) return FPM_EINVAL;  // solvers.py:240-241
   if (N > kMaxN || L > kMaxL) return FPM_EUNSUPPORTED;
   if (T == 0) return FPM_OK;
@@ -762,6 +774,8 @@ int fpm_cg_ex(const double* A, const double* b, const double* Minv, int64_t T, i
               const fpm_precision* prec, int32_t rho_update, double* x, int32_t* breakdown_at,
               int32_t* diverged_at, const fpm_cg_history* hist, void* stream) {
   if (T < 0 || N < 1 || (T > 0 && (!A || !b || !x || !breakdown_at || !diverged_at))) return FPM_EINVAL;
+  if (!al16_all({A, b, Minv, x})) return FPM_EINVAL;
+  if (hist && !al16_all({hist->alphas, hist->betas, hist->iterates, hist->residual_vectors})) return FPM_EINVAL;
   if (iters < 1) return FPM_EINVAL;                                                   // solvers.py:282-283
   if (rho_update != FPM_RHO_AS_WRITTEN && rho_update != FPM_RHO_TEXTBOOK) return FPM_EINVAL;  // :280-281
   int rc = check_prec(prec);
@@ -846,6 +860,7 @@ int fpm_cg(const double* A, const double* b, const double* Minv, int64_t T, int3
 int fpm_gram32(const double* H, const double* y, int64_t T, int32_t M, int32_t N, double sigma2, double* A,
                double* b, void* stream) {
   if (T < 0 || M < 1 || N < 1 || (T > 0 && (!H || !y || !A || !b))) return FPM_EINVAL;  // T = 0: empty batch
+  if (!al16_all({H, y, A, b})) return FPM_EINVAL;
   if (N > kMaxN || M > kMaxM) return FPM_EUNSUPPORTED;
   if (T == 0) return FPM_OK;
   return launch_gram32(reinterpret_cast<const double2*>(H), reinterpret_cast<const double2*>(y), T, M, N, sigma2,
@@ -854,6 +869,7 @@ int fpm_gram32(const double* H, const double* y, int64_t T, int32_t M, int32_t N
 
 int fpm_lmmse(const double* A, const double* b, int64_t T, int32_t N, double* x, int32_t* nonpd, void* stream) {
   if (T < 0 || N < 1 || (T > 0 && (!A || !b || !x))) return FPM_EINVAL;
+  if (!al16_all({A, b, x})) return FPM_EINVAL;
   if (N > kMaxN) return FPM_EUNSUPPORTED;
   if (T == 0) return FPM_OK;
   return launch_lmmse(reinterpret_cast<const double2*>(A), reinterpret_cast<const double2*>(b), T, N,
@@ -863,6 +879,7 @@ int fpm_lmmse(const double* A, const double* b, int64_t T, int32_t N, double* x,
 int fpm_slice_count(const double* x, const uint8_t* tx_bits, int64_t T, int32_t N, int32_t qam,
                     uint8_t* rx_bits, int64_t* counters, void* stream) {
   if (T < 0 || N < 1 || !counters || (T > 0 && !x) || (qam != 16 && qam != 64)) return FPM_EINVAL;
+  if (!al16_all({x})) return FPM_EINVAL;
   if (T == 0) return FPM_OK;
   const long TN = T * (long)N;
   const int tpb = 256;
@@ -1039,6 +1056,7 @@ int fpm_detect(const double* H, const double* y, const uint8_t* tx_bits, int64_t
                int32_t rho_update, int32_t qam, const double* Minv_in, double* x, int32_t* breakdown_at,
                int32_t* diverged_at, uint8_t* rx_bits, int64_t* counters, void* stream) {
   if (!counters || (T > 0 && (!H || !y || !x || !breakdown_at || !diverged_at))) return FPM_EINVAL;
+  if (!al16_all({H, y, x, Minv_in})) return FPM_EINVAL;
   DetectArgs a;
   Kinds k;
   int threads = 0, grid = 0;

@@ -55,6 +55,14 @@ def test_argument_validation_without_gpu(lib):
     assert lib.fpm_cg(dummy, dummy, None, 1, 8, 1, 3, ps, 7, dummy, dummy, dummy, None) == 1
     bad = _lib.Precision(_lib.Format(11, 5, 1), _lib.Format(53, 11, 1), _lib.Format(53, 11, 1))
     assert lib.fpm_cg(dummy, dummy, None, 1, 8, 1, 3, bad, 0, dummy, dummy, dummy, None) == 1
+    # device complex128 arrays off 16-byte alignment: rejected before any launch
+    odd = ctypes.c_void_p(24)
+    assert lib.fpm_cg(odd, dummy, None, 1, 8, 1, 3, ps, 0, dummy, dummy, dummy, None) == 1
+    assert lib.fpm_cg(dummy, dummy, None, 1, 8, 1, 3, ps, 0, odd, dummy, dummy, None) == 1
+    assert lib.fpm_gram(odd, dummy, 1, 16, 8, 0.1, dummy, dummy, None) == 1
+    assert lib.fpm_lmmse(dummy, odd, 1, 8, dummy, None, None) == 1
+    assert lib.fpm_detect(dummy, odd, None, 1, 16, 8, 0.1, 3, 4, 4, ps, 0, 16, None, dummy, dummy, dummy,
+                          None, dummy, None) == 1
     # L must divide N for the detector (build_blocks_batch default)
     assert lib.fpm_detect(dummy, dummy, None, 1, 16, 8, 0.1, 3, 3, 4, ps, 0, 16, None, dummy, dummy, dummy,
                           None, dummy, None) == 1
