@@ -33,9 +33,6 @@
 
 namespace fpm {
 
-#ifndef FPM_CGW_FUSE_RHO0
-#define FPM_CGW_FUSE_RHO0 0
-#endif
 #ifndef FPM_CGW_PREFETCH
 #define FPM_CGW_PREFETCH 1
 #endif
@@ -84,15 +81,13 @@ struct CgwLayout {
 };
 
 // w_i = sum_k A(i,k) p_k (matvec_fp, linalg.py:45-69) for the lane's RPL
-// rows -- one left-to-right chain per row -- and, in the same loop, the
-// optional left-to-right sum of the terms `ct` (the rho0 = r^H p chain of
-// as-written BJ, dot_fp's accumulation linalg.py:94-95): RPL + 1 independent
-// chains interleaved block by block.  The prepared p block is shared by the
-// rows.
-template <int K, int NC, int RPL, int LPR, bool CHAIN>
-__device__ __forceinline__ void mv_rows(const typename Ar<K>::C* At, const typename Ar<K>::P* pv,
-                                        const typename Ar<K>::C* ct, int lane, typename Ar<K>::C (&out)[RPL],
-                                        double2& csum, const FmtP& f, const FmtP& fi) {
+// rows: one left-to-right chain per row, the rows' chains interleaved block
+// by block; the prepared p block is shared by the rows.  (Folding the
+// as-written rho0 = r^H p chain into this loop as one more chain measured
+// 1.5 % slower at fp16 and 13 % at fp64: register pressure.)
+template <int K, int NC, int RPL, int LPR>
+__device__ __forceinline__ void mv_rows(const typename Ar<K>::C* At, const typename Ar<K>::P* pv, int lane,
+                                        typename Ar<K>::C (&out)[RPL], const FmtP& f) {
   typedef Ar<K> A;
   typedef typename A::C C;
   typedef typename A::P P;
@@ -107,13 +102,11 @@ __device__ __forceinline__ void mv_rows(const typename Ar<K>::C* At, const typen
     row[j] = At + i * NC;
     sw[j] = i & 7;
   }
-  C s[RPL], c;
+  C s[RPL];
 #pragma unroll
   for (int kb = 0; kb < NB; ++kb) {
     P p[B];
     ld_blk<B>(pv + kb * B, p);
-    C cc[B];
-    if constexpr (CHAIN) ld_blk<B>(ct + kb * B, cc);
 #pragma unroll
     for (int j = 0; j < RPL; ++j) {
       C a[B];
@@ -124,14 +117,9 @@ __device__ __forceinline__ void mv_rows(const typename Ar<K>::C* At, const typen
         s[j] = (kb + u == 0) ? t : A::add(s[j], t, f);
       }
     }
-    if constexpr (CHAIN) {
-#pragma unroll
-      for (int u = 0; u < B; ++u) c = (kb + u == 0) ? cc[u] : A::add(c, cc[u], fi);
-    }
   }
 #pragma unroll
   for (int j = 0; j < RPL; ++j) out[j] = A::asmc(s[j]);
-  if constexpr (CHAIN) csum = A::wide(A::asmc(c));
 }
 
 // left-to-right sum of the NC terms in shared memory (dot_fp's
@@ -546,15 +534,9 @@ __global__ void __launch_bounds__(TM ? 128 : 32, TM ? 4 : 1) fpm_cgw_kernel(cons
       if constexpr (TM) {
         mv_rows_tm<K>(ta, pmv, wc, fm);
       } else {
-#if FPM_CGW_FUSE_RHO0
-        if (rho_fresh) mv_rows<K, NC, RPL, 32, true>(At, pmv, tb0, l, wc, rho0, fm, fi);
-        else
-#endif
-          mv_rows<K, NC, RPL, 32, false>(At, pmv, tb0, l, wc, rho0, fm, fi);
+        mv_rows<K, NC, RPL, 32>(At, pmv, l, wc, fm);
       }
-      if (!FPM_CGW_FUSE_RHO0 || TM) {
-        if (rho_fresh) rho0 = wsum<K, NC>(tb0, fi);
-      }
+      if (rho_fresh) rho0 = wsum<K, NC>(tb0, fi);
       CGW_ST(0, A::wide(wc[RPL - 1]).x);
       CGW_ST(1, rho0.x);
 #pragma unroll
