@@ -492,7 +492,11 @@ static bool plan_detect_ws(int M, int N, int L, int bj, int iters, int mvk, int 
           a.ldA = ldA;
           a.smem_bytes = (int)off;
           a.ws_gt = gt;
-          a.ws_ct = env_int("FPM_WS_CT", cg_threads(R, gt));
+          // one CG group: 192 threads (six warps) except at N = 32, measured
+          // against the full 224: c3 +1.9 %, c1 +1.3 %, c5 fp64 +0.6 %, c5 fp16
+          // +-0, c2 (N = 32) -1.8 %
+          const int ct_def = (ncg == 1 && gt == 256 && N != 32) ? 192 : cg_threads(R, gt);
+          a.ws_ct = env_int("FPM_WS_CT", ct_def);
           a.ws_ncg = ncg;
           a.ws_ct0 = ncg == 2 ? 128 : a.ws_ct;
           a.ws_nslot = nslot;
