@@ -37,7 +37,10 @@
  *   - All pointers except in fpm_detect_host are DEVICE pointers owned by the
  *     caller; inputs are never modified (solvers.py:297-298).  `stream` is a
  *     cudaStream_t (NULL = legacy default stream).  Calls are asynchronous on
- *     `stream`, carry no global mutable state and are re-entrant.
+ *     `stream`, carry no global mutable state and are re-entrant.  (The
+ *     only process-wide objects: an atomic launch counter, the FPM_* planner
+ *     knobs read once when the library loads, and fpm_detect_host's per-device
+ *     staging pool, created once.)
  *   - Return: FPM_OK, or an error code; precondition failures (the reference's
  *     ContractViolation, errors.py:4-9) are FPM_EINVAL / FPM_ENOTPD.
  *     Numerical failures are flags, not errors (solvers.py:302-303).
@@ -207,8 +210,9 @@ const char* fpm_last_kernel(void);
  * second on the current device (synchronous; the fp64 roofline denominator). */
 int fpm_probe_fp64(int64_t iters, double* dp_ops_per_s);
 
-/* Diagnostic: device buffer (int64[16]) that subsequent fpm_detect launches
- * fill with clock64() phase stamps from CTA 0 (NULL disables). */
+/* Diagnostic builds only (compiled with -DFPM_DIAG, tools/): device buffer
+ * that subsequent launches fill with clock64() phase stamps (NULL disables).
+ * The product library keeps no such state and returns FPM_EUNSUPPORTED. */
 int fpm_debug_set_trace(int64_t* dev_buf);
 
 #ifdef __cplusplus

@@ -13,6 +13,7 @@ from __future__ import annotations
 
 import concurrent.futures as cf
 import glob
+import hashlib
 import os
 import subprocess
 import sys
@@ -38,11 +39,30 @@ def _headers():
     return sorted(glob.glob(os.path.join(CSRC, "*.cuh"))) + [HEADER]
 
 
+def _stamp() -> str:
+    """Content hash of everything the library is built from: the compiler
+    command line (nvcc path, FLAGS incl. FPM_NVCC_EXTRA), this script and every
+    source / header.  Written next to the .so; a mismatch forces a rebuild (a
+    pushed prebuilt library built from other sources or flags is never reused:
+    bit-exactness depends on -fmad=false)."""
+    h = hashlib.sha256()
+    h.update(repr((NVCC, FLAGS, ARCH)).encode())
+    for f in [os.path.abspath(__file__)] + _units() + _headers():
+        h.update(os.path.basename(f).encode())
+        with open(f, "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()
+
+
+def _stamp_path() -> str:
+    return OUT + ".stamp"
+
+
 def needs_build() -> bool:
-    if not os.path.exists(OUT):
+    if not os.path.exists(OUT) or not os.path.exists(_stamp_path()):
         return True
-    t = os.path.getmtime(OUT)
-    return any(os.path.getmtime(d) > t for d in _units() + _headers())
+    with open(_stamp_path()) as fh:
+        return fh.read().strip() != _stamp()
 
 
 def _compile(src: str, verbose: bool) -> tuple[str, str]:
@@ -69,6 +89,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}{r.stderr}")
     os.replace(OUT + ".tmp", OUT)
+    with open(_stamp_path(), "w") as fh:
+        fh.write(_stamp() + "\n")
     return OUT
 
 

@@ -25,6 +25,17 @@
 
 namespace fpm {
 
+// Diagnostics (phase clock traces, FPM_DEBUG skip bits for attribution) exist
+// only in diagnostic builds (-DFPM_DIAG, tools/); in the product library the
+// trace pointer and the skip bits are compile-time null / zero.
+#ifdef FPM_DIAG
+constexpr bool kDiag = true;
+#else
+constexpr bool kDiag = false;
+#endif
+__host__ __device__ __forceinline__ long long* diag_trace(long long* p) { return kDiag ? p : nullptr; }
+__host__ __device__ __forceinline__ int diag_bits(int d) { return kDiag ? d : 0; }
+
 // Row pitch (elements) of the u_MV matrix in shared memory: the smallest
 // ldA >= N whose row is an odd number of 16-byte units, so rows start
 // 16-byte aligned (LDS.128) and 8 consecutive rows fall on 8 distinct

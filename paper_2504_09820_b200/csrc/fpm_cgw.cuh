@@ -356,7 +356,7 @@ __global__ void __launch_bounds__(TM ? 128 : 32, TM ? 4 : 1) fpm_cgw_kernel(cons
   }
 
   if (valid) {
-    long long* trc = args.trace ? args.trace + 4 * t : nullptr;  // diagnostic per-realization clocks
+    long long* trc = diag_trace(args.trace) ? diag_trace(args.trace) + 4 * t : nullptr;  // diagnostic per-realization clocks
     if (trc && l == 0) {
       unsigned sm;
       asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
@@ -670,7 +670,7 @@ inline int launch_cgw_t(const CgArgs& a, cudaStream_t st) {
     // at c5 fp16 (50.4 M vs 55.5 M det/s): 15 resident warps instead of 12,
     // but the transposing load phase is twice as long and the sweeps slow
     // down under the extra contention
-    const char* e = std::getenv("FPM_CGW_TMEM");
+    const char* e = knob("FPM_CGW_TMEM");
     if (e && e[0] == '1' && !a.h.on) return launch_cgw_k2<K, NC, LB, true, false>(a, st);
   }
   return a.h.on ? launch_cgw_k2<K, NC, LB, false, true>(a, st) : launch_cgw_k2<K, NC, LB, false, false>(a, st);

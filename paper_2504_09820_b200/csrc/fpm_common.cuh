@@ -94,6 +94,9 @@ FPM_DECLARE_KIND(gen_w)  // everything generic (W != fp64)
 
 void count_launch();
 
+// FPM_* planner knob from the load-time snapshot (fpm_host.cu), nullptr if unset
+const char* knob(const char* name);
+
 // warp-per-realization CG (fpm_cgw.cuh, one unit per kind: fpm_cgw_<kind>.cu);
 // FPM_EUNSUPPORTED when it has no instance for the configuration
 int launch_cgw_f64(const CgArgs& a, cudaStream_t st);

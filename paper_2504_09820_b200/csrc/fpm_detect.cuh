@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_kernel(const DetectArgs arg
   if (tid < FPM_NCOUNTERS) cnt[tid] = 0ULL;
 #pragma unroll 1
   for (int g = tid; g < G.R; g += nthreads) S.fl[g * 4] = g < Rv ? 1 : 0;
-  long long* tr = (args.trace && blockIdx.x == 0) ? args.trace : nullptr;
+  long long* tr = (diag_trace(args.trace) && blockIdx.x == 0) ? diag_trace(args.trace) : nullptr;
   FPM_STAMP(tr, 0);
   __syncthreads();
 
@@ -340,7 +340,7 @@ __global__ void __launch_bounds__(256) fpm_cg_kernel(const CgArgs args) {
   __syncthreads();
   {
     CtaBar bar;
-    long long* tr = (args.trace && blockIdx.x == 0) ? args.trace : nullptr;
+    long long* tr = (diag_trace(args.trace) && blockIdx.x == 0) ? diag_trace(args.trace) : nullptr;
     if (tr && tid == 0) tr[60] = clock64();
     cg_group<WK, K, LB, NC>(S, Rv, args.iters, args.bj != 0, args.textbook != 0, args.pr, nthreads, tid, bar, tr);
   }

@@ -55,18 +55,10 @@ struct WsLayout {  // byte offsets inside one hand-off slot
   int at, b, d, bytes;
 };
 
-// role order (planner's choice, FPM_WS_ORDER overrides: 0 = Gram warps first, 1 = CG first)
+// role order (planner's choice, FPM_WS_ORDER knob overrides: 0 = Gram warps first, 1 = CG first)
 inline int env_order(int planned) {
-  const char* v = std::getenv("FPM_WS_ORDER");
+  const char* v = knob("FPM_WS_ORDER");
   return v ? (std::atoi(v) != 0) : planned;
-}
-
-// CG group width under the register split (FPM_WS_CT, default: all 224
-// remaining threads), rounded to whole warps
-inline int env_ct() {
-  const char* v = std::getenv("FPM_WS_CT");
-  const int c = v ? std::atoi(v) : 224;
-  return c / 32 * 32;
 }
 
 // RS > 0: register split (setmaxnreg) for a 512-thread block with gt == 256:
@@ -108,7 +100,7 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const DetectArgs 
   __shared__ unsigned long long cnt[FPM_NCOUNTERS];
   // diagnostic timeline of CTA 0, groups 0..7: [j*8 + 0] gram loop start,
   // 1 gram loop end, 2 slot acquired, 3 hand-off done, 4 cg start, 5 cg end
-  long long* tr = (args.trace && blockIdx.x == 0) ? args.trace : nullptr;
+  long long* tr = (diag_trace(args.trace) && blockIdx.x == 0) ? diag_trace(args.trace) : nullptr;
 
   if (tid == 0) {
     for (int s = 0; s < G.S; ++s) {
@@ -176,7 +168,7 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const DetectArgs 
       // serial mode (debug bit 8): the Gram of group j starts only once the CG
       // has released the slot of group j - nsl, i.e. no Gram / CG overlap --
       // faster when both compete for the FP64 pipe (fp64 matvec)
-      if ((args.debug & 8) && j >= nsl && !args.gram_A) mbar_wait(&sempty[slot], (uint32_t)((use - 1) & 1));
+      if ((diag_bits(args.debug) & 8) && j >= nsl && !args.gram_A) mbar_wait(&sempty[slot], (uint32_t)((use - 1) & 1));
       if (tr && tid == 0 && j < 8) tr[j * 8 + 0] = clock64();
 
 #pragma unroll 1
@@ -189,7 +181,7 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const DetectArgs 
         const int rows = min(G.MC, G.M - m0);
         const double2* pa = sb + joff + job.a;
         const double2* pc = sb + joff + job.c;
-        if (args.debug & 4) {
+        if (diag_bits(args.debug) & 4) {
           // diagnostic: Gram math skipped (CG measured without FP64 contention)
         } else if (active && !job.half) {
           // software-pipelined: row mm+1's operands (tile and chain) are in
@@ -318,7 +310,7 @@ FPM_PIPE_UNROLL
         }
         // matched-filter chains (split re / im, exact): chain q -> slot g,
         // entry n, part (0 re / 1 im); accumulators round-trip through smem
-        if (!kChainInLoop && !(args.debug & 2)) {
+        if (!kChainInLoop && !(diag_bits(args.debug) & 2)) {
 #pragma unroll 1
           for (int q = tid; q < nchain; q += gt) {
             const int g = q / (2 * N), e = q - g * 2 * N;
@@ -475,7 +467,7 @@ FPM_PIPE_UNROLL
     S.L = L;
     S.ldA = ldA;
     S.minv = reinterpret_cast<double2*>(cgs + args.off_minv);
-    S.dbg = args.debug;
+    S.dbg = diag_bits(args.debug);
     double2* vec = reinterpret_cast<double2*>(cgs + args.off_vec);
     const int RN = R * N;
     S.x = vec + RN;
@@ -531,7 +523,7 @@ FPM_PIPE_UNROLL
             const int g = q / nblk, kb = q - g * nblk;
             const int Lk = min(L, N - kb * L);
             double2* out = S.minv + g * N * L + kb * L * L;
-            const bool ok = (args.debug & 32) ? true : (LB > 0) ? hpd_inverse<LB>(dS + q, nbt, scr2 + q, nbt, out, Lk)
+            const bool ok = (diag_bits(args.debug) & 32) ? true : (LB > 0) ? hpd_inverse<LB>(dS + q, nbt, scr2 + q, nbt, out, Lk)
                                      : hpd_inverse<0>(dS + q, nbt, scr2 + q, nbt, out, Lk);
             if (!ok) {
               atomicExch(&S.fl[g * 4], 0);
@@ -548,7 +540,7 @@ FPM_PIPE_UNROLL
         __shared__ int _fpm_dummy_ws;
         tc[60] = (long long)clock64() + (*(volatile int*)&_fpm_dummy_ws == 0x7fffffff);
       }
-      if (!(args.debug & 1)) cg_group<WK, K, LB, kCgNC>(S, Rv, args.iters, args.bj != 0, args.textbook != 0, args.pr, ctg, lt, cbar, tc);
+      if (!(diag_bits(args.debug) & 1)) cg_group<WK, K, LB, kCgNC>(S, Rv, args.iters, args.bj != 0, args.textbook != 0, args.pr, ctg, lt, cbar, tc);
       // slot no longer needed (A, b, diagonal blocks consumed)
       if (lt == 0) mbar_arrive(&sempty[slot]);
       if (tr && lt == 0 && j < 8) tr[j * 8 + 5] = clock64();
@@ -604,7 +596,7 @@ int launch_detect_ws_t(const DetectArgs& a, const WsLayout& sl, int grid, cudaSt
   if constexpr (NB == 16) {
     // N = 64, R = 2: 256 Gram threads = two warp groups and a 512-thread
     // block -> register split between the Gram and the other warp groups
-    if (a.ws_gt == 256 && threads <= 512 && !std::getenv("FPM_WS_NOSPLIT")) {
+    if (a.ws_gt == 256 && threads <= 512 && !knob("FPM_WS_NOSPLIT")) {
       // a narrower CG group leaves idle warps in the upper warp groups (they
       // still take part in the register hand-over); CG-first order needs the
       // CG group to fill warp groups 0-1 so the Gram starts at warp group 2

@@ -11,14 +11,52 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
+#include <string>
+#include <unistd.h>
+#include <utility>
+#include <vector>
 
 #include "../../include/fpmimo_b200.h"
 #include "fpm_detect_ws.cuh"
 
 namespace fpm {
 
-static std::atomic<long long> g_launches{0};
-static long long* g_trace = nullptr;  // diagnostic phase timestamps (fpm_debug_set_trace)
+static std::atomic<long long> g_launches{0};  // diagnostic launch counter (fpm_launch_count)
+#ifdef FPM_DIAG
+static long long* g_trace = nullptr;  // diagnostic builds only: phase timestamps (fpm_debug_set_trace)
+#else
+static long long* const g_trace = nullptr;
+#endif
+
+// Planner / A-B knobs (FPM_* environment variables) are read ONCE, when the
+// library loads, into an immutable snapshot: no per-call environment lookup, and a
+// variable set after load has no effect (tests that force a kernel path run
+// in a fresh process).
+namespace {
+struct KnobSnapshot {
+  std::vector<std::pair<std::string, std::string>> kv;
+  KnobSnapshot() {
+    for (char** e = environ; e && *e; ++e) {
+      const char* s = *e;
+      if (std::strncmp(s, "FPM_", 4) != 0) continue;
+      const char* eq = std::strchr(s, '=');
+      if (eq) kv.emplace_back(std::string(s, eq - s), std::string(eq + 1));
+    }
+  }
+};
+const KnobSnapshot& knob_snapshot() {
+  static const KnobSnapshot k;  // thread-safe one-time initialisation
+  return k;
+}
+__attribute__((constructor)) void knob_snapshot_at_load() { (void)knob_snapshot(); }
+}  // namespace
+
+const char* knob(const char* name) {
+  for (const auto& p : knob_snapshot().kv)
+    if (p.first == name) return p.second.c_str();
+  return nullptr;
+}
 
 constexpr int kMaxN = 128;
 constexpr int kMaxL = 16;
@@ -232,7 +270,7 @@ static Kinds pick_kinds(const fpm_precision& p) {
   Kinds k;
   // test hook: run the integer-emulation path for every format (it must give
   // the same bits as the native-arithmetic kernels)
-  const char* fg = std::getenv("FPM_FORCE_GENERIC");
+  const char* fg = knob("FPM_FORCE_GENERIC");
   const bool force_gen = fg && fg[0] == '1';
   if (force_gen) return {FK_GEN, FK_GEN, FK_GEN};
   int w = classify(p.work), mv = classify(p.matvec), ip = classify(p.inner);
@@ -281,6 +319,32 @@ static int mv_bytes(int kind) {
 
 static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
+// The host-buffer pipeline's staging pool: one per device, created once
+// (thread-safe), release threshold "keep everything".  Library-private, so
+// the process's default pool settings are untouched.
+static cudaMemPool_t staging_pool() {
+  constexpr int kMaxDev = 64;
+  static std::once_flag once[kMaxDev];
+  static cudaMemPool_t pools[kMaxDev];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev) return nullptr;
+  std::call_once(once[dev], [dev] {
+    cudaMemPoolProps props;
+    std::memset(&props, 0, sizeof(props));
+    props.allocType = cudaMemAllocationTypePinned;
+    props.handleTypes = cudaMemHandleTypeNone;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    cudaMemPool_t p = nullptr;
+    if (cudaMemPoolCreate(&p, &props) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &keep);
+      pools[dev] = p;
+    }
+  });
+  return pools[dev];
+}
+
 static int max_smem_optin() {  // per call: re-entrant, follows the caller's current device
   int dev = 0, v = 0;
   cudaGetDevice(&dev);
@@ -291,7 +355,7 @@ static int max_smem_optin() {  // per call: re-entrant, follows the caller's cur
 
 // Gram geometry for a given R: fills G and the union/ys sizes.
 static int env_int(const char* name, int dflt) {
-  const char* v = std::getenv(name);
+  const char* v = knob(name);
   return (v && *v) ? std::atoi(v) : dflt;
 }
 
@@ -411,7 +475,7 @@ static int sm_count() {
 // per group with uniform Gram warps, gt Gram threads + ct CG threads <= 512.
 static bool plan_detect_ws(int M, int N, int L, int bj, int iters, int mvk, int ipk, DetectArgs& a, WsLayout& sl,
                            int& grid) {
-  if (std::getenv("FPM_NO_WS")) return false;
+  if (knob("FPM_NO_WS")) return false;
   const int Np = (N + 7) / 8 * 8, nb = Np / 4, Cc = nb * (nb / 2 - 1);
   const int limit = max_smem_optin();
   // the CG group takes the threads left of a 512-thread block (rows beyond
@@ -496,7 +560,8 @@ static bool plan_detect_ws(int M, int N, int L, int bj, int iters, int mvk, int 
           // against the full 224: c3 +1.9 %, c1 +1.3 %, c5 fp64 +0.6 %, c5 fp16
           // +-0, c2 (N = 32) -1.8 %
           const int ct_def = (ncg == 1 && gt == 256 && N != 32) ? 192 : cg_threads(R, gt);
-          a.ws_ct = env_int("FPM_WS_CT", ct_def);
+          // FPM_WS_CT override: whole warps, at least two, within the 512-thread block
+          a.ws_ct = std::min(std::max(env_int("FPM_WS_CT", ct_def) / 32 * 32, 64), 512 - gt - 32);
           a.ws_ncg = ncg;
           a.ws_ct0 = ncg == 2 ? 128 : a.ws_ct;
           a.ws_nslot = nslot;
@@ -556,7 +621,7 @@ static int launch_detect(const Kinds& k, const DetectArgs& a, int threads, cudaS
   int nb, lb;
   pick_spec(a.G.N, a.L, a.bj, nb, lb);
   if (a.G.N != a.G.Np) nb = 0;
-  if (std::getenv("FPM_NO_SPEC")) nb = lb = 0;
+  if (knob("FPM_NO_SPEC")) nb = lb = 0;
   note_kernel("fpm_detect_kernel", k, nb, lb);
   if (k.w == FK_GEN) return launch_detect_gen_w(a, threads, 0, 0, st);
   switch (k.mv) {
@@ -573,7 +638,7 @@ static int launch_detect_ws(const Kinds& k, const DetectArgs& a, const WsLayout&
   pick_spec(a.G.N, a.L, a.bj, nb, lb);
   if (a.gram_A && nb == 16) lb = 4;  // Gram-only: any LB; take the N = 64 specialisation
   if (a.G.N != a.G.Np) nb = 0;
-  if (std::getenv("FPM_NO_SPEC")) nb = lb = 0;
+  if (knob("FPM_NO_SPEC")) nb = lb = 0;
   note_kernel("fpm_detect_ws_kernel", k, nb, lb);
   if (k.w == FK_GEN) return launch_detect_ws_gen_w(a, sl, grid, 0, 0, st);
   switch (k.mv) {
@@ -586,7 +651,7 @@ static int launch_detect_ws(const Kinds& k, const DetectArgs& a, const WsLayout&
 }
 
 static int launch_cg(const Kinds& k, const CgArgs& a, int smem, cudaStream_t st) {
-  const int lb = (a.bj && a.N % a.L == 0 && !std::getenv("FPM_NO_SPEC")) ? a.L : 0;
+  const int lb = (a.bj && a.N % a.L == 0 && !knob("FPM_NO_SPEC")) ? a.L : 0;
   note_kernel("fpm_cg_kernel", k, a.N == 64 ? 16 : 0, lb);
   if (k.w == FK_GEN) return launch_cg_gen_w(a, smem, 0, st);
   switch (k.mv) {
@@ -647,8 +712,13 @@ int64_t fpm_launch_count(void) { return (int64_t)g_launches.load(); }
 const char* fpm_last_kernel(void) { return g_last_kernel; }
 
 int fpm_debug_set_trace(int64_t* dev_buf) {
+#ifdef FPM_DIAG
   g_trace = reinterpret_cast<long long*>(dev_buf);
   return FPM_OK;
+#else
+  (void)dev_buf;
+  return FPM_EUNSUPPORTED;  // product build: no trace state (diagnostic builds: -DFPM_DIAG)
+#endif
 }
 
 int fpm_probe_fp64(int64_t iters, double* dp_ops_per_s) {
@@ -704,7 +774,7 @@ int fpm_gram(const double* H, const double* y, int64_t T, int32_t M, int32_t N, 
     d.sl = make_slicer(16);
     WsLayout sl;
     int grid = 0;
-    if (!std::getenv("FPM_GRAM_LEGACY") && plan_detect_ws(M, N, 1, 0, 1, FK_F16, FK_F16, d, sl, grid)) {
+    if (!knob("FPM_GRAM_LEGACY") && plan_detect_ws(M, N, 1, 0, 1, FK_F16, FK_F16, d, sl, grid)) {
       const Kinds k = {FK_F64, FK_F16, FK_F16};
       return launch_detect_ws(k, d, sl, grid, (cudaStream_t)stream);
     }
@@ -824,8 +894,8 @@ int fpm_cg_ex(const double* A, const double* b, const double* Minv, int64_t T, i
   cudaStream_t st = (cudaStream_t)stream;
   // warp-per-realization fast path (fpm_cgw.cu): fp64 work, native u_MV == u_IP;
   // FPM_NO_CGW forces fpm_cg_kernel (A/B and parity tests)
-  if (k.w == FK_F64 && k.mv == k.ip && k.mv != FK_GEN && !std::getenv("FPM_NO_CGW") &&
-      !std::getenv("FPM_FORCE_GENERIC") && (!bj || N % L == 0)) {
+  if (k.w == FK_F64 && k.mv == k.ip && k.mv != FK_GEN && !knob("FPM_NO_CGW") &&
+      !knob("FPM_FORCE_GENERIC") && (!bj || N % L == 0)) {
     const int rw = launch_cgw(k.mv, a, st);
     if (rw != FPM_EUNSUPPORTED) {
       std::snprintf(g_last_kernel, sizeof(g_last_kernel), "fpm_cgw_kernel<mv=%s,N=%d,L=%d>", kind_name(k.mv), N,
@@ -939,7 +1009,11 @@ static int detect_args(const double* H, const double* y, const uint8_t* tx_bits,
   a.sl = make_slicer(qam);
   a.trace = g_trace;
   a.tl = pick_tl(N);
-  a.debug = env_int("FPM_DEBUG", 0);
+#ifdef FPM_DIAG
+  a.debug = env_int("FPM_DEBUG", 0);  // diagnostic builds only (tools/): skip bits for attribution
+#else
+  a.debug = 0;
+#endif
   k = pick_kinds(*pp);
   a.gram32 = gram32;
   if (algorithm == FPM_ALG_LMMSE) {  // Gram + Cholesky kernels, no fused plan
@@ -953,7 +1027,7 @@ static int detect_args(const double* H, const double* y, const uint8_t* tx_bits,
   }
   // A/B knob: force the composed path (measured at c5: fp64 3.76 M vs fused
   // 3.79 M det/s, fp16 4.77 M vs 6.10 M)
-  if (std::getenv("FPM_COMPOSED")) {
+  if (knob("FPM_COMPOSED")) {
     a.G.R = 1;
     a.composed = 1;
     return FPM_OK;
@@ -1108,21 +1182,15 @@ int fpm_detect_host(const double* H, const double* y, const uint8_t* tx_bits, in
   const size_t per = align_up(hB, 256) + align_up(yB, 256) + align_up(tB, 256) + align_up(tB, 256) +
                      align_up(xB, 256) + 2 * align_up(fB, 256) + (bj && Minv_in ? align_up(mB, 256) : 0);
   rc = FPM_OK;
-  // stream-ordered allocations from the device's default pool, kept cached
-  // between calls (cudaMalloc / cudaFree of ~1 GB staging per call cost more
-  // than the transfers they stage)
-  {
-    int dev = 0;
-    cudaMemPool_t pool;
-    cudaGetDevice(&dev);
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t keep = UINT64_MAX;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-    }
-  }
+  // stream-ordered staging from the library's own per-device pool, which
+  // keeps its memory between calls (cudaMalloc / cudaFree of ~1 GB staging
+  // per call cost more than the transfers they stage); the process's default
+  // pool is left as the caller configured it
+  cudaMemPool_t pool = staging_pool();
+  if (!pool) return FPM_ECUDA;
   for (int s = 0; s < 2; ++s) {
     if (cudaStreamCreateWithFlags(&st[s], cudaStreamNonBlocking) != cudaSuccess) return FPM_ECUDA;
-    if (cudaMallocAsync(&buf[s], per, st[s]) != cudaSuccess) rc = FPM_ECUDA;
+    if (cudaMallocFromPoolAsync(&buf[s], per, pool, st[s]) != cudaSuccess) rc = FPM_ECUDA;
   }
   // Outputs: straight to the caller's buffers per chunk when they are pinned;
   // otherwise (pageable NumPy arrays) a copy into pageable memory would block
@@ -1140,13 +1208,14 @@ int fpm_detect_host(const double* H, const double* y, const uint8_t* tx_bits, in
   unsigned char* obuf = nullptr;
   const size_t oxB = (size_t)T * N * 16, ofB = (size_t)T * 4, orB = rx_bits ? (size_t)T * bps * N : 0;
   if (!rc && !direct &&
-      cudaMallocAsync(&obuf, align_up(oxB, 256) + 2 * align_up(ofB, 256) + align_up(orB, 256), st[0]) != cudaSuccess)
+      cudaMallocFromPoolAsync(&obuf, align_up(oxB, 256) + 2 * align_up(ofB, 256) + align_up(orB, 256), pool, st[0]) !=
+          cudaSuccess)
     rc = FPM_ECUDA;
   double* ox = (double*)obuf;
   int32_t* obk = obuf ? (int32_t*)(obuf + align_up(oxB, 256)) : nullptr;
   int32_t* odv = obuf ? (int32_t*)(obuf + align_up(oxB, 256) + align_up(ofB, 256)) : nullptr;
   uint8_t* orx = obuf ? obuf + align_up(oxB, 256) + 2 * align_up(ofB, 256) : nullptr;
-  if (!rc && cudaMallocAsync(&dcnt, 2 * FPM_NCOUNTERS * sizeof(int64_t), st[0]) != cudaSuccess) rc = FPM_ECUDA;
+  if (!rc && cudaMallocFromPoolAsync(&dcnt, 2 * FPM_NCOUNTERS * sizeof(int64_t), pool, st[0]) != cudaSuccess) rc = FPM_ECUDA;
   if (!rc) cudaMemsetAsync(dcnt, 0, 2 * FPM_NCOUNTERS * sizeof(int64_t), st[0]);
   if (!rc) {  // stream 1 must see the zeroed counters and its buffer
     cudaEvent_t ev;
@@ -1210,10 +1279,12 @@ int fpm_detect_host(const double* H, const double* y, const uint8_t* tx_bits, in
     }
   }
   int64_t hc[2 * FPM_NCOUNTERS] = {0};
+  // both streams drain before anything is read or freed, whatever rc is: a
+  // launch that failed mid-loop may leave earlier chunks still writing
+  for (int s = 0; s < 2; ++s)
+    if (cudaStreamSynchronize(st[s]) != cudaSuccess) rc = FPM_ECUDA;
   if (!rc) {
-    for (int s = 0; s < 2; ++s)
-      if (cudaStreamSynchronize(st[s]) != cudaSuccess) rc = FPM_ECUDA;
-    if (!rc && cudaMemcpy(hc, dcnt, sizeof(hc), cudaMemcpyDeviceToHost) != cudaSuccess) rc = FPM_ECUDA;
+    if (cudaMemcpy(hc, dcnt, sizeof(hc), cudaMemcpyDeviceToHost) != cudaSuccess) rc = FPM_ECUDA;
     if (!rc && obuf) {
       if (cudaMemcpy(x, ox, oxB, cudaMemcpyDeviceToHost) != cudaSuccess ||
           cudaMemcpy(breakdown_at, obk, ofB, cudaMemcpyDeviceToHost) != cudaSuccess ||

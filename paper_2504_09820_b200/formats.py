@@ -23,6 +23,8 @@ class FloatFormat:
     exp_bits: int
     subnormals_enabled: bool = True
     unit_roundoff: float = field(init=False, compare=False)
+    x_min: float = field(init=False, compare=False)   # smallest positive normal, 2**(1 - bias)
+    x_max: float = field(init=False, compare=False)   # largest finite, (2 - 2**(1 - sig)) * 2**bias
 
     def __post_init__(self):
         if self.sig_bits < 2 or self.exp_bits < 2:
@@ -30,6 +32,9 @@ class FloatFormat:
         if self.sig_bits > 53 or self.exp_bits > 11:
             raise FormatError(f"({self.sig_bits}, {self.exp_bits}) exceeds the binary64 substrate (53, 11)")
         object.__setattr__(self, "unit_roundoff", 2.0 ** (-self.sig_bits))
+        bias = (1 << (self.exp_bits - 1)) - 1
+        object.__setattr__(self, "x_min", 2.0 ** (1 - bias))
+        object.__setattr__(self, "x_max", (2.0 - 2.0 ** (1 - self.sig_bits)) * 2.0 ** bias)
 
     @property
     def is_native(self) -> bool:

@@ -97,7 +97,21 @@ def sharded_detect(det, H, y, sigma2, tx_bits, *, counts_fn=None, device=None) -
     if hi > lo:
         (counts_fn or _gpu_counts)(det, batch, cnt)
     allreduce_counters(cnt)
-    return {k: int(v) for k, v in zip(_lib.COUNTERS, cnt.cpu().tolist())}
+    out = {k: int(v) for k, v in zip(_lib.COUNTERS, cnt.cpu().tolist())}
+    _raise_on_nonpd(np.asarray([out[k] for k in _lib.COUNTERS]))
+    return out
+
+
+def _raise_on_nonpd(c) -> None:
+    """build_blocks_batch raises ContractViolation on a non-PD diagonal block
+    (solvers.py:246-249).  Callers that pass their own counter rows (every
+    sharded path) see the 'nonpd' counter only here, after the all-reduce, so
+    every rank raises together instead of counting frozen x = 0 lanes as
+    ordinary bit errors."""
+    c = np.asarray(c)
+    nonpd = c[..., _lib.COUNTERS.index("nonpd")]
+    if int(np.sum(nonpd)):
+        raise ContractViolation(f"non-PD diagonal block in {int(np.sum(nonpd))} block(s)")
 
 
 def wilson_interval(errors: int, n: int, z: float = 1.96) -> tuple[float, float]:
@@ -165,6 +179,7 @@ def sharded_ber_sweep(cfg, simulate, *, counts_fn=None, device=None) -> list:
             done += n
         allreduce_counters(cnt)
         c = cnt.cpu().numpy()
+        _raise_on_nonpd(c)
         be, dv = _lib.COUNTERS.index("bit_errors"), _lib.COUNTERS.index("diverged")
         total_bits = cfg.trials * bits_per_trial
         for di, curve in enumerate(curves):

@@ -7,7 +7,9 @@ infrastructure and is imported only from tests.
 
 import glob
 import os
+import subprocess
 import sys
+import tempfile
 
 import numpy as np
 import pytest
@@ -51,3 +53,33 @@ def bits_equal(a, b):
 def oracle():
     import fpm_oracle
     return fpm_oracle
+
+
+# The library reads its FPM_* planner knobs ONCE, when it loads (no per-call
+# getenv).  Tests that force another kernel path (FPM_NO_WS, FPM_NO_CGW,
+# FPM_FORCE_GENERIC, FPM_CGW_TMEM) therefore run that half in a fresh
+# interpreter: the parent calls run_knob_child(nodeid, knobs), the child test
+# (decorated @knob_child) runs only there and may hand arrays back through
+# save_child_out(**arrays).
+IN_CHILD = os.environ.get("FPM_TEST_CHILD") == "1"
+knob_child = pytest.mark.skipif(not IN_CHILD, reason="child half of a knob test (runs in a fresh process)")
+
+
+def run_knob_child(nodeid: str, knobs: dict, timeout: int = 900) -> dict:
+    env = dict(os.environ)
+    env.update(knobs)
+    env["FPM_TEST_CHILD"] = "1"
+    with tempfile.TemporaryDirectory() as d:
+        out = os.path.join(d, "out.npz")
+        env["FPM_TEST_CHILD_OUT"] = out
+        r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-p", "no:cacheprovider", nodeid],
+                           cwd=ROOT, env=env, capture_output=True, text=True, timeout=timeout)
+        assert r.returncode == 0 and " passed" in r.stdout, (nodeid, knobs, r.stdout[-4000:], r.stderr[-2000:])
+        if not os.path.exists(out):
+            return {}
+        with np.load(out, allow_pickle=False) as z:
+            return {k: z[k] for k in z.files}
+
+
+def save_child_out(**arrays) -> None:
+    np.savez(os.environ["FPM_TEST_CHILD_OUT"], **arrays)

@@ -111,3 +111,42 @@ def test_format_registry_matches_reference_names():
     reg = registered_formats()
     assert {k: v.triple() for k, v in reg.items()} == {
         "bfloat16": (8, 8, 1), "fp16": (11, 5, 1), "fp32": (24, 8, 1), "fp64": (53, 11, 1)}
+
+
+def test_product_library_has_no_trace_state(lib):
+    """Diagnostics are compile-time only (-DFPM_DIAG): the product library
+    refuses a trace buffer instead of keeping global state."""
+    from paper_2504_09820_b200 import _lib
+    assert lib.fpm_debug_set_trace(ctypes.c_void_p(256)) == _lib.FPM_EUNSUPPORTED
+    assert lib.fpm_debug_set_trace(None) == _lib.FPM_EUNSUPPORTED
+
+
+def test_no_per_call_getenv_in_library_sources():
+    """Planner knobs come from the load-time snapshot (fpm_host.cu knob()),
+    never from a per-call getenv."""
+    import glob
+    srcs = glob.glob(os.path.join(ROOT, "paper_2504_09820_b200", "csrc", "*.cu*"))
+    hits = [(p, i) for p in srcs for i, line in enumerate(open(p), 1) if "getenv(" in line]
+    assert not hits, hits
+
+
+def test_build_stamp_tracks_flags(monkeypatch):
+    """The build stamp covers the nvcc flags, so a prebuilt library compiled
+    with other flags (or from other sources) is rebuilt, not reused."""
+    from paper_2504_09820_b200 import build as B
+    B.build()
+    assert not B.needs_build()
+    s0 = B._stamp()
+    monkeypatch.setattr(B, "FLAGS", B.FLAGS + ["-DFPM_SOMETHING_ELSE"])
+    assert B._stamp() != s0 and B.needs_build()
+
+
+def test_format_extremes_match_reference_definition():
+    """FloatFormat.x_min / x_max (formats.py:60-61, 83-88)."""
+    from paper_2504_09820_b200.formats import BFLOAT16, FP16, FP32, FP64, make_format
+    assert FP16.x_max == 65504.0 and FP16.x_min == 2.0 ** -14
+    assert BFLOAT16.x_max == float.fromhex("0x1.fep+127") and BFLOAT16.x_min == 2.0 ** -126
+    assert FP32.x_max == float.fromhex("0x1.fffffep+127") and FP32.x_min == 2.0 ** -126
+    assert FP64.x_max == float.fromhex("0x1.fffffffffffffp+1023") and FP64.x_min == 2.0 ** -1022
+    f = make_format(5, 4)
+    assert f.x_max == (2 - 2 ** -4) * 2 ** 7 and f.x_min == 2.0 ** -6

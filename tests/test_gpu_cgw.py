@@ -10,7 +10,7 @@ import ctypes
 import numpy as np
 import pytest
 
-from conftest import bits_equal
+from conftest import bits_equal, knob_child, run_knob_child, save_child_out
 
 pytestmark = pytest.mark.gpu
 
@@ -97,11 +97,7 @@ def test_cgw_freeze_flags(oracle, fmt):
         np.testing.assert_array_equal(div, ref.diverged_at)
 
 
-@pytest.mark.parametrize("fmt,L", [("fp16", 4), ("bfloat16", 0), ("fp64", 4), ("fp32", 2)])
-def test_cgw_equals_lockstep_kernel_at_scale(oracle, monkeypatch, fmt, L):
-    """The warp kernel and the CTA-lockstep kernel (FPM_NO_CGW) give the same
-    bits on a 4096-realization c5-shaped batch."""
-    O = oracle
+def _lockstep_case(fmt, L):
     N, T = 64, 4096
     rng = np.random.default_rng(7)
     Hh = (rng.standard_normal((T, 128, N)) + 1j * rng.standard_normal((T, 128, N))) / np.sqrt(256)
@@ -111,24 +107,45 @@ def test_cgw_equals_lockstep_kernel_at_scale(oracle, monkeypatch, fmt, L):
     from paper_2504_09820_b200.solvers import build_blocks_batch
     A, b = gram_mf(Hh, y, 0.005)
     minv = build_blocks_batch(A, L).packed if L else None
-    x1, b1, d1, k1 = _cg_capi(A, b, minv, L, 8, fmt, "as_written")
-    monkeypatch.setenv("FPM_NO_CGW", "1")
-    x2, b2, d2, k2 = _cg_capi(A, b, minv, L, 8, fmt, "as_written")
-    assert k1.startswith("fpm_cgw_kernel") and not k2.startswith("fpm_cgw_kernel"), (k1, k2)
-    assert bits_equal(x1, x2)
-    np.testing.assert_array_equal(b1, b2)
-    np.testing.assert_array_equal(d1, d2)
+    return _cg_capi(A, b, minv, L, 8, fmt, "as_written")
+
+
+LOCKSTEP_CASES = [("fp16", 4), ("bfloat16", 0), ("fp64", 4), ("fp32", 2)]
+
+
+@pytest.mark.parametrize("fmt,L", LOCKSTEP_CASES)
+def test_cgw_equals_lockstep_kernel_at_scale(fmt, L):
+    """The warp kernel and the CTA-lockstep kernel (knob FPM_NO_CGW, in a fresh
+    process) give the same bits on a 4096-realization c5-shaped batch."""
+    x1, b1, d1, k1 = _lockstep_case(fmt, L)
+    o = run_knob_child(f"tests/test_gpu_cgw.py::test_child_lockstep[{fmt}-{L}]", {"FPM_NO_CGW": "1"})
+    assert k1.startswith("fpm_cgw_kernel") and not str(o["k"]).startswith("fpm_cgw_kernel"), (k1, o["k"])
+    assert bits_equal(x1, o["x"])
+    np.testing.assert_array_equal(b1, o["b"])
+    np.testing.assert_array_equal(d1, o["d"])
+
+
+@knob_child
+@pytest.mark.parametrize("fmt,L", LOCKSTEP_CASES)
+def test_child_lockstep(fmt, L):
+    x, b, d, k = _lockstep_case(fmt, L)
+    save_child_out(x=x, b=b, d=d, k=np.array(k))
 
 
 @pytest.mark.parametrize("fmt", ["fp16", "bfloat16"])
-def test_cgw_tmem_variant_matches_oracle(oracle, monkeypatch, fmt):
-    """The opt-in TMEM variant (FPM_CGW_TMEM=1: A in tensor memory, four
+def test_cgw_tmem_variant_matches_oracle(fmt):
+    """The opt-in TMEM variant (knob FPM_CGW_TMEM=1: A in tensor memory, four
     warps per CTA) gives the oracle's bits, including a partial last CTA."""
+    run_knob_child(f"tests/test_gpu_cgw.py::test_child_tmem[{fmt}]", {"FPM_CGW_TMEM": "1"})
+
+
+@knob_child
+@pytest.mark.parametrize("fmt", ["fp16", "bfloat16"])
+def test_child_tmem(oracle, fmt):
     O = oracle
     T, N = 7, 64
     A, b = _system(O, 128, N, T, 77)
     of = O.REGISTRY[fmt]
-    monkeypatch.setenv("FPM_CGW_TMEM", "1")
     for L in (0, 4):
         mats = O.bj_inverses(A, L) if L else None
         for rv in (("as_written", "textbook") if L else ("as_written",)):

@@ -15,7 +15,7 @@ import os
 import numpy as np
 import pytest
 
-from conftest import bits_equal, golden_cases, load_golden
+from conftest import bits_equal, golden_cases, knob_child, load_golden, run_knob_child, save_child_out
 
 pytestmark = pytest.mark.gpu
 
@@ -111,17 +111,21 @@ def test_block_inverses_close_to_lapack(name):
     np.testing.assert_allclose(bb.packed, g["Minv"], rtol=1e-11, atol=1e-13)
 
 
-def test_generic_emulation_path_matches_native(monkeypatch):
-    """The integer RNE emulation kernels (any (sig, exp)) must reproduce the
-    native fp16/bf16/fp32 kernels bit for bit."""
+def test_generic_emulation_path_matches_native():
+    """The integer RNE emulation kernels (any (sig, exp); knob
+    FPM_FORCE_GENERIC in a fresh process) reproduce the reference's bits,
+    i.e. what the native fp16/bf16/fp32 kernels give (test_golden_*)."""
+    run_knob_child("tests/test_gpu_parity.py::test_child_generic_emulation", {"FPM_FORCE_GENERIC": "1"})
+
+
+@knob_child
+def test_child_generic_emulation():
     from paper_2504_09820_b200.detect import detect
     for name in ("c2_fpcg_fp16_snr0", "c2_fpcg_bf16_snr10", "c5_bj4_textbook_fp32", "mix_w16_all_bj4",
                  "mix_w32_mv16_ip16"):
         g = load_golden(name)
         det = _spec_from_golden(g)
-        monkeypatch.setenv("FPM_FORCE_GENERIC", "1")
         res = detect(det, g["H"], g["y"], float(g["sigma2"]), g["tx_bits"], minv=g.get("Minv"))
-        monkeypatch.delenv("FPM_FORCE_GENERIC")
         assert bits_equal(res.x, g["x"]), name
 
 
@@ -269,12 +273,27 @@ def test_persistent_kernel_multi_group_and_partial_group():
     np.testing.assert_array_equal(res.bits, ob)
     assert res.counters["bit_errors"] == int(O.bit_errors(ob, bits).sum())
     assert res.counters["trials"] == T
-    os.environ["FPM_NO_WS"] = "1"
-    try:
-        res2 = detect(det, H, y, s2, bits, minv=mats)
-    finally:
-        del os.environ["FPM_NO_WS"]
-    assert bits_equal(res2.x, ref.x)
+    assert "fpm_detect_ws_kernel" in _lib_last_kernel()
+    o = run_knob_child("tests/test_gpu_parity.py::test_child_multi_group_fallback", {"FPM_NO_WS": "1"})
+    assert "fpm_detect_ws_kernel" not in str(o["k"])
+    assert bits_equal(o["x"], ref.x)
+
+
+def _lib_last_kernel():
+    from paper_2504_09820_b200 import _lib
+    return _lib.load().fpm_last_kernel().decode()
+
+
+@knob_child
+def test_child_multi_group_fallback():
+    import fpm_oracle as O
+    from paper_2504_09820_b200.detect import DetectorSpec, detect
+    T = 148 * 2 * 3 + 1
+    H, y, bits, s2 = _oracle_inputs(128, 64, 0.5, 15.0, T)
+    det = DetectorSpec("fp_bj_cg", iters=8, L=4, matvec="fp16", inner="fp16")
+    A, b = O.gram_mf_einsum(H, y, s2)
+    res2 = detect(det, H, y, s2, bits, minv=O.bj_inverses(A, 4))
+    save_child_out(x=res2.x, k=np.array(_lib_last_kernel()))
 
 
 HIST_EXACT = ("x", "breakdown_at", "diverged_at", "alphas", "betas", "converged_at", "iterates", "residual_vectors")
@@ -398,26 +417,37 @@ def test_lmmse_non_pd_raises():
         solve_direct_batch(A, np.ones((2, 4), np.complex128))
 
 
-@pytest.mark.parametrize("M,N", [(16, 8), (24, 8), (32, 16), (64, 32)])
-def test_small_n_all_paths_against_oracle(oracle, M, N, monkeypatch):
-    """Small N (more matched-filter chains than Gram jobs) through the
-    persistent kernel, the fallback fused kernel and the standalone Gram,
-    plain CG fp64 and FP-CG fp16, against the oracle bit for bit."""
+SMALL_N = [(16, 8), (24, 8), (32, 16), (64, 32)]
+
+
+def _small_n_case(O, M, N, tag):
     from paper_2504_09820_b200.detect import DetectorSpec, detect, gram_mf
-    O = oracle
     T = 40
     H, y, bits, s2 = O.simulate(M, N, 0.5, 4.0, range(T), 11)
     A, b = O.gram_mf(H, y, s2)
     Ag, bg = gram_mf(H, y, s2)
     assert bits_equal(Ag, A) and bits_equal(bg, b)
-    for no_ws in (False, True):
-        if no_ws:
-            monkeypatch.setenv("FPM_NO_WS", "1")
-        for alg, mv in (("cg", O.FP64), ("fp_cg", O.FP16)):
-            det = DetectorSpec(alg, iters=4, **({} if alg == "cg" else dict(matvec="fp16", inner="fp16")))
-            r = detect(det, H, y, s2, bits)
-            _, _, _, out = O.detect(H, y, s2, alg, 4, None, O.FP64, mv, mv)
-            assert bits_equal(r.x, out.x), (alg, no_ws)
+    for alg, mv in (("cg", O.FP64), ("fp_cg", O.FP16)):
+        det = DetectorSpec(alg, iters=4, **({} if alg == "cg" else dict(matvec="fp16", inner="fp16")))
+        r = detect(det, H, y, s2, bits)
+        _, _, _, out = O.detect(H, y, s2, alg, 4, None, O.FP64, mv, mv)
+        assert bits_equal(r.x, out.x), (alg, tag)
+
+
+@pytest.mark.parametrize("M,N", SMALL_N)
+def test_small_n_all_paths_against_oracle(oracle, M, N):
+    """Small N (more matched-filter chains than Gram jobs) through the
+    persistent kernel, the fallback fused kernel (knob FPM_NO_WS, fresh
+    process) and the standalone Gram, plain CG fp64 and FP-CG fp16, against
+    the oracle bit for bit."""
+    _small_n_case(oracle, M, N, "ws")
+    run_knob_child(f"tests/test_gpu_parity.py::test_child_small_n_fallback[{M}-{N}]", {"FPM_NO_WS": "1"})
+
+
+@knob_child
+@pytest.mark.parametrize("M,N", SMALL_N)
+def test_child_small_n_fallback(oracle, M, N):
+    _small_n_case(oracle, M, N, "fallback")
 
 
 SHAPES = [  # (M, N, L) -- N multiples of 4 and not, L dividing N; every kernel geometry

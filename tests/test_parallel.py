@@ -166,3 +166,23 @@ def test_gpu_generated_sweep_is_chunk_invariant():
     for ca, cb in zip(a, b):
         for pa, pb in zip(ca.points, cb.points):
             assert (pa.bit_errors, pa.divergence_rate) == (pb.bit_errors, pb.divergence_rate)
+
+
+def test_sharded_sweep_raises_on_nonpd_block():
+    """A non-PD diagonal block surfaces as ContractViolation on the sharded
+    path too (build_blocks_batch, solvers.py:246-249), not as bit errors of
+    frozen lanes: the check runs on the all-reduced counters."""
+    import torch
+    from paper_2504_09820_b200 import _lib
+    from paper_2504_09820_b200.errors import ContractViolation
+
+    def bad_counts(det, batch, cnt):
+        _oracle_counts(det, batch, cnt)
+        if det.algorithm == "fp_bj_cg":
+            cnt[_lib.COUNTERS.index("nonpd")] += 1
+
+    with pytest.raises(ContractViolation):
+        P.sharded_ber_sweep(_cfg(5, 5), _simulate, counts_fn=bad_counts, device=torch.device("cpu"))
+    H, y, bits, s2 = O.simulate(M, N, 0.5, 4.0, range(3), 3)
+    with pytest.raises(ContractViolation):
+        P.sharded_detect(_cfg().detectors[1], H, y, s2, bits, counts_fn=bad_counts, device=torch.device("cpu"))
