@@ -319,7 +319,7 @@ static int mv_bytes(int kind) {
 
 static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
-// The host-buffer pipeline's staging pool: one per device, created once
+// Scratch and staging pool: one per device, created once
 // (thread-safe), release threshold "keep everything".  Library-private, so
 // the process's default pool settings are untouched.
 static cudaMemPool_t staging_pool() {
@@ -343,6 +343,17 @@ static cudaMemPool_t staging_pool() {
     }
   });
   return pools[dev];
+}
+
+// stream-ordered scratch from the library pool (falls back to the device's
+// current pool if the private one could not be created)
+template <class Tp>
+static cudaError_t pool_alloc(Tp** p, size_t bytes, cudaStream_t st) {
+  cudaMemPool_t pool = staging_pool();
+  void* v = nullptr;
+  const cudaError_t e = pool ? cudaMallocFromPoolAsync(&v, bytes, pool, st) : cudaMallocAsync(&v, bytes, st);
+  *p = static_cast<Tp*>(v);
+  return e;
 }
 
 static int max_smem_optin() {  // per call: re-entrant, follows the caller's current device
@@ -817,7 +828,7 @@ int fpm_bj_setup(const double* A, int64_t T, int32_t N, int32_t L, int32_t allow
   if (T == 0) return FPM_OK;
   cudaStream_t st = (cudaStream_t)stream;
   unsigned int* d_nonpd = nullptr;
-  if (cudaMallocAsync(&d_nonpd, sizeof(unsigned int), st) != cudaSuccess) return FPM_ECUDA;
+  if (pool_alloc(&d_nonpd, sizeof(unsigned int), st) != cudaSuccess) return FPM_ECUDA;
   cudaMemsetAsync(d_nonpd, 0, sizeof(unsigned int), st);
   if (bad_block) {
     // fill with INT_MAX via memset pattern 0x7f
@@ -912,7 +923,7 @@ int fpm_cg_ex(const double* A, const double* b, const double* Minv, int64_t T, i
     a.a_glob = A;
   } else {
     const long n = T * (long)N * N;
-    if (cudaMallocAsync(&tmp, (size_t)n * 16, st) != cudaSuccess) return FPM_ECUDA;
+    if (pool_alloc(&tmp, (size_t)n * 16, st) != cudaSuccess) return FPM_ECUDA;
     const int rr = launch_round_mv_gen(reinterpret_cast<const double2*>(A), tmp, n, a.pr.mv, st);
     if (rr) {
       cudaFreeAsync(tmp, st);
@@ -1050,8 +1061,8 @@ static int run_lmmse(const DetectArgs& a, int M, int N, cudaStream_t st) {
                 a.gram32 ? "fpm_gram32_kernel" : "fpm_gram_kernel");
   const long chunk = std::min<long>(T, 8192);
   double2 *A = nullptr, *b = nullptr;
-  if (cudaMallocAsync(&A, (size_t)chunk * N * N * 16, st) != cudaSuccess) return FPM_ECUDA;
-  if (cudaMallocAsync(&b, (size_t)chunk * N * 16, st) != cudaSuccess) {
+  if (pool_alloc(&A, (size_t)chunk * N * N * 16, st) != cudaSuccess) return FPM_ECUDA;
+  if (pool_alloc(&b, (size_t)chunk * N * 16, st) != cudaSuccess) {
     cudaFreeAsync(A, st);
     return FPM_ECUDA;
   }
@@ -1086,9 +1097,9 @@ static int run_composed(const DetectArgs& a, int M, int N, int algorithm, int L,
   const long chunk = std::min<long>(T, 2048);
   double2 *A = nullptr, *b = nullptr, *mv = nullptr;
   int rc = FPM_OK;
-  if (cudaMallocAsync(&A, (size_t)chunk * N * N * 16, st) != cudaSuccess ||
-      cudaMallocAsync(&b, (size_t)chunk * N * 16, st) != cudaSuccess ||
-      (bj && !a.minv_in && cudaMallocAsync(&mv, (size_t)chunk * N * L * 16, st) != cudaSuccess))
+  if (pool_alloc(&A, (size_t)chunk * N * N * 16, st) != cudaSuccess ||
+      pool_alloc(&b, (size_t)chunk * N * 16, st) != cudaSuccess ||
+      (bj && !a.minv_in && pool_alloc(&mv, (size_t)chunk * N * L * 16, st) != cudaSuccess))
     rc = FPM_ECUDA;
   for (long c0 = 0; !rc && c0 < T; c0 += chunk) {
     const long n = std::min(chunk, T - c0);
