@@ -17,6 +17,8 @@
  *   fpm_gen_trials  <- the draws of simulate_trials, detect.py:189-214,
  *                      channel.py:138-161, 206-219, rng.py:19-39
  *                      (distribution level, keyed per-trial streams)
+ *   fpm_simulate    <- simulate_trials, detect.py:189-214 (whole link model:
+ *                      colouring, QAM payload, y = H s + n; one kernel)
  *   fpm_gram32      <- EXTENSION: binary32 Gram (BASELINE config c4)
  *   fpm_slice_count <- demodulate_16qam + error sum, detect.py:78-84, :260-262
  *   fpm_detect      <- _detect_batch, detect.py:223-237, fused with the Gram
@@ -174,6 +176,21 @@ int fpm_lmmse(const double* A, const double* b, int64_t T, int32_t N, double* x,
  * reproduced.  context < 2^12, point < 2^16 as in rng.py. */
 int fpm_gen_trials(uint64_t seed, int32_t context, int32_t point, int64_t trial0, int64_t T, int32_t M, int32_t N,
                    int32_t nbits, double* W, uint8_t* bits, double* noise, double* csi, void* stream);
+
+/* The whole link model of simulate_trials (detect.py:189-214) in one kernel,
+ * from the same draws as fpm_gen_trials: H = F_r W F_t^T with F the AR(1)
+ * (Cholesky) factor of the exponential correlation zeta^|i-j| (channel.py:
+ * 101-125; same distribution as the reference's symmetric square roots,
+ * restarting per user block when block_diag_users with n_ue users per
+ * block), Gray QAM symbols of the payload bits (detect.py:54-67; qam 16 or
+ * 64), y = H s + sqrt(sigma2/2) g (detect.py:210-211) and, when csi_var >= 0,
+ * H_est = H + sqrt(csi_var/2) c (channel.py:206-219; csi_var = (1/M)/eps).
+ * Outputs (device, caller-owned): H, H_est (NULL iff csi_var < 0), y, bits
+ * (T, bps*N), symbols (T, N) or NULL.  N <= 128. */
+int fpm_simulate(uint64_t seed, int32_t context, int32_t point, int64_t trial0, int64_t T, int32_t M, int32_t N,
+                 double zeta_r, double zeta_t, int32_t n_ue, int32_t block_diag_users, int32_t qam, double sigma2,
+                 double csi_var, double* H, double* H_est, double* y, uint8_t* bits, double* symbols,
+                 void* stream);
 
 /* qam = 16 (reference) or 64 (extension).  tx_bits / rx_bits: (T, bits*N)
  * uint8 in the reference's layout, both nullable. */

@@ -4,8 +4,9 @@ Restates the reference's simulated link (detect.py:189-214
 `simulate_trials`; channel.py:101-161 `exp_correlation_matrix` /
 `sample_channel`; channel.py:206-219 `perturb_csi`; detect.py:54-67,
 87-93 modulation and noise) with the random draws made on the device by
-`fpm_gen_trials` (per-trial keyed Philox streams) and the Kronecker colouring
-and y = H s + n composed with cuBLAS matmuls.  Every trial's inputs depend
+`fpm_gen_trials` (per-trial keyed Philox streams); `simulate_batch` runs
+the whole link model -- colouring, payload, y = H s + n -- in one kernel
+(`fpm_simulate`).  Every trial's inputs depend
 only on (seed, context, point, trial), so batches, chunks and ranks can be
 generated independently and a sharded sweep sees the same inputs at any GPU
 count.  Parity with the reference generator is distribution-level (its NumPy
@@ -112,32 +113,38 @@ def simulate_batch(M: int, N: int, zeta_r: float, zeta_t: float, snr_db: float, 
                    point: int = 0, context: int = 2, qam: int = 16, epsilon_db: float | None = None,
                    convention: str = "receive_total", N_UE: int = 1, block_diag_users: bool = False, device=None):
     """simulate_trials (detect.py:189-214) on the GPU for trials
-    trial0 .. trial0+T-1: H = sqrt(R_r) W sqrt(R_t), uniform bits ->
-    QAM symbols s, y = H s + CN(0, sigma^2), optional imperfect CSI H_est.
-    Returns the reference's batch dict keys (CUDA tensors; A and b are left
-    to the detector, which builds them bit-exactly from H_est and y)."""
+    trial0 .. trial0+T-1, one fused kernel (fpm_simulate): H coloured by the
+    AR(1) / Cholesky factors of the exponential correlations (the same
+    Kronecker distribution as sqrt(R_r) W sqrt(R_t), channel.py:138-161),
+    uniform bits -> Gray QAM symbols s, y = H s + CN(0, sigma^2), optional
+    imperfect CSI H_est (channel.py:206-219).  Returns the reference's batch
+    dict keys (CUDA tensors; A and b are left to the detector, which builds
+    them bit-exactly from H_est and y)."""
     torch = _torch()
-    W, bits, g, C = gen_trials(seed, point, trial0, T, M, N, context=context, qam=qam,
-                               csi=epsilon_db is not None, device=device)
-    dev = W.device
-    H = W
-    if zeta_r > 0:
-        Sr = torch.as_tensor(matrix_sqrt_psd(exp_correlation_matrix(M, zeta_r)), device=dev)
-        H = torch.matmul(Sr, H)
-    if zeta_t > 0:
-        St = torch.as_tensor(matrix_sqrt_psd(user_correlation_matrix(N, zeta_t, N_UE, block_diag_users)), device=dev)
-        H = torch.matmul(H, St)
-    H = H.contiguous()
-    s = modulate(bits, qam)
+    if not (0.0 <= zeta_r < 1.0 and 0.0 <= zeta_t < 1.0):
+        raise ContractViolation("zeta must lie in [0, 1)")
+    if block_diag_users and N % N_UE:
+        raise ContractViolation("N must be a multiple of N_UE")
+    dev = device or torch.device("cuda")
+    bps = 4 if qam == 16 else 6
     sigma2 = noise_variance(M, N, snr_db, convention)
-    y = torch.einsum("tmn,tn->tm", H, s) + math.sqrt(sigma2 / 2.0) * g
-    H_est = H
+    csi_var = -1.0
     if epsilon_db is not None:  # channel.py:206-219: CN(0, (1/M)/eps) estimate error
         if not math.isfinite(epsilon_db):
             raise ContractViolation("epsilon_db must be finite")
-        var = (1.0 / M) / 10.0 ** (epsilon_db / 10.0)
-        H_est = H + math.sqrt(var / 2.0) * C
-    return {"H": H, "H_est": H_est, "bits": bits, "symbols": s, "y": y.contiguous(), "sigma_n2": sigma2}
+        csi_var = (1.0 / M) / 10.0 ** (epsilon_db / 10.0)
+    H = torch.empty((T, M, N), dtype=torch.complex128, device=dev)
+    H_est = torch.empty_like(H) if csi_var >= 0 else None
+    y = torch.empty((T, M), dtype=torch.complex128, device=dev)
+    bits = torch.empty((T, bps * N), dtype=torch.uint8, device=dev)
+    s = torch.empty((T, N), dtype=torch.complex128, device=dev)
+    rc = _lib.load().fpm_simulate(int(seed) & 0xFFFFFFFFFFFFFFFF, int(context), int(point), int(trial0), int(T),
+                                  int(M), int(N), float(zeta_r), float(zeta_t), int(N_UE) if block_diag_users else 1,
+                                  int(bool(block_diag_users)), int(qam), float(sigma2), float(csi_var),
+                                  H.data_ptr(), None if H_est is None else H_est.data_ptr(), y.data_ptr(),
+                                  bits.data_ptr(), s.data_ptr(), _stream())
+    _lib.check(rc, "simulate")
+    return {"H": H, "H_est": H if H_est is None else H_est, "bits": bits, "symbols": s, "y": y, "sigma_n2": sigma2}
 
 
 def simulate_trials(cfg, snr_idx: int, trial_ids, device=None, qam: int = 16):

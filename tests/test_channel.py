@@ -123,3 +123,61 @@ def test_simulated_ber_matches_oracle_generator_statistically():
     ber_ref = r2.counters["bit_errors"] / (1024 * 4 * N)
     sd = math.sqrt(ber_ref * (1 - ber_ref) / (1024 * 4 * N)) + math.sqrt(ber_gpu * (1 - ber_gpu) / (T * 4 * N))
     assert abs(ber_gpu - ber_ref) < 5 * sd + 1e-3, (ber_gpu, ber_ref)
+
+
+def _ar_factor(n, zeta, n_ue=None):
+    """Lower factor of the AR(1) recursion x_0 = w_0, x_k = zeta x_{k-1} +
+    sqrt(1 - zeta^2) w_k (restarting every n_ue entries when given)."""
+    F = np.zeros((n, n))
+    for k in range(n):
+        start = k == 0 or (n_ue and k % n_ue == 0)
+        if start:
+            F[k, k] = 1.0
+        else:
+            F[k] = zeta * F[k - 1]
+            F[k, k] = math.sqrt(1 - zeta * zeta)
+    return F
+
+
+@pytest.mark.parametrize("zeta,n_ue", [(0.0, None), (0.5, None), (0.8, None), (0.7, 4)])
+def test_ar1_recursion_is_the_cholesky_factor_of_exponential_correlation(zeta, n_ue):
+    """fpm_simulate colours with the AR(1) recursion: it IS the lower
+    Cholesky factor of [R]_ij = zeta^|i-j| (block-diagonal per user block),
+    so F W F^T has the reference's Kronecker distribution."""
+    n = 16
+    R = C.user_correlation_matrix(n, zeta, n_ue or 1, block_diag_users=bool(n_ue)).real
+    F = _ar_factor(n, zeta, n_ue)
+    np.testing.assert_allclose(F @ F.T, R, atol=1e-14)
+    np.testing.assert_allclose(F, np.linalg.cholesky(R), atol=1e-14)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("M,N,zr,zt,qam,bd", [(16, 8, 0.0, 0.0, 16, 0), (32, 64, 0.6, 0.5, 16, 0),
+                                              (24, 128, 0.8, 0.8, 64, 0), (16, 48, 0.3, 0.7, 16, 4),
+                                              (8, 20, 0.5, 0.5, 64, 0)])
+def test_fused_simulate_against_draws(M, N, zr, zt, qam, bd):
+    """fpm_simulate == the AR(1) colouring of fpm_gen_trials' draws, QAM of
+    its bits, y = H s + sqrt(sigma^2/2) g (bit-exact draws / bits, 1e-13 on
+    the coloured values: the kernel uses FMAs and a different sum order)."""
+    _cuda()
+    T, snr, seed = 37, 7.0, 99
+    bps = 4 if qam == 16 else 6
+    b = C.simulate_batch(M, N, zr, zt, snr, 5, T, seed, point=2, qam=qam, N_UE=bd or 1, block_diag_users=bool(bd),
+                         epsilon_db=12.0)
+    W, bits, g, Cn = C.gen_trials(seed, 2, 5, T, M, N, qam=qam, csi=True)
+    assert torch.equal(b["bits"], bits)
+    W, g, Cn = W.cpu().numpy(), g.cpu().numpy(), Cn.cpu().numpy()
+    Fr, Ft = _ar_factor(M, zr), _ar_factor(N, zt, bd or None)
+    H = np.einsum("ij,tjn,kn->tik", Fr, W, Ft)
+    Hg = b["H"].cpu().numpy()
+    if zr == 0 and zt == 0:
+        assert bits_equal(Hg, W)
+    np.testing.assert_allclose(Hg, H, rtol=0, atol=1e-13)
+    s = b["symbols"].cpu().numpy()
+    want_s = O.mod16(bits.cpu().numpy()) if qam == 16 else O.mod64(bits.cpu().numpy())
+    assert bits_equal(s, want_s)
+    s2 = C.noise_variance(M, N, snr)
+    y = np.einsum("tmn,tn->tm", Hg, s) + math.sqrt(s2 / 2) * g
+    np.testing.assert_allclose(b["y"].cpu().numpy(), y, rtol=0, atol=1e-13)
+    var = (1.0 / M) / 10.0 ** 1.2
+    np.testing.assert_allclose(b["H_est"].cpu().numpy(), Hg + math.sqrt(var / 2) * Cn, rtol=0, atol=1e-14)

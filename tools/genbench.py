@@ -1,6 +1,6 @@
 #!/usr/bin/env python
 """Input-generation and LMMSE throughput (dev tool): fpm_gen_trials draws
-and the full channel.simulate_batch composition, per realization, c5 shape."""
+and the fused channel.simulate_batch kernel, per realization, c5 shape."""
 import os
 import sys
 import time
@@ -29,7 +29,8 @@ M, N, T = 128, 64, 32768
 ms = timed(lambda: channel.gen_trials(1, 0, 0, T, M, N))
 print(f"fpm_gen_trials: {T / ms * 1e3 / 1e6:.2f} M realizations/s ({T * M * N * 16 * 2 / (ms / 1e3) / 1e9:.0f} GB/s written)")
 ms = timed(lambda: channel.simulate_batch(M, N, 0.5, 0.5, 15.0, 0, T, 1))
-print(f"simulate_batch (draws + Kronecker ZGEMMs + y): {T / ms * 1e3 / 1e6:.2f} M realizations/s")
+print(f"simulate_batch (fpm_simulate: draws + AR(1) colouring + QAM + y, one kernel): {T / ms * 1e3 / 1e6:.2f} M "
+      f"realizations/s ({T * (M * N * 16 + M * 16 + N * 16 + 4 * N) / (ms / 1e3) / 1e9:.0f} GB/s written)")
 b = channel.simulate_batch(M, N, 0.5, 0.5, 15.0, 0, T, 1)
 A, bb = gram_mf(b["H"], b["y"], b["sigma_n2"])
 ms = timed(lambda: solve_direct_batch(A, bb))
