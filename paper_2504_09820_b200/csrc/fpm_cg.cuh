@@ -30,6 +30,7 @@
 // computed once.
 #pragma once
 #include "fpm_arith.cuh"
+#include "fpm_ptx.cuh"
 
 namespace fpm {
 
@@ -516,6 +517,7 @@ __device__ void cg_group(CgSmem<K>& S, int Rv, int iters, bool bj, bool textbook
       if (tr && tid == 0 && it == 2) tr[77] = clock64() + (S.w[q].x == 1.234e300);
     }
     if (rho_fresh && og >= 0 && ow == 1 && S.fl[og * 4]) S.sc[og * 8 + 3] = csum(S.trho + og * N);
+    diag_jitter(S.dbg, 8, it);
     bar.sync();
     FPM_STAMP(tr, 1 + (it - 1) * 6 + 0);
     // ---- B: phi, flags, alpha ----
@@ -537,6 +539,7 @@ __device__ void cg_group(CgSmem<K>& S, int Rv, int iters, bool bj, bool textbook
       // alphas[i-1] = alpha where active | newly_bad | broke (solvers.py:371)
       if (H && H->al) H->al[h_at(it - 1, g)] = stall ? make_double2(0.0, 0.0) : al;
     }
+    diag_jitter(S.dbg, 9, it);
     bar.sync();
     FPM_STAMP(tr, 1 + (it - 1) * 6 + 1);
     // ---- C: x, r updates (u_W) + finiteness; z = M r and rho1 terms ----
@@ -590,6 +593,7 @@ __device__ void cg_group(CgSmem<K>& S, int Rv, int iters, bool bj, bool textbook
         S.tr1[q] = A::mulc(ipr(S.rn[q]), ipr(zv), fi);
       }
     }
+    diag_jitter(S.dbg, 10, it);
     bar.sync();
     FPM_STAMP(tr, 1 + (it - 1) * 6 + 2);
     // ---- E: rho1, beta, divergence flag ----
@@ -608,6 +612,7 @@ __device__ void cg_group(CgSmem<K>& S, int Rv, int iters, bool bj, bool textbook
         if (H && H->be) H->be[h_at(it - 1, g)] = be;  // betas: where(active, beta, 0)
       }
     }
+    diag_jitter(S.dbg, 11, it);
     bar.sync();
     FPM_STAMP(tr, 1 + (it - 1) * 6 + 3);
     // ---- F: commit x, r; p = (z|r) + beta p ; pmv = rnd(p) ; next rho0 terms ----

@@ -17,6 +17,7 @@
 // hardware barriers: 1 = Gram group, 2 = CG group.
 #pragma once
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 #include "fpm_detect.cuh"
@@ -61,6 +62,11 @@ inline int env_order(int planned) {
   return v ? (std::atoi(v) != 0) : planned;
 }
 
+#ifdef FPM_CHECKED
+__device__ __forceinline__ long stage_elems_of(const GramGeom& G, int Np) { return (long)G.R * G.MC * Np; }
+__device__ __forceinline__ int nsl_of(const DetectArgs& a) { return a.ws_nslot; }
+#endif
+
 // RS > 0: register split (setmaxnreg) for a 512-thread block with gt == 256:
 // the two Gram warp groups run with RS registers per thread, the other two
 // (producer + CG + idle warps) with 256 - RS.
@@ -102,6 +108,23 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const DetectArgs 
   // 1 gram loop end, 2 slot acquired, 3 hand-off done, 4 cg start, 5 cg end
   long long* tr = (diag_trace(args.trace) && blockIdx.x == 0) ? diag_trace(args.trace) : nullptr;
 
+#ifdef FPM_CHECKED
+  if (tid == 0) {  // the planner's shared-memory layout lies inside the launch's dynamic allocation
+    uint32_t dyn;
+    asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+    const long ends[] = {(long)(2 * G.S + 8) * 8 - args.off_union + 256,  // barriers <= 256 B
+                         (long)args.off_union + (long)G.S * stage_elems_of(G, Np) * 16,
+                         (long)args.off_ys + 2L * R * G.M * 16, (long)args.off_slot + (long)nsl_of(args) * sl.bytes,
+                         (long)args.off_bsm + 2L * R * N * 8, (long)args.smem_bytes};
+    const long starts[] = {256, args.off_ys, args.off_slot, args.off_bsm, args.off_minv, (long)dyn};
+    for (int k = 0; k < 6; ++k)
+      if (ends[k] > starts[k]) {
+        printf("FPM_CHECKED: shared-memory region %d ends at %ld > %ld (dyn %u)\n", k, ends[k], starts[k], dyn);
+        __trap();
+      }
+    if (gt + 32 + ct > (int)blockDim.x || (gt & 31) || (ct & 31)) __trap();
+  }
+#endif
   if (tid == 0) {
     for (int s = 0; s < G.S; ++s) {
       mbar_init(&full[s], 1);
@@ -176,6 +199,7 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const DetectArgs 
         const long gc = (long)j * nch + c;
         const int s = (int)(gc % G.S);
         mbar_wait(&full[s], (uint32_t)((gc / G.S) & 1));
+        diag_jitter(args.debug, 2, (int)gc);
         const double2* sb = stages + s * stage_elems;
         const int m0 = c * G.MC;
         const int rows = min(G.MC, G.M - m0);
@@ -328,6 +352,7 @@ FPM_PIPE_UNROLL
             bsm[q] = a;
           }
         }
+        diag_jitter(args.debug, 3, (int)gc);
         __syncwarp();
         if ((tid & 31) == 0) mbar_arrive(&empty[s]);
       }
@@ -362,6 +387,7 @@ FPM_PIPE_UNROLL
       // ---- hand-off: wait until the CG side has released this slot ----
       if (tr && tid == 0 && j < 8) tr[j * 8 + 1] = clock64();
       if (tr && (tid & 31) == 0 && j == 2) tr[72 + tid / 32] = clock64();
+      diag_jitter(args.debug, 4, j);
       if (j >= nsl) mbar_wait(&sempty[slot], (uint32_t)((use - 1) & 1));
       if (tr && tid == 0 && j < 8) tr[j * 8 + 2] = clock64();
       unsigned char* sp = slots + slot * sl.bytes;
@@ -406,6 +432,7 @@ FPM_PIPE_UNROLL
         }
       }
       gbar.sync();
+      diag_jitter(args.debug, 5, j);
       if (tid == 0) {
         mbar_arrive(&sfull[slot]);
         mbar_arrive(&ydone[yb]);  // every Gram warp is past this group's y reads
@@ -448,6 +475,7 @@ FPM_PIPE_UNROLL
           const int jj = (int)(gc / nch);
           FPM_PWAIT(&ydone[jj & 1], (uint32_t)(((jj - 2) >> 1) & 1));
         }
+        diag_jitter(args.debug, 1, (int)gc);
         issue(gc);
       }
     }
@@ -498,6 +526,7 @@ FPM_PIPE_UNROLL
       S.b = reinterpret_cast<double2*>(sp + sl.b);
       double2* dS = reinterpret_cast<double2*>(sp + sl.d);
       FPM_CWAIT(&sfull[slot], (uint32_t)(use & 1));
+      diag_jitter(args.debug, 6, j);
       if (tr && lt == 0 && j < 8) tr[j * 8 + 4] = clock64();
 #pragma unroll 1
       for (int g = lt; g < R; g += ctg) S.fl[g * 4] = g < Rv ? 1 : 0;
@@ -542,6 +571,7 @@ FPM_PIPE_UNROLL
       }
       if (!(diag_bits(args.debug) & 1)) cg_group<WK, K, LB, kCgNC>(S, Rv, args.iters, args.bj != 0, args.textbook != 0, args.pr, ctg, lt, cbar, tc);
       // slot no longer needed (A, b, diagonal blocks consumed)
+      diag_jitter(args.debug, 7, j);
       if (lt == 0) mbar_arrive(&sempty[slot]);
       if (tr && lt == 0 && j < 8) tr[j * 8 + 5] = clock64();
       // slicer + counters + write-back

@@ -1,6 +1,9 @@
 // Thin PTX wrappers: mbarrier + bulk async copy (TMA 1-D, cp.async.bulk).
 #pragma once
 #include <stdint.h>
+#ifdef FPM_CHECKED
+#include <cstdio>
+#endif
 
 namespace fpm {
 
@@ -25,6 +28,31 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
                : "memory");
 }
 
+#ifdef FPM_CHECKED
+// checked builds (tools/, -DFPM_CHECKED): a wait that has not completed
+// after ~10 s of SM clock is a deadlock -- report the barrier and trap
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
+  uint32_t done;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(done)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return done != 0;
+}
+static __device__ __noinline__ void mbar_deadlock(uint64_t* bar, uint32_t parity) {
+  printf("FPM_CHECKED: mbarrier wait timed out (smem 0x%x parity %u) block %d thread %d\n", smem_u32(bar), parity,
+         (int)blockIdx.x, (int)threadIdx.x);
+  __trap();
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const long long t0 = clock64();
+  for (uint32_t k = 0; !mbar_try(bar, parity); ++k)
+    if ((k & 1023) == 1023 && clock64() - t0 > 20000000000LL) mbar_deadlock(bar, parity);
+}
+#else
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n"
@@ -34,11 +62,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+#endif
 
 // wait with a back-off between polls, for warps whose wait is long and not
 // latency-critical (the TMA producer, the CG side waiting for the next slot):
 // their polling would otherwise take issue slots from the Gram warps
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, unsigned ns) {
+#ifdef FPM_CHECKED
+  (void)ns;
+  mbar_wait(bar, parity);
+  return;
+#endif
   uint32_t done = 0;
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
@@ -63,6 +97,11 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, 
 // try, resuming when the phase completes) instead of polling: a waiting warp
 // takes no issue slots from the warps it shares an SM sub-partition with
 __device__ __forceinline__ void mbar_wait_suspend(uint64_t* bar, uint32_t parity, uint32_t hint_ns) {
+#ifdef FPM_CHECKED
+  (void)hint_ns;
+  mbar_wait(bar, parity);
+  return;
+#endif
   asm volatile(
       "{\n\t.reg .pred p;\n"
       "WAITS_%=:\n\t"
@@ -96,4 +135,28 @@ __device__ __forceinline__ void reg_dealloc() {
   asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N));
 }
 
+}  // namespace fpm
+
+namespace fpm {
+// Schedule perturbation for race testing (diagnostic builds, FPM_DEBUG bits
+// 16..31 = seed): a warp sleeps a pseudo-random 0..4 us at a synchronisation
+// site, so a missing barrier or a wrong mbarrier phase changes the results
+// of a run with another seed (tools/sanitize_cases.py --jitter).
+__device__ __forceinline__ void diag_jitter(int dbg, int site, int iter) {
+#ifdef FPM_DIAG
+  const uint32_t seed = (uint32_t)dbg >> 16;
+  if (seed) {
+    uint32_t h = seed * 0x9E3779B9u ^ (uint32_t)blockIdx.x * 0x85EBCA6Bu ^ (uint32_t)(threadIdx.x >> 5) * 0xC2B2AE35u ^
+                 (uint32_t)site * 0x27D4EB2Fu ^ (uint32_t)iter * 0x165667B1u;
+    h ^= h >> 15;
+    h *= 0x2C1B3C6Du;
+    h ^= h >> 12;
+    if ((h & 3) == 0) __nanosleep(h >> 20);  // a quarter of the visits, up to ~4 us
+  }
+#else
+  (void)dbg;
+  (void)site;
+  (void)iter;
+#endif
+}
 }  // namespace fpm

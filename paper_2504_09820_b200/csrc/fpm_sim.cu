@@ -38,7 +38,8 @@
 
 namespace fpm {
 
-constexpr int kSimMaxCpl = 4;  // N <= 128
+constexpr int kSimCplMax = 4;  // N <= 128; kernels for 1, 2, 4 columns per lane
+constexpr int kSimRows = 4;    // antenna rows drawn ahead of their recursions
 
 struct SimArgs {
   uint32_t k0, k1;
@@ -71,7 +72,8 @@ __device__ __forceinline__ void affine_scan(double& A, double2& B, int lane) {
   }
 }
 
-__global__ void __launch_bounds__(256) fpm_sim_kernel(const SimArgs a) {
+template <int kSimMaxCpl>
+__global__ void __launch_bounds__(256, kSimMaxCpl == 4 ? 2 : 3) fpm_sim_kernel(const SimArgs a) {
   const int lane = threadIdx.x & 31;
   const long warp = ((long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const long nwarps = ((long)gridDim.x * blockDim.x) >> 5;
@@ -104,60 +106,78 @@ __global__ void __launch_bounds__(256) fpm_sim_kernel(const SimArgs a) {
     for (int k = 0; k < kSimMaxCpl; ++k) hprev[k] = make_double2(0.0, 0.0);
     double2* Ht = a.H + (long)t * M * N;
     double2* Et = a.Hest ? a.Hest + (long)t * M * N : nullptr;
-    for (int m = 0; m < M; ++m) {
-      // transmit side: x_n = at_n x_{n-1} + ct_n w_n along the users; the
-      // lane folds its segment into (A, B), the warp scans the segments
-      double2 xl[kSimMaxCpl];
-      double A = 1.0;
-      double2 B = make_double2(0.0, 0.0);
+    for (int m0 = 0; m0 < M; m0 += kSimRows) {
+      // draws of kSimRows rows first (independent Philox / Box-Muller chains
+      // in flight together), then the recursions of those rows
+      double2 wv[kSimRows][kSimMaxCpl];
+      double2 gn = make_double2(0.0, 0.0);
 #pragma unroll
-      for (int k = 0; k < kSimMaxCpl; ++k) {
-        const int n = n0 + k;
-        xl[k] = make_double2(0.0, 0.0);
-        if (k < cpl && n < N) {
-          const double2 g = cnormal(a.k0, a.k1, kStreamW, (uint32_t)(m * N + n), trial);
-          const double2 w = make_double2(g.x * a.wscale, g.y * a.wscale);
-          const bool start = (n == 0) || (a.block_diag && n % a.n_ue == 0);
-          const double an = start ? 0.0 : a.zt, cn = start ? 1.0 : a.ct;
-          B = make_double2(fma(an, B.x, cn * w.x), fma(an, B.y, cn * w.y));
-          A *= an;
-          xl[k] = B;  // value with a zero carry-in
-        }
-      }
-      affine_scan(A, B, lane);
-      // carry into this lane = inclusive value of the previous lane
-      double2 cin = make_double2(__shfl_up_sync(0xffffffffu, B.x, 1), __shfl_up_sync(0xffffffffu, B.y, 1));
-      if (lane == 0) cin = make_double2(0.0, 0.0);
-      // receive side: H[m, n] = ar_m H[m-1, n] + cr_m X[m, n]
-      const double ar = m == 0 ? 0.0 : a.zr, crm = m == 0 ? 1.0 : a.cr;
-      double2 acc = make_double2(0.0, 0.0);  // this lane's part of (H s)[m]
-      double mul = 1.0;
+      for (int r = 0; r < kSimRows; ++r)
 #pragma unroll
-      for (int k = 0; k < kSimMaxCpl; ++k) {
-        const int n = n0 + k;
-        if (k < cpl && n < N) {
-          const bool start = (n == 0) || (a.block_diag && n % a.n_ue == 0);
-          mul = start ? 0.0 : mul * a.zt;  // product of the multipliers from the lane start to n
-          const double2 x = make_double2(fma(mul, cin.x, xl[k].x), fma(mul, cin.y, xl[k].y));
-          const double2 hv = make_double2(fma(ar, hprev[k].x, crm * x.x), fma(ar, hprev[k].y, crm * x.y));
-          hprev[k] = hv;
-          Ht[(long)m * N + n] = hv;
-          if (Et) {
-            const double2 c = cnormal(a.k0, a.k1, kStreamCsi, (uint32_t)(m * N + n), trial);
-            Et[(long)m * N + n] = make_double2(fma(a.cscale, c.x, hv.x), fma(a.cscale, c.y, hv.y));
+        for (int k = 0; k < kSimMaxCpl; ++k) {
+          const int n = n0 + k, m = m0 + r;
+          wv[r][k] = make_double2(0.0, 0.0);
+          if (k < cpl && n < N && m < M) {
+            const double2 g = cnormal(a.k0, a.k1, kStreamW, (uint32_t)(m * N + n), trial);
+            wv[r][k] = make_double2(g.x * a.wscale, g.y * a.wscale);
           }
-          acc.x = fma(hv.x, s[k].x, fma(-hv.y, s[k].y, acc.x));
-          acc.y = fma(hv.x, s[k].y, fma(hv.y, s[k].x, acc.y));
         }
-      }
+      if (lane < kSimRows && m0 + lane < M) gn = cnormal(a.k0, a.k1, kStreamNoise, (uint32_t)(m0 + lane), trial);
 #pragma unroll
-      for (int off = 16; off; off >>= 1) {
-        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
-        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
-      }
-      if (lane == 0) {
-        const double2 g = cnormal(a.k0, a.k1, kStreamNoise, (uint32_t)m, trial);
-        a.y[(long)t * M + m] = make_double2(fma(a.nscale, g.x, acc.x), fma(a.nscale, g.y, acc.y));
+      for (int r = 0; r < kSimRows; ++r) {
+        const int m = m0 + r;
+        if (m >= M) break;
+        // transmit side: x_n = at_n x_{n-1} + ct_n w_n along the users; the
+        // lane folds its segment into (A, B), the warp scans the segments
+        double2 xl[kSimMaxCpl];
+        double A = 1.0;
+        double2 B = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int k = 0; k < kSimMaxCpl; ++k) {
+          const int n = n0 + k;
+          xl[k] = make_double2(0.0, 0.0);
+          if (k < cpl && n < N) {
+            const double2 w = wv[r][k];
+            const bool start = (n == 0) || (a.block_diag && n % a.n_ue == 0);
+            const double an = start ? 0.0 : a.zt, cn = start ? 1.0 : a.ct;
+            B = make_double2(fma(an, B.x, cn * w.x), fma(an, B.y, cn * w.y));
+            A *= an;
+            xl[k] = B;  // value with a zero carry-in
+          }
+        }
+        affine_scan(A, B, lane);
+        // carry into this lane = inclusive value of the previous lane
+        double2 cin = make_double2(__shfl_up_sync(0xffffffffu, B.x, 1), __shfl_up_sync(0xffffffffu, B.y, 1));
+        if (lane == 0) cin = make_double2(0.0, 0.0);
+        // receive side: H[m, n] = ar_m H[m-1, n] + cr_m X[m, n]
+        const double ar = m == 0 ? 0.0 : a.zr, crm = m == 0 ? 1.0 : a.cr;
+        double2 acc = make_double2(0.0, 0.0);  // this lane's part of (H s)[m]
+        double mul = 1.0;
+#pragma unroll
+        for (int k = 0; k < kSimMaxCpl; ++k) {
+          const int n = n0 + k;
+          if (k < cpl && n < N) {
+            const bool start = (n == 0) || (a.block_diag && n % a.n_ue == 0);
+            mul = start ? 0.0 : mul * a.zt;  // product of the multipliers from the lane start to n
+            const double2 x = make_double2(fma(mul, cin.x, xl[k].x), fma(mul, cin.y, xl[k].y));
+            const double2 hv = make_double2(fma(ar, hprev[k].x, crm * x.x), fma(ar, hprev[k].y, crm * x.y));
+            hprev[k] = hv;
+            Ht[(long)m * N + n] = hv;
+            if (Et) {
+              const double2 c = cnormal(a.k0, a.k1, kStreamCsi, (uint32_t)(m * N + n), trial);
+              Et[(long)m * N + n] = make_double2(fma(a.cscale, c.x, hv.x), fma(a.cscale, c.y, hv.y));
+            }
+            acc.x = fma(hv.x, s[k].x, fma(-hv.y, s[k].y, acc.x));
+            acc.y = fma(hv.x, s[k].y, fma(hv.y, s[k].x, acc.y));
+          }
+        }
+#pragma unroll
+        for (int off = 16; off; off >>= 1) {
+          acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
+          acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
+        }
+        if (lane == r)  // every lane holds the row sum; lane r drew row m's noise
+          a.y[(long)t * M + m] = make_double2(fma(a.nscale, gn.x, acc.x), fma(a.nscale, gn.y, acc.y));
       }
     }
   }
@@ -177,7 +197,7 @@ extern "C" int fpm_simulate(uint64_t seed, int32_t context, int32_t point, int64
   if (qam != 16 && qam != 64) return FPM_EINVAL;
   if (!(sigma2 >= 0.0) || n_ue < 1 || (block_diag_users && N % n_ue)) return FPM_EINVAL;
   if ((H_est != nullptr) != (csi_var >= 0.0)) return FPM_EINVAL;
-  if (N > 32 * kSimMaxCpl) return FPM_EUNSUPPORTED;
+  if (N > 32 * kSimCplMax) return FPM_EUNSUPPORTED;
   if (T == 0) return FPM_OK;
   SimArgs a;
   a.k0 = (uint32_t)seed;
@@ -216,7 +236,9 @@ extern "C" int fpm_simulate(uint64_t seed, int32_t context, int32_t point, int64
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int tpb = 256;
   const long grid = std::min<long>((T + tpb / 32 - 1) / (tpb / 32), (long)sms * 8);
-  fpm_sim_kernel<<<(unsigned)grid, tpb, 0, (cudaStream_t)stream>>>(a);
+  if (a.cpl == 1) fpm_sim_kernel<1><<<(unsigned)grid, tpb, 0, (cudaStream_t)stream>>>(a);
+  else if (a.cpl == 2) fpm_sim_kernel<2><<<(unsigned)grid, tpb, 0, (cudaStream_t)stream>>>(a);
+  else fpm_sim_kernel<4><<<(unsigned)grid, tpb, 0, (cudaStream_t)stream>>>(a);
   count_launch();
   return cudaGetLastError() == cudaSuccess ? FPM_OK : FPM_ECUDA;
 }
