@@ -188,8 +188,11 @@ def racecheck(seeds: int) -> int:
             p = os.path.join(d, "o.npz")
             e = dict(os.environ)
             e.update(env)
+            import time
+            t0 = time.time()
             r = subprocess.run([sys.executable, os.path.abspath(__file__), "--dump", p], env=e, capture_output=True,
                                text=True, timeout=1200)
+            wall = time.time() - t0
             if r.returncode != 0:
                 print(f"{name}: FAILED rc={r.returncode}\n{r.stdout[-3000:]}\n{r.stderr[-3000:]}")
                 rc = 1
@@ -199,11 +202,11 @@ def racecheck(seeds: int) -> int:
             guard_line = [ln for ln in r.stdout.splitlines() if ln.startswith("guards")]
             if ref is None:
                 ref = o
-                print(f"{name}: {len(o)} outputs; {guard_line[0] if guard_line else ''}")
+                print(f"{name}: {len(o)} outputs; {guard_line[0] if guard_line else ''}; {wall:.1f} s")
                 continue
             diff = _compare(ref, o)
             print(f"{name}: {'bit-identical to the product run' if not diff else 'DIFFERS: ' + ', '.join(diff[:10])}; "
-                  f"{guard_line[0] if guard_line else ''}")
+                  f"{guard_line[0] if guard_line else ''}; {wall:.1f} s")
             rc |= bool(diff)
     print("racecheck:", "PASS" if rc == 0 else "FAIL")
     return rc
