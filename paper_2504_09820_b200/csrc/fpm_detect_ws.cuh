@@ -62,6 +62,30 @@ inline int env_order(int planned) {
   return v ? (std::atoi(v) != 0) : planned;
 }
 
+// extra matched-filter chains of a Gram thread (kCPT > 1): operands of row
+// mm loaded before the row's tile products, added after them (exact split
+// re / im chains: re += fl(fl(hr yr) + fl(hi yi)), im += fl(fl(hr yi) + fl(hi (-yr))))
+template <int X>
+__device__ __forceinline__ void xchain_load(const double2* sb, const double2* ys, int m0, int mm, int Np,
+                                            const int (&hoff)[X], const int (&yoff)[X], double2 (&h)[X],
+                                            double2 (&y)[X]) {
+#pragma unroll
+  for (int k = 0; k < X; ++k) {
+    h[k] = sb[hoff[k] + mm * Np];
+    y[k] = ys[yoff[k] + m0 + mm];
+  }
+}
+template <int X>
+__device__ __forceinline__ void xchain_add(double (&c)[X], const double2 (&h)[X], const double2 (&y)[X],
+                                           const int (&part)[X]) {
+#pragma unroll
+  for (int k = 0; k < X; ++k) {
+    const double y1 = part[k] ? y[k].y : y[k].x;
+    const double y2 = part[k] ? __longlong_as_double(__double_as_longlong(y[k].x) ^ 0x8000000000000000ULL) : y[k].y;
+    c[k] = __dadd_rn(c[k], __dadd_rn(__dmul_rn(h[k].x, y1), __dmul_rn(h[k].y, y2)));
+  }
+}
+
 #ifdef FPM_CHECKED
 __device__ __forceinline__ long stage_elems_of(const GramGeom& G, int Np) { return (long)G.R * G.MC * Np; }
 __device__ __forceinline__ int nsl_of(const DetectArgs& a) { return a.ws_nslot; }
@@ -161,12 +185,26 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const DetectArgs 
     // (one binary64 per chain), so no chain state occupies registers across
     // the tile loop
     double* bsm = reinterpret_cast<double*>(smem + args.off_bsm);
-    // N = 64: 2*R*N chains == gt threads, so each thread carries exactly one
-    // chain inside the tile loop (latency hidden by the tile math)
-    constexpr bool kChainInLoop = (NB == 16);
+    // Compile-time nb in {4, 8, 16}: the layout has 2*R*N = (16/nb) * gt
+    // chains, so each thread carries kCPT = 16/nb chains inside the tile loop
+    // (their latency hidden by the tile math).  Chain 0 is software-pipelined
+    // with the tile operands; the extra chains (N = 32: one, N = 16: three)
+    // load their operands at the top of each row and add after its products.
+    constexpr int kCPT = (NB == 4 || NB == 8 || NB == 16) ? 16 / NB : 0;
+    constexpr bool kChainInLoop = kCPT > 0;
+    constexpr int kXC = kCPT > 1 ? kCPT - 1 : 1;  // extra chains (array size >= 1)
     const int cq_g = tid / (2 * N), cq_e = tid - cq_g * 2 * N;
     const int cq_part = cq_e / N, cq_n = cq_e - cq_part * N;
     const int cq_hoff = cq_g * G.MC * Np + cq_n, cq_yoff = cq_g * G.M;
+    int xq_hoff[kXC], xq_yoff[kXC], xq_part[kXC];
+#pragma unroll
+    for (int k = 0; k < kXC; ++k) {
+      const int q = tid + (k + 1) * gt;  // < 2*R*N: in-bounds operands even for idle chains
+      const int g = q / (2 * N), e = q - g * 2 * N;
+      xq_part[k] = e / N;
+      xq_hoff[k] = g * G.MC * Np + (e - xq_part[k] * N);
+      xq_yoff[k] = g * G.M;
+    }
 
 #pragma unroll 1
     for (int j = 0; j < my_groups; ++j) {
@@ -179,6 +217,9 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const DetectArgs 
       const int nchain = 2 * Rv * N;
       const bool chain_ok = kChainInLoop && tid < nchain;
       double ca = 0.0;
+      double cx[kXC];
+#pragma unroll
+      for (int k = 0; k < kXC; ++k) cx[k] = 0.0;
       double2 acc[16];
 #pragma unroll
       for (int k = 0; k < 16; ++k) acc[k] = make_double2(0.0, 0.0);
@@ -243,6 +284,8 @@ FPM_PIPE_UNROLL
               ny1 = y1p[2 * mn];
               ny2 = y2p[2 * mn];
             }
+            double2 xh[kXC], xy[kXC];
+            if constexpr (kCPT > 1) xchain_load<kXC>(sb, ys, m0, mm, Np, xq_hoff, xq_yoff, xh, xy);
 #pragma unroll
             for (int u = 0; u < 4; ++u)
 #pragma unroll
@@ -251,6 +294,7 @@ FPM_PIPE_UNROLL
               const double y2s = __longlong_as_double(__double_as_longlong(y2) ^ yneg);
               ca = __dadd_rn(ca, __dadd_rn(__dmul_rn(hc.x, y1), __dmul_rn(hc.y, y2s)));
             }
+            if constexpr (kCPT > 1) xchain_add<kXC>(cx, xh, xy, xq_part);
 #pragma unroll
             for (int u = 0; u < 4; ++u) hi[u] = ni[u];
 #pragma unroll
@@ -296,6 +340,8 @@ FPM_PIPE_UNROLL
               ny1 = y1p[2 * mn];
               ny2 = y2p[2 * mn];
             }
+            double2 xh[kXC], xy[kXC];
+            if constexpr (kCPT > 1) xchain_load<kXC>(sb, ys, m0, mm, Np, xq_hoff, xq_yoff, xh, xy);
             int p = 0;
 #pragma unroll
             for (int u = 0; u < 4; ++u)
@@ -313,6 +359,7 @@ FPM_PIPE_UNROLL
               const double y2s = __longlong_as_double(__double_as_longlong(y2) ^ yneg);
               ca = __dadd_rn(ca, __dadd_rn(__dmul_rn(hc.x, y1), __dmul_rn(hc.y, y2s)));
             }
+            if constexpr (kCPT > 1) xchain_add<kXC>(cx, xh, xy, xq_part);
 #pragma unroll
             for (int u = 0; u < 4; ++u) hx[u] = nx[u];
 #pragma unroll
@@ -323,13 +370,18 @@ FPM_PIPE_UNROLL
             y1 = ny1;
             y2 = ny2;
           }
-        } else if (chain_ok) {  // idle job slot (partial group) that still owns a chain
+        } else if (kChainInLoop) {  // idle job slot (partial group): its chains only
 #pragma unroll 1
           for (int mm = 0; mm < rows; ++mm) {
             const double2 h = sb[cq_hoff + mm * Np];
             const double2 yv = ys[cq_yoff + m0 + mm];
             const double y1 = cq_part ? yv.y : yv.x, y2 = cq_part ? -yv.x : yv.y;
             ca = __dadd_rn(ca, __dadd_rn(__dmul_rn(h.x, y1), __dmul_rn(h.y, y2)));
+            if constexpr (kCPT > 1) {
+              double2 xh[kXC], xy[kXC];
+              xchain_load<kXC>(sb, ys, m0, mm, Np, xq_hoff, xq_yoff, xh, xy);
+              xchain_add<kXC>(cx, xh, xy, xq_part);
+            }
           }
         }
         // matched-filter chains (split re / im, exact): chain q -> slot g,
@@ -372,6 +424,14 @@ FPM_PIPE_UNROLL
         }
         if (kChainInLoop) {
           if (chain_ok) reinterpret_cast<double*>(args.gram_b + (t0 + cq_g) * N + cq_n)[cq_part] = ca;
+#pragma unroll
+          for (int k = 0; k < kCPT - 1; ++k) {
+            const int q = tid + (k + 1) * gt;
+            if (q < nchain) {
+              const int g = q / (2 * N), e = q - g * 2 * N;
+              reinterpret_cast<double*>(args.gram_b + (t0 + g) * N + (e - xq_part[k] * N))[xq_part[k]] = cx[k];
+            }
+          }
         } else {
 #pragma unroll 1
           for (int q = tid; q < nchain; q += gt) {
@@ -423,6 +483,14 @@ FPM_PIPE_UNROLL
       }
       if (kChainInLoop) {
         if (chain_ok) reinterpret_cast<double*>(bS + cq_g * N + cq_n)[cq_part] = ca;
+#pragma unroll
+        for (int k = 0; k < kCPT - 1; ++k) {
+          const int q = tid + (k + 1) * gt;
+          if (q < nchain) {
+            const int g = q / (2 * N), e = q - g * 2 * N;
+            reinterpret_cast<double*>(bS + g * N + (e - xq_part[k] * N))[xq_part[k]] = cx[k];
+          }
+        }
       } else {
 #pragma unroll 1
         for (int q = tid; q < nchain; q += gt) {
@@ -623,9 +691,10 @@ int launch_detect_ws_t(const DetectArgs& a, const WsLayout& sl, int grid, cudaSt
   DetectArgs b = a;
   b.ws_order = env_order(a.ws_order);
   const int threads = a.ws_gt + 32 + a.ws_ct;
-  if constexpr (NB == 16) {
-    // N = 64, R = 2: 256 Gram threads = two warp groups and a 512-thread
-    // block -> register split between the Gram and the other warp groups
+  if constexpr (NB > 0) {
+    // 256 Gram threads (N = 64: R = 2, N = 32: R = 8, N = 16: R = 32) = two
+    // warp groups of a 512-thread block -> register split between the Gram
+    // and the other warp groups
     if (a.ws_gt == 256 && threads <= 512 && !knob("FPM_WS_NOSPLIT")) {
       // a narrower CG group leaves idle warps in the upper warp groups (they
       // still take part in the register hand-over); CG-first order needs the
