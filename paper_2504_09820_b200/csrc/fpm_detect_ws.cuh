@@ -62,6 +62,30 @@ inline int env_order(int planned) {
   return v ? (std::atoi(v) != 0) : planned;
 }
 
+// Stage c of a group: antenna rows m0 .. m0+rows of H for every realization
+// of the group (one bulk copy each, rows contiguous in global memory) and the
+// same rows of y (one bulk copy each), behind the R x MC x Np H block; the
+// whole warp issues, lane 0 posts the stage's bytes first.
+__device__ __forceinline__ void ws_issue(const double2* H, const double2* y, long t0, int Rv, const GramGeom& G,
+                                         int chunk, double2* stage_buf, uint64_t* bar, int lane, int nlanes) {
+  const int m0 = chunk * G.MC;
+  const int rows = min(G.MC, G.M - m0);
+  const uint32_t rowb = (uint32_t)G.N * 16u;
+  if (lane == 0) mbar_expect_tx(bar, (uint32_t)Rv * (uint32_t)rows * (rowb + 16u));
+  if (nlanes > 1) __syncwarp();
+  double2* ybuf = stage_buf + (long)G.R * G.MC * G.Np;
+  for (int g = lane; g < Rv; g += nlanes) {
+    const double2* src = H + ((t0 + g) * (long)G.M + m0) * (long)G.N;
+    double2* dst = stage_buf + (long)g * G.MC * G.Np;
+    if (G.N == G.Np) {
+      bulk_g2s(dst, src, rows * rowb, bar);
+    } else {
+      for (int r = 0; r < rows; ++r) bulk_g2s(dst + r * G.Np, src + (long)r * G.N, rowb, bar);
+    }
+    bulk_g2s(ybuf + g * G.MC, y + (t0 + g) * (long)G.M + m0, (uint32_t)rows * 16u, bar);
+  }
+}
+
 // extra matched-filter chains of a Gram thread (kCPT > 1): operands of row
 // mm loaded before the row's tile products, added after them (exact split
 // re / im chains: re += fl(fl(hr yr) + fl(hi yi)), im += fl(fl(hr yi) + fl(hi (-yr))))
@@ -72,7 +96,7 @@ __device__ __forceinline__ void xchain_load(const double2* sb, const double2* ys
 #pragma unroll
   for (int k = 0; k < X; ++k) {
     h[k] = sb[hoff[k] + mm * Np];
-    y[k] = ys[yoff[k] + m0 + mm];
+    y[k] = ys[yoff[k] + m0 + mm];  // ys: the stage's y block (m0 = 0)
   }
 }
 template <int X>
@@ -87,7 +111,7 @@ __device__ __forceinline__ void xchain_add(double (&c)[X], const double2 (&h)[X]
 }
 
 #ifdef FPM_CHECKED
-__device__ __forceinline__ long stage_elems_of(const GramGeom& G, int Np) { return (long)G.R * G.MC * Np; }
+__device__ __forceinline__ long stage_elems_of(const GramGeom& G, int Np) { return (long)G.R * G.MC * (Np + 1); }
 __device__ __forceinline__ int nsl_of(const DetectArgs& a) { return a.ws_nslot; }
 #endif
 
@@ -119,13 +143,10 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const DetectArgs 
 
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + G.S;
-  uint64_t* ybar = full + 2 * G.S;   // [2]
-  uint64_t* sfull = ybar + 2;        // [2]
+  uint64_t* sfull = full + 2 * G.S + 2;  // [2]
   uint64_t* sempty = sfull + 2;      // [2]
-  uint64_t* ydone = sempty + 2;      // [2] Gram finished reading y buffer b
   const int nsl = args.ws_nslot;     // hand-off slots (2, or 1 when two do not fit)
   double2* stages = reinterpret_cast<double2*>(smem + args.off_union);
-  double2* ysb = reinterpret_cast<double2*>(smem + args.off_ys);  // [2][R*M]
   unsigned char* slots = smem + args.off_slot;
   __shared__ unsigned long long cnt[FPM_NCOUNTERS];
   // diagnostic timeline of CTA 0, groups 0..7: [j*8 + 0] gram loop start,
@@ -138,7 +159,7 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const DetectArgs 
     asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
     const long ends[] = {(long)(2 * G.S + 8) * 8 - args.off_union + 256,  // barriers <= 256 B
                          (long)args.off_union + (long)G.S * stage_elems_of(G, Np) * 16,
-                         (long)args.off_ys + 2L * R * G.M * 16, (long)args.off_slot + (long)nsl_of(args) * sl.bytes,
+                         (long)args.off_ys, (long)args.off_slot + (long)nsl_of(args) * sl.bytes,
                          (long)args.off_bsm + 2L * R * N * 8, (long)args.smem_bytes};
     const long starts[] = {256, args.off_ys, args.off_slot, args.off_bsm, args.off_minv, (long)dyn};
     for (int k = 0; k < 6; ++k)
@@ -155,17 +176,15 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const DetectArgs 
       mbar_init(&empty[s], gt / 32);
     }
     for (int k = 0; k < 2; ++k) {
-      mbar_init(&ybar[k], 1);
       mbar_init(&sfull[k], 1);
       mbar_init(&sempty[k], 1);
-      mbar_init(&ydone[k], 1);
     }
     fence_mbar_init();
   }
   if (tid < FPM_NCOUNTERS) cnt[tid] = 0ULL;
   __syncthreads();
 
-  const int stage_elems = R * G.MC * Np;
+  const int stage_elems = R * G.MC * (Np + 1);  // H rows, then the rows' y entries
   const long total = (long)my_groups * nch;
   // role layout: ws_order 0 = [Gram | producer | CG], 1 = [CG | producer |
   // Gram].  CG-first gives the latency-bound CG warps the lower warp ids,
@@ -195,7 +214,7 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const DetectArgs 
     constexpr int kXC = kCPT > 1 ? kCPT - 1 : 1;  // extra chains (array size >= 1)
     const int cq_g = tid / (2 * N), cq_e = tid - cq_g * 2 * N;
     const int cq_part = cq_e / N, cq_n = cq_e - cq_part * N;
-    const int cq_hoff = cq_g * G.MC * Np + cq_n, cq_yoff = cq_g * G.M;
+    const int cq_hoff = cq_g * G.MC * Np + cq_n, cq_yoff = cq_g * G.MC;  // y: the stage's y block
     int xq_hoff[kXC], xq_yoff[kXC], xq_part[kXC];
 #pragma unroll
     for (int k = 0; k < kXC; ++k) {
@@ -203,14 +222,13 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const DetectArgs 
       const int g = q / (2 * N), e = q - g * 2 * N;
       xq_part[k] = e / N;
       xq_hoff[k] = g * G.MC * Np + (e - xq_part[k] * N);
-      xq_yoff[k] = g * G.M;
+      xq_yoff[k] = g * G.MC;
     }
 
 #pragma unroll 1
     for (int j = 0; j < my_groups; ++j) {
       const long t0 = ((long)blockIdx.x + (long)j * gridDim.x) * R;
       const int Rv = (int)min((long)R, args.T - t0);
-      const int yb = j & 1;                     // y double buffer
       const int slot = nsl == 2 ? (j & 1) : 0;  // hand-off slot and its use count
       const int use = nsl == 2 ? (j >> 1) : j;
       const bool active = job.g >= 0 && job.g < Rv;
@@ -227,8 +245,6 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const DetectArgs 
 #pragma unroll 1
         for (int q = tid; q < nchain; q += gt) bsm[q] = 0.0;
       }
-      const double2* ys = ysb + yb * R * G.M;
-      mbar_wait(&ybar[yb], (uint32_t)((j >> 1) & 1));
       // serial mode (debug bit 8): the Gram of group j starts only once the CG
       // has released the slot of group j - nsl, i.e. no Gram / CG overlap --
       // faster when both compete for the FP64 pipe (fp64 matvec)
@@ -242,6 +258,7 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const DetectArgs 
         mbar_wait(&full[s], (uint32_t)((gc / G.S) & 1));
         diag_jitter(args.debug, 2, (int)gc);
         const double2* sb = stages + s * stage_elems;
+        const double2* sy = sb + R * G.MC * Np;  // y rows m0 .. m0 + rows of every realization of the group
         const int m0 = c * G.MC;
         const int rows = min(G.MC, G.M - m0);
         const double2* pa = sb + joff + job.a;
@@ -254,7 +271,7 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const DetectArgs 
           // (its operands are in-bounds stale data for an idle chain, and the
           // result is only stored when chain_ok); part 1 reads (yi, yr) and
           // flips the sign of yr exactly (sign-bit xor = IEEE negation).
-          const double* yrow = reinterpret_cast<const double*>(ys + cq_yoff + m0);
+          const double* yrow = reinterpret_cast<const double*>(sy + cq_yoff);
           const double* y1p = yrow + cq_part;
           const double* y2p = yrow + (1 - cq_part);
           const unsigned long long yneg = cq_part ? 0x8000000000000000ULL : 0ULL;
@@ -285,7 +302,7 @@ FPM_PIPE_UNROLL
               ny2 = y2p[2 * mn];
             }
             double2 xh[kXC], xy[kXC];
-            if constexpr (kCPT > 1) xchain_load<kXC>(sb, ys, m0, mm, Np, xq_hoff, xq_yoff, xh, xy);
+            if constexpr (kCPT > 1) xchain_load<kXC>(sb, sy, 0, mm, Np, xq_hoff, xq_yoff, xh, xy);
 #pragma unroll
             for (int u = 0; u < 4; ++u)
 #pragma unroll
@@ -306,7 +323,7 @@ FPM_PIPE_UNROLL
         } else if (active) {
           // half-pair job, software-pipelined like the circulant loop above
           const double2* py = sb + joff + job.y + nb * job.yo;
-          const double* yrow = reinterpret_cast<const double*>(ys + cq_yoff + m0);
+          const double* yrow = reinterpret_cast<const double*>(sy + cq_yoff);
           const double* y1p = yrow + cq_part;
           const double* y2p = yrow + (1 - cq_part);
           const unsigned long long yneg = cq_part ? 0x8000000000000000ULL : 0ULL;
@@ -341,7 +358,7 @@ FPM_PIPE_UNROLL
               ny2 = y2p[2 * mn];
             }
             double2 xh[kXC], xy[kXC];
-            if constexpr (kCPT > 1) xchain_load<kXC>(sb, ys, m0, mm, Np, xq_hoff, xq_yoff, xh, xy);
+            if constexpr (kCPT > 1) xchain_load<kXC>(sb, sy, 0, mm, Np, xq_hoff, xq_yoff, xh, xy);
             int p = 0;
 #pragma unroll
             for (int u = 0; u < 4; ++u)
@@ -374,12 +391,12 @@ FPM_PIPE_UNROLL
 #pragma unroll 1
           for (int mm = 0; mm < rows; ++mm) {
             const double2 h = sb[cq_hoff + mm * Np];
-            const double2 yv = ys[cq_yoff + m0 + mm];
+            const double2 yv = sy[cq_yoff + mm];
             const double y1 = cq_part ? yv.y : yv.x, y2 = cq_part ? -yv.x : yv.y;
             ca = __dadd_rn(ca, __dadd_rn(__dmul_rn(h.x, y1), __dmul_rn(h.y, y2)));
             if constexpr (kCPT > 1) {
               double2 xh[kXC], xy[kXC];
-              xchain_load<kXC>(sb, ys, m0, mm, Np, xq_hoff, xq_yoff, xh, xy);
+              xchain_load<kXC>(sb, sy, 0, mm, Np, xq_hoff, xq_yoff, xh, xy);
               xchain_add<kXC>(cx, xh, xy, xq_part);
             }
           }
@@ -392,7 +409,7 @@ FPM_PIPE_UNROLL
             const int g = q / (2 * N), e = q - g * 2 * N;
             const int part = e / N, n = e - part * N;
             const double2* hcol = sb + g * G.MC * Np + n;
-            const double2* yy = ys + g * G.M + m0;
+            const double2* yy = sy + g * G.MC;
             double a = bsm[q];
 #pragma unroll 1
             for (int mm = 0; mm < rows; ++mm) {
@@ -441,7 +458,6 @@ FPM_PIPE_UNROLL
           }
         }
         gbar.sync();
-        if (tid == 0) mbar_arrive(&ydone[yb]);
         continue;
       }
       // ---- hand-off: wait until the CG side has released this slot ----
@@ -501,10 +517,7 @@ FPM_PIPE_UNROLL
       }
       gbar.sync();
       diag_jitter(args.debug, 5, j);
-      if (tid == 0) {
-        mbar_arrive(&sfull[slot]);
-        mbar_arrive(&ydone[yb]);  // every Gram warp is past this group's y reads
-      }
+      if (tid == 0) mbar_arrive(&sfull[slot]);
       if (tr && tid == 0 && j < 8) tr[j * 8 + 3] = clock64();
     }
   } else {
@@ -523,26 +536,13 @@ FPM_PIPE_UNROLL
         const int jj = (int)(gc / nch), c = (int)(gc - (long)jj * nch);
         const long t0 = ((long)blockIdx.x + (long)jj * gridDim.x) * R;
         const int Rv = (int)min((long)R, args.T - t0);
-        if (c == 0) {  // this group's y rides with its first chunk
-          double2* yd = ysb + (jj & 1) * R * G.M;
-          if (pl == 0) mbar_expect_tx(&ybar[jj & 1], (uint32_t)Rv * (uint32_t)G.M * 16u);
-          if (pn > 1) __syncwarp();
-          for (int g = pl; g < Rv; g += pn)
-            bulk_g2s(yd + g * G.M, args.y + (t0 + g) * (long)G.M, G.M * 16u, &ybar[jj & 1]);
-        }
         const int s = (int)(gc % G.S);
-        gram_issue(args.H, t0, Rv, G, c, stages + s * stage_elems, &full[s], pl, pn);
+        ws_issue(args.H, args.y, t0, Rv, G, c, stages + s * stage_elems, &full[s], pl, pn);
       };
       fence_proxy_async();
 #pragma unroll 1
       for (long gc = 0; gc < total; ++gc) {
         if (gc >= G.S) FPM_PWAIT(&empty[gc % G.S], (uint32_t)(((gc - G.S) / G.S) & 1));
-        if (gc >= 2 * nch && gc % nch == 0) {
-          // the y buffer of group jj was last read by group jj-2: wait until
-          // that group's Gram is done (its hand-off has been published)
-          const int jj = (int)(gc / nch);
-          FPM_PWAIT(&ydone[jj & 1], (uint32_t)(((jj - 2) >> 1) & 1));
-        }
         diag_jitter(args.debug, 1, (int)gc);
         issue(gc);
       }

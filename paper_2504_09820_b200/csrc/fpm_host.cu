@@ -524,13 +524,17 @@ static bool plan_detect_ws(int M, int N, int L, int bj, int iters, int mvk, int 
         GramGeom G;
         gram_geom(R, M, N, G, stage_kb);
         G.S = std::max(3, G.S);  // the producer refills two chunks behind
+        // a stage carries MC antenna rows of H (stage_kb) and the same rows of y
+        // for every realization.  A second slot / CG group is not worth stages
+        // of fewer than 4 antenna rows (per-stage hand-shakes and TMA latency
+        // then starve the Gram warps: c1 0.16 -> 0.09 of FP64 measured)
+        if ((ncg > 1 || nslot > 1) && G.MC < std::min(4, M)) continue;
         const int ldA = lda_for(N, mv_bytes(mvk));
-        size_t off = 256;  // mbarriers: full[S], empty[S], ybar, sfull, sempty, ydone [2 each]
+        size_t off = 256;  // mbarriers: full[S], empty[S], (2 unused), sfull[2], sempty[2]
         if ((2 * G.S + 8) * 8 > 256) continue;
-        a.off_union = (int)off;  // H stage ring
-        off = align_up(off + (size_t)G.S * R * G.MC * G.Np * 16, 128);
-        a.off_ys = (int)off;
-        off = align_up(off + (size_t)2 * R * M * 16, 128);
+        a.off_union = (int)off;  // H + y stage ring
+        off = align_up(off + (size_t)G.S * R * G.MC * (G.Np + 1) * 16, 128);
+        a.off_ys = (int)off;  // (no separate y buffer: y rows ride in the stages)
         sl.at = 0;
         sl.b = (int)align_up((size_t)R * N * ldA * mv_bytes(mvk), 128);
         sl.d = (int)align_up(sl.b + (size_t)R * N * 16, 128);
