@@ -18,7 +18,17 @@ struct Slicer {
   int bpa;  // bits per axis
 };
 
+// 128-byte opaque TMA descriptor (CUtensorMap layout; encoded on the host by
+// cuTensorMapEncodeTiled, fpm_host.cu)
+struct alignas(64) TmaDesc {
+  unsigned long long w[16];
+};
+
 struct DetectArgs {
+  // tensor maps of the WS kernel's stages (use_tma): H as (2N doubles, M, T)
+  // with box (2N, MC, R), y as (2 doubles, M, T) with box (2, MC, R)
+  TmaDesc tmH, tmY;
+  int use_tma;
   const double2* H;
   const double2* y;
   const uint8_t* tx;

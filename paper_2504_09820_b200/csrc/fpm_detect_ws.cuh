@@ -62,6 +62,13 @@ inline int env_order(int planned) {
   return v ? (std::atoi(v) != 0) : planned;
 }
 
+// double2 elements of one stage: R x MC x Np of H, then R x MC of y padded
+// to whole 128-byte units (every stage and its y block start 128-byte
+// aligned: tensor-map TMA destinations)
+__host__ __device__ __forceinline__ int ws_stage_elems(const GramGeom& G) {
+  return G.R * G.MC * G.Np + (G.R * G.MC + 7) / 8 * 8;
+}
+
 // Stage c of a group: antenna rows m0 .. m0+rows of H for every realization
 // of the group (one bulk copy each, rows contiguous in global memory) and the
 // same rows of y (one bulk copy each), behind the R x MC x Np H block; the
@@ -111,7 +118,7 @@ __device__ __forceinline__ void xchain_add(double (&c)[X], const double2 (&h)[X]
 }
 
 #ifdef FPM_CHECKED
-__device__ __forceinline__ long stage_elems_of(const GramGeom& G, int Np) { return (long)G.R * G.MC * (Np + 1); }
+__device__ __forceinline__ long stage_elems_of(const GramGeom& G, int Np) { return ws_stage_elems(G); }
 __device__ __forceinline__ int nsl_of(const DetectArgs& a) { return a.ws_nslot; }
 #endif
 
@@ -119,7 +126,7 @@ __device__ __forceinline__ int nsl_of(const DetectArgs& a) { return a.ws_nslot; 
 // the two Gram warp groups run with RS registers per thread, the other two
 // (producer + CG + idle warps) with 256 - RS.
 template <int WK, int K, int NB, int LB, int RS>
-__global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const DetectArgs args, const WsLayout sl) {
+__global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const __grid_constant__ DetectArgs args, const WsLayout sl) {
   extern __shared__ __align__(128) unsigned char smem[];
   typedef typename Ar<K>::C C;
   typedef typename Ar<K>::P P;
@@ -184,7 +191,7 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const DetectArgs 
   if (tid < FPM_NCOUNTERS) cnt[tid] = 0ULL;
   __syncthreads();
 
-  const int stage_elems = R * G.MC * (Np + 1);  // H rows, then the rows' y entries
+  const int stage_elems = ws_stage_elems(G);  // H rows, then the rows' y entries
   const long total = (long)my_groups * nch;
   // role layout: ws_order 0 = [Gram | producer | CG], 1 = [CG | producer |
   // Gram].  CG-first gives the latency-bound CG warps the lower warp ids,
@@ -209,7 +216,8 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const DetectArgs 
     // (their latency hidden by the tile math).  Chain 0 is software-pipelined
     // with the tile operands; the extra chains (N = 32: one, N = 16: three)
     // load their operands at the top of each row and add after its products.
-    constexpr int kCPT = (NB == 4 || NB == 8 || NB == 16) ? 16 / NB : 0;
+    // (extra chains only with the register split: at 128 registers they spill)
+    constexpr int kCPT = (NB == 16 || ((NB == 4 || NB == 8) && RS > 0)) ? 16 / NB : 0;
     constexpr bool kChainInLoop = kCPT > 0;
     constexpr int kXC = kCPT > 1 ? kCPT - 1 : 1;  // extra chains (array size >= 1)
     const int cq_g = tid / (2 * N), cq_e = tid - cq_g * 2 * N;
@@ -537,7 +545,19 @@ FPM_PIPE_UNROLL
         const long t0 = ((long)blockIdx.x + (long)jj * gridDim.x) * R;
         const int Rv = (int)min((long)R, args.T - t0);
         const int s = (int)(gc % G.S);
-        ws_issue(args.H, args.y, t0, Rv, G, c, stages + s * stage_elems, &full[s], pl, pn);
+        if (args.use_tma) {
+          // one tensor-map TMA per operand and stage: the whole group's rows
+          // m0 .. m0+MC of H and of y (realizations past T / rows past M are
+          // zero-filled and never read)
+          if (pl == 0) {
+            double2* sbuf = stages + s * stage_elems;
+            mbar_expect_tx(&full[s], (uint32_t)R * (uint32_t)G.MC * ((uint32_t)G.N * 16u + 16u));
+            tma_load_3d(sbuf, &args.tmH, 0, c * G.MC, (int)t0, &full[s]);
+            tma_load_3d(sbuf + R * G.MC * G.Np, &args.tmY, 0, c * G.MC, (int)t0, &full[s]);
+          }
+        } else {
+          ws_issue(args.H, args.y, t0, Rv, G, c, stages + s * stage_elems, &full[s], pl, pn);
+        }
       };
       fence_proxy_async();
 #pragma unroll 1

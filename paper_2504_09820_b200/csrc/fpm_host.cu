@@ -1,6 +1,8 @@
 // Host side of libfpmimo_b200.so (C ABI: include/fpmimo_b200.h): planning,
 // dispatch to the per-kind kernel units (fpm_inst_<kind>.cu), the standalone
 // Gram / block-Jacobi / slicer kernels, the host-buffer pipeline.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -533,7 +535,7 @@ static bool plan_detect_ws(int M, int N, int L, int bj, int iters, int mvk, int 
         size_t off = 256;  // mbarriers: full[S], empty[S], (2 unused), sfull[2], sempty[2]
         if ((2 * G.S + 8) * 8 > 256) continue;
         a.off_union = (int)off;  // H + y stage ring
-        off = align_up(off + (size_t)G.S * R * G.MC * (G.Np + 1) * 16, 128);
+        off = align_up(off + (size_t)G.S * ws_stage_elems(G) * 16, 128);
         a.off_ys = (int)off;  // (no separate y buffer: y rows ride in the stages)
         sl.at = 0;
         sl.b = (int)align_up((size_t)R * N * ldA * mv_bytes(mvk), 128);
@@ -648,7 +650,51 @@ static int launch_detect(const Kinds& k, const DetectArgs& a, int threads, cudaS
   }
 }
 
-static int launch_detect_ws(const Kinds& k, const DetectArgs& a, const WsLayout& sl, int grid, cudaStream_t st) {
+// cuTensorMapEncodeTiled from the driver (resolved once; no libcuda link)
+static PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }();
+  return fn;
+}
+
+// Tensor maps of the WS kernel's stages (fpm_detect_ws.cuh): H viewed as
+// (2N doubles, M, T) with box (2N, MC, R), y as (2 doubles, M, T) with box
+// (2, MC, R); the boxes land densely as the stage layout [g][m][n] / [g][m]
+// (needs N == Np).  Otherwise (or without the driver entry point) the
+// producer issues one bulk copy per realization.
+static void ws_encode_tma(DetectArgs& a) {
+  a.use_tma = 0;
+  const GramGeom& G = a.G;
+  PFN_cuTensorMapEncodeTiled_v12000 enc = tma_encoder();
+  if (!enc || G.N != G.Np || 2 * G.N > 256 || G.MC > 256 || G.R > 256 || a.T > 0x7fffffffL) return;
+  const cuuint32_t es[3] = {1, 1, 1};
+  const cuuint64_t hd[3] = {(cuuint64_t)2 * G.N, (cuuint64_t)G.M, (cuuint64_t)a.T};
+  const cuuint64_t hs[2] = {(cuuint64_t)G.N * 16, (cuuint64_t)G.M * G.N * 16};
+  const cuuint32_t hb[3] = {(cuuint32_t)(2 * G.N), (cuuint32_t)G.MC, (cuuint32_t)G.R};
+  const cuuint64_t yd[3] = {2, (cuuint64_t)G.M, (cuuint64_t)a.T};
+  const cuuint64_t ys[2] = {16, (cuuint64_t)G.M * 16};
+  const cuuint32_t yb[3] = {2, (cuuint32_t)G.MC, (cuuint32_t)G.R};
+  static_assert(sizeof(TmaDesc) == sizeof(CUtensorMap), "TmaDesc must mirror CUtensorMap");
+  if (enc(reinterpret_cast<CUtensorMap*>(&a.tmH), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double2*>(a.H), hd, hs,
+          hb, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return;
+  if (enc(reinterpret_cast<CUtensorMap*>(&a.tmY), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double2*>(a.y), yd, ys,
+          yb, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return;
+  a.use_tma = knob("FPM_NO_TMA") ? 0 : 1;
+}
+
+static int launch_detect_ws(const Kinds& k, const DetectArgs& a0, const WsLayout& sl, int grid, cudaStream_t st) {
+  DetectArgs a = a0;
+  ws_encode_tma(a);
   int nb, lb;
   pick_spec(a.G.N, a.L, a.bj, nb, lb);
   if (a.gram_A && nb == 16) lb = 4;  // Gram-only: any LB; take the N = 64 specialisation

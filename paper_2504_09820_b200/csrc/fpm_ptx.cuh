@@ -124,6 +124,18 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// tensor-map TMA (cp.async.bulk.tensor): the box at coordinates (c0, c1, c2)
+// of a 3-D tensor map lands densely in shared memory and completes on the
+// mbarrier (transaction bytes = the whole box; out-of-range elements are
+// zero-filled).  `tmap` is the generic address of a __grid_constant__ map.
+__device__ __forceinline__ void tma_load_3d(void* dst, const void* tmap, int c0, int c1, int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+          smem_u32(dst)),
+      "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+
 // warp-group register reallocation (sm_90a+): every thread of the warp group
 // executes the same instruction
 template <int N>
