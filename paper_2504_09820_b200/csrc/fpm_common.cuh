@@ -56,6 +56,7 @@ struct DetectArgs {
   int ws_ncg, ws_ct0;  // CG groups (1 or 2) and the thread count of group 0
   int cg_stride;       // bytes between the two CG groups' state regions
   int ws_nslot;        // hand-off slots (2 double-buffered, 1 when two do not fit)
+  int ws_npass;        // Gram passes per group (2 at N = 128: 512 jobs on 256 Gram threads)
   int debug;  // diagnostic bits (FPM_DEBUG): 1 = WS kernel skips the CG side
   int composed;  // no fused plan fits: fpm_gram -> fpm_bj_setup -> fpm_cg -> slicer
   int gram32;    // FPM_FLAG_GRAM_FP32: binary32 Gram (extension), composed path

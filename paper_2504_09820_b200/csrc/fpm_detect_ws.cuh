@@ -192,7 +192,11 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const __grid_cons
   __syncthreads();
 
   const int stage_elems = ws_stage_elems(G);  // H rows, then the rows' y entries
-  const long total = (long)my_groups * nch;
+  // N = 128: the 512 Gram jobs of a realization run as two passes of 256
+  // over all antenna rows (H streams twice; the FP64 work is unchanged); the
+  // hand-off of pass 0's entries goes out before pass 1 starts
+  const int npass = NB == 32 ? 2 : (NB > 0 ? 1 : args.ws_npass);
+  const long total = (long)my_groups * npass * nch;
   // role layout: ws_order 0 = [Gram | producer | CG], 1 = [CG | producer |
   // Gram].  CG-first gives the latency-bound CG warps the lower warp ids,
   // which the warp schedulers favour when several warps are ready, so the
@@ -205,8 +209,6 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const __grid_cons
     const int tid = threadIdx.x - gbase;  // Gram-local thread id
     // =========================== Gram warps ===========================
     NamedBar gbar{1, gt};
-    const GramJob job = gram_job(tid, R, nb);
-    const int joff = job.g * G.MC * Np;
     // matched-filter chain accumulators live in shared memory between chunks
     // (one binary64 per chain), so no chain state occupies registers across
     // the tile loop
@@ -217,7 +219,7 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const __grid_cons
     // with the tile operands; the extra chains (N = 32: one, N = 16: three)
     // load their operands at the top of each row and add after its products.
     // (extra chains only with the register split: at 128 registers they spill)
-    constexpr int kCPT = (NB == 16 || ((NB == 4 || NB == 8) && RS > 0)) ? 16 / NB : 0;
+    constexpr int kCPT = (NB == 16 || NB == 32 || ((NB == 4 || NB == 8) && RS > 0)) ? (NB == 32 ? 1 : 16 / NB) : 0;
     constexpr bool kChainInLoop = kCPT > 0;
     constexpr int kXC = kCPT > 1 ? kCPT - 1 : 1;  // extra chains (array size >= 1)
     const int cq_g = tid / (2 * N), cq_e = tid - cq_g * 2 * N;
@@ -239,20 +241,25 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const __grid_cons
       const int Rv = (int)min((long)R, args.T - t0);
       const int slot = nsl == 2 ? (j & 1) : 0;  // hand-off slot and its use count
       const int use = nsl == 2 ? (j >> 1) : j;
-      const bool active = job.g >= 0 && job.g < Rv;
       const int nchain = 2 * Rv * N;
       const bool chain_ok = kChainInLoop && tid < nchain;
       double ca = 0.0;
       double cx[kXC];
 #pragma unroll
       for (int k = 0; k < kXC; ++k) cx[k] = 0.0;
-      double2 acc[16];
-#pragma unroll
-      for (int k = 0; k < 16; ++k) acc[k] = make_double2(0.0, 0.0);
       if (!kChainInLoop) {
 #pragma unroll 1
         for (int q = tid; q < nchain; q += gt) bsm[q] = 0.0;
       }
+      double ca_keep = 0.0, cx_keep[kXC];  // chains of pass 0 (later passes recompute and discard them)
+#pragma unroll 1
+      for (int pass = 0; pass < npass; ++pass) {
+      const GramJob job = gram_job(tid + pass * gt, R, nb);
+      const int joff = job.g * G.MC * Np;
+      const bool active = job.g >= 0 && job.g < Rv;
+      double2 acc[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) acc[k] = make_double2(0.0, 0.0);
       // serial mode (debug bit 8): the Gram of group j starts only once the CG
       // has released the slot of group j - nsl, i.e. no Gram / CG overlap --
       // faster when both compete for the FP64 pipe (fp64 matvec)
@@ -261,7 +268,7 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const __grid_cons
 
 #pragma unroll 1
       for (int c = 0; c < nch; ++c) {
-        const long gc = (long)j * nch + c;
+        const long gc = ((long)j * npass + pass) * nch + c;
         const int s = (int)(gc % G.S);
         mbar_wait(&full[s], (uint32_t)((gc / G.S) & 1));
         diag_jitter(args.debug, 2, (int)gc);
@@ -411,7 +418,7 @@ FPM_PIPE_UNROLL
         }
         // matched-filter chains (split re / im, exact): chain q -> slot g,
         // entry n, part (0 re / 1 im); accumulators round-trip through smem
-        if (!kChainInLoop && !(diag_bits(args.debug) & 2)) {
+        if (!kChainInLoop && pass == 0 && !(diag_bits(args.debug) & 2)) {
 #pragma unroll 1
           for (int q = tid; q < nchain; q += gt) {
             const int g = q / (2 * N), e = q - g * 2 * N;
@@ -434,6 +441,11 @@ FPM_PIPE_UNROLL
         if ((tid & 31) == 0) mbar_arrive(&empty[s]);
       }
 
+      if (pass == 0) {
+        ca_keep = ca;
+#pragma unroll
+        for (int k = 0; k < kXC; ++k) cx_keep[k] = cx[k];
+      }
       if (args.gram_A) {
         // Gram-only mode (fpm_gram): final / mirror entries straight to HBM
         // in binary64, no hand-off to the CG side
@@ -447,6 +459,11 @@ FPM_PIPE_UNROLL
               },
               [&](int i, double2 vii) { Agl[(long)i * N + i] = vii; });
         }
+        if (pass + 1 < npass) continue;
+        const double ca = ca_keep;
+        double cx[kXC];
+#pragma unroll
+        for (int k = 0; k < kXC; ++k) cx[k] = cx_keep[k];
         if (kChainInLoop) {
           if (chain_ok) reinterpret_cast<double*>(args.gram_b + (t0 + cq_g) * N + cq_n)[cq_part] = ca;
 #pragma unroll
@@ -469,11 +486,13 @@ FPM_PIPE_UNROLL
         continue;
       }
       // ---- hand-off: wait until the CG side has released this slot ----
-      if (tr && tid == 0 && j < 8) tr[j * 8 + 1] = clock64();
-      if (tr && (tid & 31) == 0 && j == 2) tr[72 + tid / 32] = clock64();
-      diag_jitter(args.debug, 4, j);
-      if (j >= nsl) mbar_wait(&sempty[slot], (uint32_t)((use - 1) & 1));
-      if (tr && tid == 0 && j < 8) tr[j * 8 + 2] = clock64();
+      if (pass == 0) {
+        if (tr && tid == 0 && j < 8) tr[j * 8 + 1] = clock64();
+        if (tr && (tid & 31) == 0 && j == 2) tr[72 + tid / 32] = clock64();
+        diag_jitter(args.debug, 4, j);
+        if (j >= nsl) mbar_wait(&sempty[slot], (uint32_t)((use - 1) & 1));
+        if (tr && tid == 0 && j < 8) tr[j * 8 + 2] = clock64();
+      }
       unsigned char* sp = slots + slot * sl.bytes;
       C* At = reinterpret_cast<C*>(sp + sl.at);
       double2* bS = reinterpret_cast<double2*>(sp + sl.b);
@@ -505,6 +524,13 @@ FPM_PIPE_UNROLL
               }
             });
       }
+      if (pass + 1 < npass) continue;
+      } // pass loop (the last pass falls through with its slot pointers)
+      unsigned char* sp = slots + slot * sl.bytes;
+      double2* bS = reinterpret_cast<double2*>(sp + sl.b);
+      ca = ca_keep;
+#pragma unroll
+      for (int k = 0; k < kXC; ++k) cx[k] = cx_keep[k];
       if (kChainInLoop) {
         if (chain_ok) reinterpret_cast<double*>(bS + cq_g * N + cq_n)[cq_part] = ca;
 #pragma unroll
@@ -541,7 +567,7 @@ FPM_PIPE_UNROLL
     if (pl < pn) {
       // issue global chunk gc (group gc/nch, local chunk gc%nch) into its stage
       auto issue = [&](long gc) {
-        const int jj = (int)(gc / nch), c = (int)(gc - (long)jj * nch);
+        const int jj = (int)(gc / (npass * nch)), c = (int)(gc % nch);
         const long t0 = ((long)blockIdx.x + (long)jj * gridDim.x) * R;
         const int Rv = (int)min((long)R, args.T - t0);
         const int s = (int)(gc % G.S);
@@ -705,6 +731,9 @@ FPM_PIPE_UNROLL
 #ifndef FPM_WS_GRAM_REGS
 #define FPM_WS_GRAM_REGS 176
 #endif
+#ifndef FPM_WS_GRAM_REGS_NB8  // N = 32: two matched-filter chains per Gram thread
+#define FPM_WS_GRAM_REGS_NB8 184  // measured c2: 176 0.610, 184 0.618, 192 0.581 of FP64
+#endif
 
 template <int WK, int K, int NB, int LB>
 int launch_detect_ws_t(const DetectArgs& a, const WsLayout& sl, int grid, cudaStream_t st) {
@@ -720,7 +749,9 @@ int launch_detect_ws_t(const DetectArgs& a, const WsLayout& sl, int grid, cudaSt
       // still take part in the register hand-over); CG-first order needs the
       // CG group to fill warp groups 0-1 so the Gram starts at warp group 2
       if (threads < 512) b.ws_order = 0;
-      constexpr int kRS = sizeof(typename Ar<K>::C) >= 16 ? FPM_WS_GRAM_REGS_WIDE : FPM_WS_GRAM_REGS;
+      constexpr int kRS = sizeof(typename Ar<K>::C) >= 16 ? FPM_WS_GRAM_REGS_WIDE
+                          : NB == 8                        ? FPM_WS_GRAM_REGS_NB8
+                                                           : FPM_WS_GRAM_REGS;
       auto k = fpm_detect_ws_kernel<WK, K, NB, LB, kRS>;
       if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, a.smem_bytes) != cudaSuccess)
         return FPM_ECUDA;

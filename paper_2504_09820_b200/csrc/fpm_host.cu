@@ -497,9 +497,9 @@ static bool plan_detect_ws(int M, int N, int L, int bj, int iters, int mvk, int 
   auto cg_threads = [&](int R, int gt) { return 512 - gt - 32; };
   // largest R whose thread layout works, falling back to smaller R when the
   // shared memory does not fit
-  auto try_R = [&](const int R) -> bool {
+  auto try_R = [&](const int R, const int npass) -> bool {
     const int Lb = bj ? L : 1;
-    const int gt = R * nb * nb / 2;
+    const int gt = R * nb * nb / 2 / npass;
     // two CG groups (alternating hand-off slots) when the Gram side is two full
     // warp groups: 512 threads = 256 Gram + 32 producer + 128 + 96 CG
     const int ncg_env = env_int("FPM_WS_NCG", 0);
@@ -573,6 +573,7 @@ static bool plan_detect_ws(int M, int N, int L, int bj, int iters, int mvk, int 
           a.ldA = ldA;
           a.smem_bytes = (int)off;
           a.ws_gt = gt;
+          a.ws_npass = npass;
           // one CG group: 192 threads (six warps) except at N = 32, measured
           // against the full 224: c3 +1.9 %, c1 +1.3 %, c5 fp64 +0.6 %, c5 fp16
           // +-0, c2 (N = 32) -1.8 %
@@ -592,12 +593,14 @@ static bool plan_detect_ws(int M, int N, int L, int bj, int iters, int mvk, int 
     return false;
   };
   for (int R = 64; R >= 1; R /= 2) {
-    const int gt = R * nb * nb / 2;
+    // N = 128 (R = 1, 512 jobs): two Gram passes of 256 jobs per realization
+    const int npass = (R == 1 && R * nb * nb / 2 == 512) ? 2 : 1;
+    const int gt = R * nb * nb / 2 / npass;
     const int ct = cg_threads(R, gt);
     if (gt > 384 || ct < 64 || gt < 32) continue;
     if ((R * Cc) % 32 || (R * nb) % 32) continue;
     if (env_int("FPM_R", 0) && env_int("FPM_R", 0) != R) continue;
-    if (try_R(R)) return true;
+    if (try_R(R, npass)) return true;
   }
   return false;
 }

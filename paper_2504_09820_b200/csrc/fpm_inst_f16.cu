@@ -15,6 +15,7 @@ int launch_cg_f16(const CgArgs& a, int smem, int lb, cudaStream_t st) {
 int launch_detect_ws_f16(const DetectArgs& a, const WsLayout& sl, int grid, int nb, int lb, cudaStream_t st) {
   if (nb == 16 && lb == 4) return launch_detect_ws_t<FK_F64, FK_F16, 16, 4>(a, sl, grid, st);
   if (nb == 8 && lb == 0) return launch_detect_ws_t<FK_F64, FK_F16, 8, 0>(a, sl, grid, st);
+  if (nb == 32 && lb == 8) return launch_detect_ws_t<FK_F64, FK_F16, 32, 8>(a, sl, grid, st);
   return launch_detect_ws_t<FK_F64, FK_F16, 0, 0>(a, sl, grid, st);
 }
 }  // namespace fpm
