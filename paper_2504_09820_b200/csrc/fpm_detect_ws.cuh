@@ -195,7 +195,8 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const __grid_cons
   // N = 128: the 512 Gram jobs of a realization run as two passes of 256
   // over all antenna rows (H streams twice; the FP64 work is unchanged); the
   // hand-off of pass 0's entries goes out before pass 1 starts
-  const int npass = NB == 32 ? 2 : (NB > 0 ? 1 : args.ws_npass);
+  constexpr int kNpass = NB == 32 ? 2 : (NB > 0 ? 1 : 0);  // 0: run time
+  const int npass = kNpass ? kNpass : args.ws_npass;
   const long total = (long)my_groups * npass * nch;
   // role layout: ws_order 0 = [Gram | producer | CG], 1 = [CG | producer |
   // Gram].  CG-first gives the latency-bound CG warps the lower warp ids,
@@ -209,6 +210,7 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const __grid_cons
     const int tid = threadIdx.x - gbase;  // Gram-local thread id
     // =========================== Gram warps ===========================
     NamedBar gbar{1, gt};
+    const GramJob job0 = gram_job(tid, R, nb);
     // matched-filter chain accumulators live in shared memory between chunks
     // (one binary64 per chain), so no chain state occupies registers across
     // the tile loop
@@ -252,9 +254,11 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const __grid_cons
         for (int q = tid; q < nchain; q += gt) bsm[q] = 0.0;
       }
       double ca_keep = 0.0, cx_keep[kXC];  // chains of pass 0 (later passes recompute and discard them)
+#pragma unroll
+      for (int k = 0; k < kXC; ++k) cx_keep[k] = 0.0;
 #pragma unroll 1
-      for (int pass = 0; pass < npass; ++pass) {
-      const GramJob job = gram_job(tid + pass * gt, R, nb);
+      for (int pass = 0; pass < (kNpass ? kNpass : npass); ++pass) {
+      const GramJob job = kNpass == 1 ? job0 : gram_job(tid + pass * gt, R, nb);
       const int joff = job.g * G.MC * Np;
       const bool active = job.g >= 0 && job.g < Rv;
       double2 acc[16];
@@ -441,7 +445,7 @@ FPM_PIPE_UNROLL
         if ((tid & 31) == 0) mbar_arrive(&empty[s]);
       }
 
-      if (pass == 0) {
+      if (kNpass != 1 && pass == 0) {
         ca_keep = ca;
 #pragma unroll
         for (int k = 0; k < kXC; ++k) cx_keep[k] = cx[k];
@@ -460,10 +464,11 @@ FPM_PIPE_UNROLL
               [&](int i, double2 vii) { Agl[(long)i * N + i] = vii; });
         }
         if (pass + 1 < npass) continue;
-        const double ca = ca_keep;
-        double cx[kXC];
+        if (kNpass != 1) {
+          ca = ca_keep;
 #pragma unroll
-        for (int k = 0; k < kXC; ++k) cx[k] = cx_keep[k];
+          for (int k = 0; k < kXC; ++k) cx[k] = cx_keep[k];
+        }
         if (kChainInLoop) {
           if (chain_ok) reinterpret_cast<double*>(args.gram_b + (t0 + cq_g) * N + cq_n)[cq_part] = ca;
 #pragma unroll
@@ -528,9 +533,11 @@ FPM_PIPE_UNROLL
       } // pass loop (the last pass falls through with its slot pointers)
       unsigned char* sp = slots + slot * sl.bytes;
       double2* bS = reinterpret_cast<double2*>(sp + sl.b);
-      ca = ca_keep;
+      if (kNpass != 1) {
+        ca = ca_keep;
 #pragma unroll
-      for (int k = 0; k < kXC; ++k) cx[k] = cx_keep[k];
+        for (int k = 0; k < kXC; ++k) cx[k] = cx_keep[k];
+      }
       if (kChainInLoop) {
         if (chain_ok) reinterpret_cast<double*>(bS + cq_g * N + cq_n)[cq_part] = ca;
 #pragma unroll

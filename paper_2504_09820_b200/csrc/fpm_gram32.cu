@@ -17,48 +17,10 @@
 
 #include "../../include/fpmimo_b200.h"
 #include "fpm_common.cuh"
+#include "fpm_gram32.cuh"
 #include "fpm_ptx.cuh"
 
 namespace fpm {
-
-// Packed binary32 pairs (FMUL2 / FFMA2, f32x2 PTX, sm_100a): two lanes per
-// instruction, each an IEEE binary32 op rounded to nearest.  ptxas contracts
-// even explicit-.rn f32x2 mul/add pairs into FFMA2, so every add is written
-// as fma(x, k, y) with k = (1, 1) or (1, -1) passed in at run time: k is
-// opaque to the compiler, x*k is exact, and the fma rounds once -- the same
-// bits as add.rn / sub.rn, and nothing left to contract.
-typedef unsigned long long f2x;
-__device__ __forceinline__ f2x pk2(float a, float b) {
-  f2x r;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
-  return r;
-}
-__device__ __forceinline__ float2 upk2(f2x r) {
-  float2 v;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(r));
-  return v;
-}
-__device__ __forceinline__ f2x mul2(f2x a, f2x b) {
-  f2x d;
-  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
-__device__ __forceinline__ f2x fma2(f2x a, f2x b, f2x c) {
-  f2x d;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
-  return d;
-}
-
-// acc += conj(h_i) h_j:  P1 = (hr_i hr_j, hr_i hi_j), P2 = (hi_i hi_j, hi_i hr_j),
-// (pr, pi) = P1 + (1, -1) P2, acc = acc + (pr, pi)
-struct Cj32 {
-  f2x one, pm;  // (1, 1), (1, -1) -- run-time values
-  __device__ __forceinline__ void mac(f2x& acc, float2 hi, float2 hj) const {
-    const f2x p1 = mul2(pk2(hi.x, hi.x), pk2(hj.x, hj.y));
-    const f2x p2 = mul2(pk2(hi.y, hi.y), pk2(hj.y, hj.x));
-    acc = fma2(fma2(p2, pm, p1), one, acc);
-  }
-};
 
 constexpr int kG32Rows = 16;  // antenna rows per staged chunk
 constexpr int kG32Jobs = 2;   // jobs per thread (N = 128: 512 jobs on 256 threads)
@@ -233,8 +195,7 @@ __global__ void __launch_bounds__(256) fpm_gram32_kernel(const double2* __restri
   if (chain) reinterpret_cast<double*>(b + t * N + cn)[cpart] = (double)ca;
 }
 
-// (1, 1) and (1, -1) as binary32 pairs, lane 0 in the low word
-static const f2x g32_one = 0x3F8000003F800000ull, g32_pm = 0xBF8000003F800000ull;
+static const f2x g32_one = kG32One, g32_pm = kG32Pm;
 
 int launch_gram32(const double2* H, const double2* y, long T, int M, int N, double sigma2, double2* A, double2* b,
                   cudaStream_t st) {
