@@ -58,7 +58,7 @@ def f_gram():
 def ncu_traffic(units):
     """dram__bytes_read.sum + dram__bytes_write.sum of the fused kernel from
     the committed `ncu --set full` capture (profiles/), scaled per launch."""
-    p = os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")
+    p = os.path.join(ROOT, "profiles", "r02_ncu_traffic.json")
     try:
         d = json.load(open(p))
     except (OSError, ValueError):
