@@ -205,6 +205,96 @@ __device__ __noinline__ typename Ar<K>::C mv_row(const typename Ar<K>::C* row, c
   return A::asmc(s);
 }
 
+// binary64 complex sums in program order (volatile PTX: ptxas keeps the
+// order, so the in-flight depth -- and the register footprint -- is the one
+// written here; the fully unrolled C++ versions hoist every load and spill
+// under the CG warps' register budget of the warp-specialised kernel).
+// Each dependent add is separated from the previous one by independent
+// loads / products, so the serial chain runs at the DADD latency.
+namespace v64 {
+__device__ __forceinline__ double2 ld(uint32_t a) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ double add(double a, double b) {
+  double r;
+  asm volatile("add.rn.f64 %0, %1, %2;" : "=d"(r) : "d"(a), "d"(b));
+  return r;
+}
+__device__ __forceinline__ double sub(double a, double b) {
+  double r;
+  asm volatile("sub.rn.f64 %0, %1, %2;" : "=d"(r) : "d"(a), "d"(b));
+  return r;
+}
+__device__ __forceinline__ double mul(double a, double b) {
+  double r;
+  asm volatile("mul.rn.f64 %0, %1, %2;" : "=d"(r) : "d"(a), "d"(b));
+  return r;
+}
+// _cmul at binary64 (Ar<FK_F64>::mul): (fl(fl(ar pr) - fl(ai pi)), fl(fl(ar pi) + fl(ai pr)))
+__device__ __forceinline__ double2 cmul(double2 a, double2 p) {
+  const double rr = mul(a.x, p.x), ii = mul(a.y, p.y), ri = mul(a.x, p.y), ir = mul(a.y, p.x);
+  return make_double2(sub(rr, ii), add(ri, ir));
+}
+}  // namespace v64
+
+// left-to-right sum of NC binary64 complex terms (chain_sum at u_IP = fp64);
+// terms requested kD ahead of their add
+template <int NC>
+__device__ __noinline__ double2 chain_sum_f64(const double2* t) {
+  constexpr int kD = 6;
+  const uint32_t a0 = smem_u32(t);
+  double2 v[kD];
+#pragma unroll
+  for (int j = 0; j < kD && j < NC; ++j) v[j] = v64::ld(a0 + 16 * j);
+  double2 s = v[0];
+#pragma unroll
+  for (int k = 1; k < NC; ++k) {
+    if (k - 1 + kD < NC) v[(k - 1) % kD] = v64::ld(a0 + 16 * (k - 1 + kD));
+    s = make_double2(v64::add(s.x, v[k % kD].x), v64::add(s.y, v[k % kD].y));
+  }
+  return assemble(s.x, s.y);
+}
+
+// one matvec row at binary64 (mv_row at u_MV = fp64): the (A, p) operands of
+// term q + kD are requested when term q's product is formed, and products run
+// kP terms ahead of their add
+template <int NC>
+__device__ __noinline__ double2 mv_row_f64(const double2* row, const double2* pv) {
+  constexpr int kD = 5, kP = 2;
+  static_assert(NC >= kD, "row shorter than the operand ring");
+  const uint32_t ra = smem_u32(row), pa = smem_u32(pv);
+  double2 a[kD], p[kD], t[kP];
+#pragma unroll
+  for (int j = 0; j < kD; ++j) {
+    a[j] = v64::ld(ra + 16 * j);
+    p[j] = v64::ld(pa + 16 * j);
+  }
+#pragma unroll
+  for (int j = 0; j < kP; ++j) {
+    t[j] = v64::cmul(a[j], p[j]);
+    if (j + kD < NC) {
+      a[j] = v64::ld(ra + 16 * (j + kD));
+      p[j] = v64::ld(pa + 16 * (j + kD));
+    }
+  }
+  double2 s = t[0];
+#pragma unroll
+  for (int k = 1; k < NC; ++k) {
+    const int q = k - 1 + kP;  // term whose product is formed in this step
+    if (q < NC) {
+      t[q % kP] = v64::cmul(a[q % kD], p[q % kD]);
+      if (q + kD < NC) {
+        a[q % kD] = v64::ld(ra + 16 * (q + kD));
+        p[q % kD] = v64::ld(pa + 16 * (q + kD));
+      }
+    }
+    s = make_double2(v64::add(s.x, t[k % kP].x), v64::add(s.y, t[k % kP].y));
+  }
+  return assemble(s.x, s.y);
+}
+
 // Compile-time N (NC > 0): the whole sum is one basic block, so the
 // scheduler overlaps every load and product with the dependent add chain
 // (the loop versions above issue in order: a block's adds stall the next
@@ -214,7 +304,9 @@ __device__ __noinline__ double2 chain_sum_n(const typename Ar<K>::C* t, const Fm
   typedef Ar<K> A;
   typedef typename A::C C;
   constexpr int n16 = V16<C>::n;
-  if constexpr (NC % n16 == 0 && NC * sizeof(C) <= 256) {
+  if constexpr (K == FK_F64 && NC >= 8) {
+    return chain_sum_f64<NC>(t);
+  } else if constexpr (NC % n16 == 0 && NC * sizeof(C) <= 256) {
     C v[NC];
 #pragma unroll
     for (int i = 0; i < NC / n16; ++i) V16<C>::ld(t + i * n16, v + i * n16);
@@ -253,7 +345,10 @@ __device__ __noinline__ typename Ar<K>::C mv_row_n(const typename Ar<K>::C* row,
   typedef typename A::C C;
   typedef typename A::P P;
   constexpr int B = sizeof(C) >= 16 ? 2 : (sizeof(C) >= 8 ? 4 : 8);
-  if constexpr (NC % B == 0 && NC * sizeof(C) <= 256) {
+  if constexpr (K == FK_F64 && NC >= 8) {
+    if (__isShared(row)) return mv_row_f64<NC>(row, pv);  // (A stays in HBM when it does not fit: fpm_cg)
+    return mv_row<K>(row, pv, NC, f);
+  } else if constexpr (NC % B == 0 && NC * sizeof(C) <= 256) {
     C s;
 #pragma unroll
     for (int k = 0; k < NC; k += B) {

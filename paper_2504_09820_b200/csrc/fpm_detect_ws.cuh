@@ -144,7 +144,8 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const __grid_cons
   // compile-time N for the CG sums, except for 16-byte (fp64 / generic)
   // matvec terms under the register split: their unrolled sums do not fit the
   // CG warps' 256 - RS registers, the loop versions do
-  constexpr int kCgNC = (NB > 0 && (RS == 0 || RS <= FPM_WIDE_NC_MAX_RS || sizeof(typename Ar<K>::C) < 16)) ? 4 * NB : 0;
+  constexpr int kCgNC = (NB > 0 && (RS == 0 || RS <= FPM_WIDE_NC_MAX_RS || sizeof(typename Ar<K>::C) != 16 ||
+                                    K == FK_F64)) ? 4 * NB : 0;
   const int nblk = args.bj ? (N + L - 1) / L : 1;
   const int ldA = NB > 0 ? lda_for(N, (int)sizeof(C)) : args.ldA;
 

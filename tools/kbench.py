@@ -51,7 +51,10 @@ def main():
     ap.add_argument("--wstrace", action="store_true")
     ap.add_argument("--cgtrace", action="store_true")
     ap.add_argument("--cgwtrace", action="store_true")
+    ap.add_argument("--alg", default="fp_bj_cg", choices=list(_lib.FPM_ALG))
+    ap.add_argument("--iters", type=int, default=bench.ITERS)
     a = ap.parse_args()
+    bench.ITERS = a.iters
     bench.M, bench.N, bench.L = a.M, a.N, a.L
     M, N, L, T = a.M, a.N, a.L, a.T
     lib = _lib.load()
@@ -97,7 +100,7 @@ def main():
                           1e-6, None, None)
 
     def fused():
-        _lib.check(lib.fpm_detect(H.data_ptr(), y.data_ptr(), bits.data_ptr(), T, M, N, bench.SIGMA2, 3, L,
+        _lib.check(lib.fpm_detect(H.data_ptr(), y.data_ptr(), bits.data_ptr(), T, M, N, bench.SIGMA2, _lib.FPM_ALG[a.alg], L,
                                   bench.ITERS, ps, 0, 16, None, x.data_ptr(), brk.data_ptr(), div.data_ptr(), None,
                                   cnt.data_ptr(), st), "detect")
 
