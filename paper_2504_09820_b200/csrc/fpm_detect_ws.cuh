@@ -222,11 +222,18 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const __grid_cons
     // with the tile operands; the extra chains (N = 32: one, N = 16: three)
     // load their operands at the top of each row and add after its products.
     // (extra chains only with the register split: at 128 registers they spill)
-    constexpr int kCPT = (NB == 16 || NB == 32 || ((NB == 4 || NB == 8) && RS > 0)) ? (NB == 32 ? 1 : 16 / NB) : 0;
+    // N = 32 (nb = 8; R * N == 256 == gt): one "paired" chain per thread
+    // instead of two split ones -- chain (g, n) accumulates b.re and b.im
+    // from one H load and one (warp-broadcast) y load per row:
+    //   re += fl(fl(hr yr) + fl(hi yi)),  im += fl(fl(hr yi) - fl(hi yr))
+    // (bit-identical to the split chains: fl(hi (-yr)) = -fl(hi yr)); the
+    // split form needs 2.4x the shared-memory wavefronts per row
+    constexpr bool kPair = NB == 8 && RS > 0;
+    constexpr int kCPT = kPair ? 1 : (NB == 16 || NB == 32 || ((NB == 4 || NB == 8) && RS > 0)) ? (NB == 32 ? 1 : 16 / NB) : 0;
     constexpr bool kChainInLoop = kCPT > 0;
     constexpr int kXC = kCPT > 1 ? kCPT - 1 : 1;  // extra chains (array size >= 1)
-    const int cq_g = tid / (2 * N), cq_e = tid - cq_g * 2 * N;
-    const int cq_part = cq_e / N, cq_n = cq_e - cq_part * N;
+    const int cq_g = kPair ? tid / N : tid / (2 * N), cq_e = kPair ? tid - cq_g * N : tid - cq_g * 2 * N;
+    const int cq_part = kPair ? 0 : cq_e / N, cq_n = cq_e - cq_part * N;
     const int cq_hoff = cq_g * G.MC * Np + cq_n, cq_yoff = cq_g * G.MC;  // y: the stage's y block
     int xq_hoff[kXC], xq_yoff[kXC], xq_part[kXC];
 #pragma unroll
@@ -245,8 +252,8 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const __grid_cons
       const int slot = nsl == 2 ? (j & 1) : 0;  // hand-off slot and its use count
       const int use = nsl == 2 ? (j >> 1) : j;
       const int nchain = 2 * Rv * N;
-      const bool chain_ok = kChainInLoop && tid < nchain;
-      double ca = 0.0;
+      const bool chain_ok = kChainInLoop && tid < (kPair ? Rv * N : nchain);
+      double ca = 0.0, cb = 0.0;  // cb: imaginary part of a paired chain
       double cx[kXC];
 #pragma unroll
       for (int k = 0; k < kXC; ++k) cx[k] = 0.0;
@@ -254,7 +261,7 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const __grid_cons
 #pragma unroll 1
         for (int q = tid; q < nchain; q += gt) bsm[q] = 0.0;
       }
-      double ca_keep = 0.0, cx_keep[kXC];  // chains of pass 0 (later passes recompute and discard them)
+      double ca_keep = 0.0, cb_keep = 0.0, cx_keep[kXC];  // chains of pass 0 (later passes recompute and discard them)
 #pragma unroll
       for (int k = 0; k < kXC; ++k) cx_keep[k] = 0.0;
 #pragma unroll 1
@@ -330,6 +337,7 @@ FPM_PIPE_UNROLL
             if (kChainInLoop) {
               const double y2s = __longlong_as_double(__double_as_longlong(y2) ^ yneg);
               ca = __dadd_rn(ca, __dadd_rn(__dmul_rn(hc.x, y1), __dmul_rn(hc.y, y2s)));
+              if constexpr (kPair) cb = __dadd_rn(cb, __dsub_rn(__dmul_rn(hc.x, y2), __dmul_rn(hc.y, y1)));
             }
             if constexpr (kCPT > 1) xchain_add<kXC>(cx, xh, xy, xq_part);
 #pragma unroll
@@ -395,6 +403,7 @@ FPM_PIPE_UNROLL
             if (kChainInLoop) {
               const double y2s = __longlong_as_double(__double_as_longlong(y2) ^ yneg);
               ca = __dadd_rn(ca, __dadd_rn(__dmul_rn(hc.x, y1), __dmul_rn(hc.y, y2s)));
+              if constexpr (kPair) cb = __dadd_rn(cb, __dsub_rn(__dmul_rn(hc.x, y2), __dmul_rn(hc.y, y1)));
             }
             if constexpr (kCPT > 1) xchain_add<kXC>(cx, xh, xy, xq_part);
 #pragma unroll
@@ -414,6 +423,7 @@ FPM_PIPE_UNROLL
             const double2 yv = sy[cq_yoff + mm];
             const double y1 = cq_part ? yv.y : yv.x, y2 = cq_part ? -yv.x : yv.y;
             ca = __dadd_rn(ca, __dadd_rn(__dmul_rn(h.x, y1), __dmul_rn(h.y, y2)));
+            if constexpr (kPair) cb = __dadd_rn(cb, __dsub_rn(__dmul_rn(h.x, yv.y), __dmul_rn(h.y, yv.x)));
             if constexpr (kCPT > 1) {
               double2 xh[kXC], xy[kXC];
               xchain_load<kXC>(sb, sy, 0, mm, Np, xq_hoff, xq_yoff, xh, xy);
@@ -448,6 +458,7 @@ FPM_PIPE_UNROLL
 
       if (kNpass != 1 && pass == 0) {
         ca_keep = ca;
+        cb_keep = cb;
 #pragma unroll
         for (int k = 0; k < kXC; ++k) cx_keep[k] = cx[k];
       }
@@ -467,10 +478,13 @@ FPM_PIPE_UNROLL
         if (pass + 1 < npass) continue;
         if (kNpass != 1) {
           ca = ca_keep;
+          cb = cb_keep;
 #pragma unroll
           for (int k = 0; k < kXC; ++k) cx[k] = cx_keep[k];
         }
-        if (kChainInLoop) {
+        if (kPair) {
+          if (chain_ok) args.gram_b[(t0 + cq_g) * N + cq_n] = make_double2(ca, cb);
+        } else if (kChainInLoop) {
           if (chain_ok) reinterpret_cast<double*>(args.gram_b + (t0 + cq_g) * N + cq_n)[cq_part] = ca;
 #pragma unroll
           for (int k = 0; k < kCPT - 1; ++k) {
@@ -536,10 +550,13 @@ FPM_PIPE_UNROLL
       double2* bS = reinterpret_cast<double2*>(sp + sl.b);
       if (kNpass != 1) {
         ca = ca_keep;
+        cb = cb_keep;
 #pragma unroll
         for (int k = 0; k < kXC; ++k) cx[k] = cx_keep[k];
       }
-      if (kChainInLoop) {
+      if (kPair) {
+        if (chain_ok) bS[cq_g * N + cq_n] = make_double2(ca, cb);
+      } else if (kChainInLoop) {
         if (chain_ok) reinterpret_cast<double*>(bS + cq_g * N + cq_n)[cq_part] = ca;
 #pragma unroll
         for (int k = 0; k < kCPT - 1; ++k) {

@@ -509,7 +509,9 @@ static bool plan_detect_ws(int M, int N, int L, int bj, int iters, int mvk, int 
     // c5 fp16 CG 84 K vs Gram 89 K cycles per group) a single CG group on a
     // single slot keeps up and leaves the most shared memory to the H ring;
     // otherwise two CG groups on alternating slots, then fallbacks.
-    const bool cg_short = (long)iters * N <= 8L * M && mvk != FK_F64;
+    // (more than 128 rows per group -- c2: R = 8 at N = 32 -- makes the
+    // lockstep pass long too: two CG groups measured 0.597 -> 0.611 of FP64)
+    const bool cg_short = (long)iters * N <= 8L * M && mvk != FK_F64 && R * N <= 128;
     const int cand_short[4][2] = {{1, 1}, {2, 2}, {1, 2}, {1, 1}};
     const int cand_long[4][2] = {{2, 2}, {1, 2}, {1, 1}, {1, 1}};
     const int(*cand)[2] = cg_short ? cand_short : cand_long;
