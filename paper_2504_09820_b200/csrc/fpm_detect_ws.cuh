@@ -122,11 +122,12 @@ __device__ __forceinline__ long stage_elems_of(const GramGeom& G, int Np) { retu
 __device__ __forceinline__ int nsl_of(const DetectArgs& a) { return a.ws_nslot; }
 #endif
 
-// RS > 0: register split (setmaxnreg) for a 512-thread block with gt == 256:
-// the two Gram warp groups run with RS registers per thread, the other two
-// (producer + CG + idle warps) with 256 - RS.
-template <int WK, int K, int NB, int LB, int RS>
+// RS > 0: register split (setmaxnreg) for a 512-thread block: the GWG Gram
+// warp groups (gt = 128 * GWG) run with RS registers per thread, the other
+// 4 - GWG (producer + CG + idle warps) with the rest of the register file.
+template <int WK, int K, int NB, int LB, int RS, int GWG = 2>
 __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const __grid_constant__ DetectArgs args, const WsLayout sl) {
+  constexpr int kOtherRegs = RS > 0 ? ((512 - RS * GWG) / (4 - GWG)) / 8 * 8 : 0;
   extern __shared__ __align__(128) unsigned char smem[];
   typedef typename Ar<K>::C C;
   typedef typename Ar<K>::P P;
@@ -581,7 +582,7 @@ FPM_PIPE_UNROLL
     }
   } else {
     // the producer warp and the CG warp groups hand registers to the Gram warps
-    if constexpr (RS > 0) reg_dealloc<256 - RS>();
+    if constexpr (RS > 0) reg_dealloc<kOtherRegs>();
     if (tid >= pbase && tid < pbase + 32) {
     // ========================= producer warp ==========================
     // the whole warp issues (many realizations per group at small N: one bulk
@@ -756,6 +757,9 @@ FPM_PIPE_UNROLL
 #ifndef FPM_WS_GRAM_REGS
 #define FPM_WS_GRAM_REGS 176
 #endif
+#ifndef FPM_WS_GRAM_REGS_1WG  // one Gram warp group (c1: N = 16, R = 16): 216 + 3 x 96
+#define FPM_WS_GRAM_REGS_1WG 216  // measured c1: 184 0.315, 200 0.354, 216 0.363, 232 0.358 of FP64
+#endif
 #ifndef FPM_WS_GRAM_REGS_NB8  // N = 32: two matched-filter chains per Gram thread
 #define FPM_WS_GRAM_REGS_NB8 184  // measured c2: 176 0.610, 184 0.618, 192 0.581 of FP64
 #endif
@@ -783,6 +787,19 @@ int launch_detect_ws_t(const DetectArgs& a, const WsLayout& sl, int grid, cudaSt
       k<<<(unsigned)grid, 512, a.smem_bytes, st>>>(b, sl);
       count_launch();
       return cudaGetLastError() == cudaSuccess ? FPM_OK : FPM_ECUDA;
+    }
+    // one Gram warp group (gt = 128) as the last warp group of a 512-thread
+    // CG-first block (ct = 352): it takes 216 registers, the CG / producer
+    // groups 96 (the 128-register default spills the pipelined tile loop)
+    if constexpr (NB == 4) {
+      if (a.ws_gt == 128 && threads == 512 && b.ws_order == 1 && !knob("FPM_WS_NOSPLIT")) {
+        auto k = fpm_detect_ws_kernel<WK, K, NB, LB, FPM_WS_GRAM_REGS_1WG, 1>;
+        if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, a.smem_bytes) != cudaSuccess)
+          return FPM_ECUDA;
+        k<<<(unsigned)grid, 512, a.smem_bytes, st>>>(b, sl);
+        count_launch();
+        return cudaGetLastError() == cudaSuccess ? FPM_OK : FPM_ECUDA;
+      }
     }
   }
   auto k = fpm_detect_ws_kernel<WK, K, NB, LB, 0>;
