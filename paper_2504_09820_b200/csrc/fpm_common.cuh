@@ -59,7 +59,8 @@ struct DetectArgs {
   int ws_npass;        // Gram passes per group (2 at N = 128: 512 jobs on 256 Gram threads)
   int debug;  // diagnostic bits (FPM_DEBUG): 1 = WS kernel skips the CG side
   int composed;  // no fused plan fits: fpm_gram -> fpm_bj_setup -> fpm_cg -> slicer
-  int gram32;    // FPM_FLAG_GRAM_FP32: binary32 Gram (extension), composed path
+  int gram32;    // FPM_FLAG_GRAM_FP32: binary32 Gram (extension): fused WS kernel at N = 128, else composed
+  unsigned long long g32_one, g32_pm;  // (1, 1), (1, -1) binary32 pairs, opaque run-time values (fpm_gram32.cuh)
   double2* gram_A;  // non-null: Gram-only mode of the WS kernel (fpm_gram): A, b to HBM
   double2* gram_b;
 };

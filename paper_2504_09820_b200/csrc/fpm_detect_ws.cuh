@@ -21,6 +21,7 @@
 #include <cstdlib>
 
 #include "fpm_detect.cuh"
+#include "fpm_gram32.cuh"
 
 namespace fpm {
 
@@ -117,6 +118,99 @@ __device__ __forceinline__ void xchain_add(double (&c)[X], const double2 (&h)[X]
   }
 }
 
+// ---- FP32-Gram extension (G32): rows of a stage converted in place to binary32 ----
+// operands of one row of a binary32 Gram job (circulant: hi[4] hj[4]; half:
+// hx[4] hy[2] hz[4])
+template <bool HALF>
+__device__ __forceinline__ void g32_load(const GramJob& jb, const float2* row, int nb, float2 (&o)[10]) {
+#pragma unroll
+  for (int u = 0; u < 4; ++u) o[u] = row[jb.a + nb * u];
+  if constexpr (!HALF) {
+#pragma unroll
+    for (int v = 0; v < 4; ++v) o[4 + v] = row[jb.c + nb * v];
+  } else {
+#pragma unroll
+    for (int w = 0; w < 2; ++w) o[4 + w] = row[jb.y + nb * (jb.yo + w)];
+#pragma unroll
+    for (int v = 0; v < 4; ++v) o[6 + v] = row[jb.c + nb * v];
+  }
+}
+// the products of one row (gram32_row's arithmetic, operands from registers)
+template <bool HALF>
+__device__ __forceinline__ void g32_mac(const float2 (&o)[10], const Cj32& cj, f2x (&acc)[16]) {
+  if constexpr (!HALF) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) cj.mac(acc[u * 4 + v], o[u], o[4 + v]);
+  } else {
+    int p = 0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = u + 1; v < 4; ++v) cj.mac(acc[p++], o[u], o[v]);
+#pragma unroll
+    for (int w = 0; w < 2; ++w)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) cj.mac(acc[6 + w * 4 + v], o[4 + w], o[6 + v]);
+    const f2x q0 = mul2(pk2(o[0].x, o[1].x), pk2(o[0].x, o[1].x));
+    const f2x q1 = mul2(pk2(o[0].y, o[1].y), pk2(o[0].y, o[1].y));
+    const f2x q2 = mul2(pk2(o[2].x, o[3].x), pk2(o[2].x, o[3].x));
+    const f2x q3 = mul2(pk2(o[2].y, o[3].y), pk2(o[2].y, o[3].y));
+    acc[14] = fma2(fma2(q1, cj.one, q0), cj.one, acc[14]);
+    acc[15] = fma2(fma2(q3, cj.one, q2), cj.one, acc[15]);
+  }
+}
+// rows 0 .. rows-1 of one stage for one job, software-pipelined (row mm+1's
+// operands in flight during row mm's products), with the thread's split
+// matched-filter chain in binary32: re += fl(fl(hr yr) + fl(hi yi)),
+// im += fl(fl(hr yi) + fl(hi (-yr))) (gram_mf_fp32's b)
+template <bool HALF>
+__device__ __forceinline__ void g32_rows(const GramJob& jb, const float2* rows0, int Np, int nb, int rows,
+                                         const Cj32& cj, f2x (&acc)[16], const float2* hcp, const float2* ycp,
+                                         int part, float& ca) {
+  float2 c[10], n[10];
+  g32_load<HALF>(jb, rows0, nb, c);
+  float2 hc = hcp[0], yc = ycp[0];
+#pragma unroll 1
+  for (int mm = 0; mm < rows; ++mm) {
+    const int mn = (mm + 1 < rows) ? mm + 1 : mm;
+    g32_load<HALF>(jb, rows0 + mn * Np, nb, n);
+    const float2 nh = hcp[mn * Np], ny = ycp[mn];
+    g32_mac<HALF>(c, cj, acc);
+    const float y1 = part ? yc.y : yc.x, y2 = part ? -yc.x : yc.y;
+    ca = __fadd_rn(ca, __fadd_rn(__fmul_rn(hc.x, y1), __fmul_rn(hc.y, y2)));
+#pragma unroll
+    for (int k = 0; k < 10; ++k) c[k] = n[k];
+    hc = nh;
+    yc = ny;
+  }
+}
+// producer side: convert stage s (H rows then y rows, binary64 from TMA) to
+// binary32 in place (float2 k over the first half of double2 k's bytes).  A
+// warp step handles 128 consecutive elements: its stores overwrite the bytes
+// of elements < k0/2 + 64, read by this or an earlier step, so the loads of a
+// step complete (__syncwarp) before its stores.
+__device__ __forceinline__ void g32_convert(double2* buf, int n, int lane) {
+  float2* out = reinterpret_cast<float2*>(buf);
+#pragma unroll 1
+  for (int k0 = 0; k0 < n; k0 += 128) {
+    double2 v[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int k = k0 + j * 32 + lane;
+      v[j] = k < n ? buf[k] : make_double2(0.0, 0.0);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int k = k0 + j * 32 + lane;
+      if (k < n) out[k] = make_float2(__double2float_rn(v[j].x), __double2float_rn(v[j].y));
+    }
+    __syncwarp();
+  }
+}
+
 #ifdef FPM_CHECKED
 __device__ __forceinline__ long stage_elems_of(const GramGeom& G, int Np) { return ws_stage_elems(G); }
 __device__ __forceinline__ int nsl_of(const DetectArgs& a) { return a.ws_nslot; }
@@ -125,8 +219,11 @@ __device__ __forceinline__ int nsl_of(const DetectArgs& a) { return a.ws_nslot; 
 // RS > 0: register split (setmaxnreg) for a 512-thread block: the GWG Gram
 // warp groups (gt = 128 * GWG) run with RS registers per thread, the other
 // 4 - GWG (producer + CG + idle warps) with the rest of the register file.
-template <int WK, int K, int NB, int LB, int RS, int GWG = 2>
+template <int WK, int K, int NB, int LB, int RS, int GWG = 2, int G32 = 0>
 __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const __grid_constant__ DetectArgs args, const WsLayout sl) {
+  // G32: binary32 Gram (FP32-Gram extension, BASELINE c4); only N = 128 (one
+  // realization per group, two Gram passes) is instantiated
+  static_assert(!G32 || NB == 32, "binary32 Gram: N = 128 only");
   constexpr int kOtherRegs = RS > 0 ? ((512 - RS * GWG) / (4 - GWG)) / 8 * 8 : 0;
   extern __shared__ __align__(128) unsigned char smem[];
   typedef typename Ar<K>::C C;
@@ -154,6 +251,7 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const __grid_cons
   uint64_t* empty = full + G.S;
   uint64_t* sfull = full + 2 * G.S + 2;  // [2]
   uint64_t* sempty = sfull + 2;      // [2]
+  uint64_t* conv = sempty + 2;       // [S] G32: stage converted to binary32 (producer)
   const int nsl = args.ws_nslot;     // hand-off slots (2, or 1 when two do not fit)
   double2* stages = reinterpret_cast<double2*>(smem + args.off_union);
   unsigned char* slots = smem + args.off_slot;
@@ -188,6 +286,8 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const __grid_cons
       mbar_init(&sfull[k], 1);
       mbar_init(&sempty[k], 1);
     }
+    if constexpr (G32)
+      for (int s = 0; s < G.S; ++s) mbar_init(&conv[s], 1);
     fence_mbar_init();
   }
   if (tid < FPM_NCOUNTERS) cnt[tid] = 0ULL;
@@ -262,7 +362,8 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const __grid_cons
 #pragma unroll 1
         for (int q = tid; q < nchain; q += gt) bsm[q] = 0.0;
       }
-      double ca_keep = 0.0, cb_keep = 0.0, cx_keep[kXC];  // chains of pass 0 (later passes recompute and discard them)
+      double ca_keep = 0.0, cb_keep = 0.0, cx_keep[kXC];
+      float ca32 = 0.f, ca32_keep = 0.f;  // G32: the split chain in binary32  // chains of pass 0 (later passes recompute and discard them)
 #pragma unroll
       for (int k = 0; k < kXC; ++k) cx_keep[k] = 0.0;
 #pragma unroll 1
@@ -273,6 +374,9 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const __grid_cons
       double2 acc[16];
 #pragma unroll
       for (int k = 0; k < 16; ++k) acc[k] = make_double2(0.0, 0.0);
+      f2x acc32[16];  // G32: binary32 pairs
+#pragma unroll
+      for (int k = 0; k < 16; ++k) acc32[k] = 0ull;
       // serial mode (debug bit 8): the Gram of group j starts only once the CG
       // has released the slot of group j - nsl, i.e. no Gram / CG overlap --
       // faster when both compete for the FP64 pipe (fp64 matvec)
@@ -283,7 +387,7 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const __grid_cons
       for (int c = 0; c < nch; ++c) {
         const long gc = ((long)j * npass + pass) * nch + c;
         const int s = (int)(gc % G.S);
-        mbar_wait(&full[s], (uint32_t)((gc / G.S) & 1));
+        mbar_wait(G32 ? &conv[s] : &full[s], (uint32_t)((gc / G.S) & 1));
         diag_jitter(args.debug, 2, (int)gc);
         const double2* sb = stages + s * stage_elems;
         const double2* sy = sb + R * G.MC * Np;  // y rows m0 .. m0 + rows of every realization of the group
@@ -291,7 +395,15 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const __grid_cons
         const int rows = min(G.MC, G.M - m0);
         const double2* pa = sb + joff + job.a;
         const double2* pc = sb + joff + job.c;
-        if (diag_bits(args.debug) & 4) {
+        if constexpr (G32) {
+          const float2* sbf = reinterpret_cast<const float2*>(sb);
+          const float2* syf = sbf + 2 * (R * G.MC * Np);  // the stage's y rows (converted)
+          const Cj32 cj{args.g32_one, args.g32_pm};
+          if (active && !job.half)
+            g32_rows<false>(job, sbf + joff, Np, nb, rows, cj, acc32, sbf + cq_hoff, syf + cq_yoff, cq_part, ca32);
+          else if (active)
+            g32_rows<true>(job, sbf + joff, Np, nb, rows, cj, acc32, sbf + cq_hoff, syf + cq_yoff, cq_part, ca32);
+        } else if (diag_bits(args.debug) & 4) {
           // diagnostic: Gram math skipped (CG measured without FP64 contention)
         } else if (active && !job.half) {
           // software-pipelined: row mm+1's operands (tile and chain) are in
@@ -460,10 +572,11 @@ FPM_PIPE_UNROLL
       if (kNpass != 1 && pass == 0) {
         ca_keep = ca;
         cb_keep = cb;
+        ca32_keep = ca32;
 #pragma unroll
         for (int k = 0; k < kXC; ++k) cx_keep[k] = cx[k];
       }
-      if (args.gram_A) {
+      if (!G32 && args.gram_A) {
         // Gram-only mode (fpm_gram): final / mirror entries straight to HBM
         // in binary64, no hand-off to the CG side
         if (active) {
@@ -523,27 +636,27 @@ FPM_PIPE_UNROLL
       if (active) {
         C* Ag = At + job.g * N * ldA;
         double2* dg = dS + job.g * nblk;
-        gram_entries(
-            job, acc, nb, N, args.sigma2,
-            [&](int i, int jx, double2 vij, double2 vji) {
-              Ag[i * ldA + jx] = Ar<K>::rnd(vij, args.pr.mv);
-              Ag[jx * ldA + i] = Ar<K>::rnd(vji, args.pr.mv);
-              if (onchip) {
-                const int kb = i / L;
-                if (kb == jx / L) {
-                  const int il = i - kb * L, jl = jx - kb * L;
-                  dg[(il * L + jl) * nbt + kb] = vij;
-                  dg[(jl * L + il) * nbt + kb] = vji;
-                }
-              }
-            },
-            [&](int i, double2 vii) {
-              Ag[i * ldA + i] = Ar<K>::rnd(vii, args.pr.mv);
-              if (onchip) {
-                const int kb = i / L, il = i - kb * L;
-                dg[(il * L + il) * nbt + kb] = vii;
-              }
-            });
+        auto put = [&](int i, int jx, double2 vij, double2 vji) {
+          Ag[i * ldA + jx] = Ar<K>::rnd(vij, args.pr.mv);
+          Ag[jx * ldA + i] = Ar<K>::rnd(vji, args.pr.mv);
+          if (onchip) {
+            const int kb = i / L;
+            if (kb == jx / L) {
+              const int il = i - kb * L, jl = jx - kb * L;
+              dg[(il * L + jl) * nbt + kb] = vij;
+              dg[(jl * L + il) * nbt + kb] = vji;
+            }
+          }
+        };
+        auto put_diag = [&](int i, double2 vii) {
+          Ag[i * ldA + i] = Ar<K>::rnd(vii, args.pr.mv);
+          if (onchip) {
+            const int kb = i / L, il = i - kb * L;
+            dg[(il * L + il) * nbt + kb] = vii;
+          }
+        };
+        if constexpr (G32) gram32_entries(job, acc32, nb, N, __double2float_rn(args.sigma2), put, put_diag);
+        else gram_entries(job, acc, nb, N, args.sigma2, put, put_diag);
       }
       if (pass + 1 < npass) continue;
       } // pass loop (the last pass falls through with its slot pointers)
@@ -552,9 +665,11 @@ FPM_PIPE_UNROLL
       if (kNpass != 1) {
         ca = ca_keep;
         cb = cb_keep;
+        ca32 = ca32_keep;
 #pragma unroll
         for (int k = 0; k < kXC; ++k) cx[k] = cx_keep[k];
       }
+      if constexpr (G32) ca = (double)ca32;  // exact widening
       if (kPair) {
         if (chain_ok) bS[cq_g * N + cq_n] = make_double2(ca, cb);
       } else if (kChainInLoop) {
@@ -611,13 +726,28 @@ FPM_PIPE_UNROLL
           ws_issue(args.H, args.y, t0, Rv, G, c, stages + s * stage_elems, &full[s], pl, pn);
         }
       };
+      // G32: chunk gc - 1 is converted to binary32 while chunk gc's copy is in flight
+      auto convert = [&](long gc) {
+        const int s = (int)(gc % G.S);
+        FPM_PWAIT(&full[s], (uint32_t)((gc / G.S) & 1));
+        double2* sbuf = stages + s * stage_elems;
+        g32_convert(sbuf, R * G.MC * Np, pl);
+        g32_convert(sbuf + R * G.MC * Np, R * G.MC, pl);
+        fence_proxy_async();  // these generic-proxy writes precede the next TMA into the stage
+        __syncwarp();
+        if (pl == 0) mbar_arrive(&conv[s]);
+      };
       fence_proxy_async();
 #pragma unroll 1
       for (long gc = 0; gc < total; ++gc) {
         if (gc >= G.S) FPM_PWAIT(&empty[gc % G.S], (uint32_t)(((gc - G.S) / G.S) & 1));
         diag_jitter(args.debug, 1, (int)gc);
         issue(gc);
+        if constexpr (G32)
+          if (gc >= 1) convert(gc - 1);
       }
+      if constexpr (G32)
+        if (total >= 1) convert(total - 1);
     }
     } else if (tid >= cbase && tid < cbase + ct && !args.gram_A) {
     // ============================ CG warps ============================
@@ -769,6 +899,19 @@ int launch_detect_ws_t(const DetectArgs& a, const WsLayout& sl, int grid, cudaSt
   DetectArgs b = a;
   b.ws_order = env_order(a.ws_order);
   const int threads = a.ws_gt + 32 + a.ws_ct;
+  if constexpr (NB == 32 && K != FK_F64 && K != FK_GEN) {
+    if (a.gram32) {  // binary32 Gram (FP32-Gram extension): N = 128, two passes of 256 Gram threads
+      if (a.ws_gt != 256 || threads > 512) return FPM_EUNSUPPORTED;
+      if (threads < 512) b.ws_order = 0;
+      auto k = fpm_detect_ws_kernel<WK, K, NB, LB, FPM_WS_GRAM_REGS, 2, 1>;
+      if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, a.smem_bytes) != cudaSuccess)
+        return FPM_ECUDA;
+      k<<<(unsigned)grid, 512, a.smem_bytes, st>>>(b, sl);
+      count_launch();
+      return cudaGetLastError() == cudaSuccess ? FPM_OK : FPM_ECUDA;
+    }
+  }
+  if (a.gram32) return FPM_EUNSUPPORTED;
   if constexpr (NB > 0) {
     // 256 Gram threads (N = 64: R = 2, N = 32: R = 8, N = 16: R = 32) = two
     // warp groups of a 512-thread block -> register split between the Gram

@@ -527,7 +527,7 @@ static bool plan_detect_ws(int M, int N, int L, int bj, int iters, int mvk, int 
         if (env_int("FPM_STAGE_KB", 0) && si > 0) break;
         GramGeom G;
         gram_geom(R, M, N, G, stage_kb);
-        G.S = std::max(3, G.S);  // the producer refills two chunks behind
+        G.S = std::max(a.gram32 ? 4 : 3, G.S);  // the producer refills two chunks behind (G32: and converts one)
         // a stage carries MC antenna rows of H (stage_kb) and the same rows of y
         // for every realization.  A second slot / CG group is not worth stages
         // of fewer than 4 antenna rows (per-stage hand-shakes and TMA latency
@@ -535,7 +535,7 @@ static bool plan_detect_ws(int M, int N, int L, int bj, int iters, int mvk, int 
         if ((ncg > 1 || nslot > 1) && G.MC < std::min(4, M)) continue;
         const int ldA = lda_for(N, mv_bytes(mvk));
         size_t off = 256;  // mbarriers: full[S], empty[S], (2 unused), sfull[2], sempty[2]
-        if ((2 * G.S + 8) * 8 > 256) continue;
+        if ((a.gram32 ? 3 * G.S + 6 : 2 * G.S + 8) * 8 > 256) continue;  // + conv[S] (G32)
         a.off_union = (int)off;  // H + y stage ring
         off = align_up(off + (size_t)G.S * ws_stage_elems(G) * 16, 128);
         a.off_ys = (int)off;  // (no separate y buffer: y rows ride in the stages)
@@ -705,7 +705,7 @@ static int launch_detect_ws(const Kinds& k, const DetectArgs& a0, const WsLayout
   if (a.gram_A && nb == 16) lb = 4;  // Gram-only: any LB; take the N = 64 specialisation
   if (a.G.N != a.G.Np) nb = 0;
   if (knob("FPM_NO_SPEC")) nb = lb = 0;
-  note_kernel("fpm_detect_ws_kernel", k, nb, lb);
+  note_kernel(a.gram32 ? "fpm_detect_ws_kernel[gram32]" : "fpm_detect_ws_kernel", k, nb, lb);
   if (k.w == FK_GEN) return launch_detect_ws_gen_w(a, sl, grid, 0, 0, st);
   switch (k.mv) {
     case FK_F64: return launch_detect_ws_f64(a, sl, grid, nb, lb, st);
@@ -1086,7 +1086,21 @@ static int detect_args(const double* H, const double* y, const uint8_t* tx_bits,
     a.G.R = 1;
     return FPM_OK;
   }
-  if (gram32) {  // extension: binary32 Gram kernel, then the standalone stages
+  a.g32_one = kG32One;
+  a.g32_pm = kG32Pm;
+  // FP32-Gram extension: fused (binary32 Gram warps in the persistent kernel,
+  // A never leaves the SM) for the c4 geometry -- N = 128, block-Jacobi L = 8,
+  // fp16 matvec / inner, fp64 work; otherwise the binary32 Gram kernel and
+  // the standalone stages
+  if (gram32) {
+    const bool fusable = N == 128 && bj && L == 8 && k.w == FK_F64 && k.mv == FK_F16 && k.ip == FK_F16 &&
+                         !knob("FPM_COMPOSED");
+    DetectArgs aw = a;
+    if (fusable && plan_detect_ws(M, N, a.L, bj, iters, k.mv, k.ip, aw, sl, grid)) {
+      ws = true;
+      a = aw;
+      return FPM_OK;
+    }
     a.G.R = 1;
     a.composed = 1;
     return FPM_OK;

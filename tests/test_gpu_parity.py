@@ -562,25 +562,36 @@ def test_edge_inputs_against_oracle(oracle, case):
         np.testing.assert_array_equal(r.bits, O.demod16(ref.x))
 
 
-@pytest.mark.parametrize("M,N", [(128, 64), (512, 128), (40, 16), (33, 12)])
-def test_fp32_gram_extension(oracle, M, N):
+@pytest.mark.parametrize("M,N,L,T", [(128, 64, 4, 5), (512, 128, 4, 5), (40, 16, 4, 5), (33, 12, 4, 5),
+                                     (512, 128, 8, 300), (200, 128, 8, 151)])
+def test_fp32_gram_extension(oracle, M, N, L, T):
     """FP32-Gram extension (BASELINE c4; parity unpinned -- no reference knob):
     the binary32 Gram / matched filter bit-exact against its restatement, and
-    the detector on top of it bit-exact with injected inverses."""
+    the detector on top of it bit-exact with injected inverses.  N = 128 with
+    L = 8 runs the fused persistent kernel with binary32 Gram warps (stages
+    converted in place by the producer warp; several groups per CTA at T =
+    300, antenna rows not a multiple of the stage rows at M = 200); the rest
+    the composed path (binary32 Gram kernel, then the standalone stages)."""
+    from paper_2504_09820_b200 import _lib
     from paper_2504_09820_b200.detect import DetectorSpec, detect, gram_mf
     O = oracle
-    T = 5
     H, y, bits, s2 = O.simulate(M, N, 0.6, 12.0, range(T), 17)
     A, b = O.gram_mf_fp32(H, y, s2)
     Ag, bg = gram_mf(H, y, s2, gram="fp32")
     assert bits_equal(Ag, A) and bits_equal(bg, b)
-    L = 4
     mats = O.bj_inverses(A, L)
     det = DetectorSpec("fp_bj_cg", iters=4, L=L, matvec="fp16", inner="fp16", gram="fp32")
     ref = O.cg_batch(A, b, 4, O.FP64, O.FP16, O.FP16, mats)
     r = detect(det, H, y, s2, bits, minv=mats, want_bits=True)
+    kname = _lib.load().fpm_last_kernel().decode()
+    assert ("gram32" in kname and "ws" in kname) == (N == 128 and L == 8), kname
     assert bits_equal(r.x, ref.x)
     np.testing.assert_array_equal(r.bits, O.demod16(ref.x))
+    # on-chip block inverses: the same decisions, x within the fp16 tolerance
+    r2 = detect(det, H, y, s2, bits, want_bits=True)
+    np.testing.assert_array_equal(r2.bits, O.demod16(ref.x))
+    err = np.linalg.norm(r2.x - ref.x, axis=1) / np.linalg.norm(ref.x, axis=1)
+    assert err.max() <= 2.0 ** -(10 - 2), err.max()
 
 
 @pytest.mark.parametrize("scale", [1e-20, 3e-23, 3e19])

@@ -53,6 +53,7 @@ def main():
     ap.add_argument("--cgwtrace", action="store_true")
     ap.add_argument("--alg", default="fp_bj_cg", choices=list(_lib.FPM_ALG))
     ap.add_argument("--iters", type=int, default=bench.ITERS)
+    ap.add_argument("--gram32", action="store_true", help="FP32-Gram extension (FPM_FLAG_GRAM_FP32)")
     a = ap.parse_args()
     bench.ITERS = a.iters
     bench.M, bench.N, bench.L = a.M, a.N, a.L
@@ -100,7 +101,7 @@ def main():
                           1e-6, None, None)
 
     def fused():
-        _lib.check(lib.fpm_detect(H.data_ptr(), y.data_ptr(), bits.data_ptr(), T, M, N, bench.SIGMA2, _lib.FPM_ALG[a.alg], L,
+        _lib.check(lib.fpm_detect(H.data_ptr(), y.data_ptr(), bits.data_ptr(), T, M, N, bench.SIGMA2, _lib.FPM_ALG[a.alg] | (_lib.FPM_FLAG_GRAM_FP32 if a.gram32 else 0), L,
                                   bench.ITERS, ps, 0, 16, None, x.data_ptr(), brk.data_ptr(), div.data_ptr(), None,
                                   cnt.data_ptr(), st), "detect")
 
