@@ -186,6 +186,32 @@ __device__ __forceinline__ void g32_rows(const GramJob& jb, const float2* rows0,
     yc = ny;
   }
 }
+// N = 128 in binary32 (G32): the thread's two jobs (t and t + 256) in ONE
+// pass over the antenna rows (binary32 accumulators take half the registers,
+// so H streams once): job 1's operands load while job 0's products run and
+// vice versa
+template <bool HALF1>
+__device__ __forceinline__ void g32_rows2(const GramJob& j0, const GramJob& j1, const float2* r0, const float2* r1,
+                                          int Np, int nb, int rows, const Cj32& cj, f2x (&acc0)[16],
+                                          f2x (&acc1)[16], const float2* hcp, const float2* ycp, int part, float& ca) {
+  float2 o0[10], o1[10];
+  g32_load<false>(j0, r0, nb, o0);
+  float2 hc = hcp[0], yc = ycp[0];
+#pragma unroll 1
+  for (int mm = 0; mm < rows; ++mm) {
+    const int mn = (mm + 1 < rows) ? mm + 1 : mm;
+    g32_load<HALF1>(j1, r1 + mm * Np, nb, o1);
+    const float2 nh = hcp[mn * Np], ny = ycp[mn];
+    g32_mac<false>(o0, cj, acc0);
+    const float y1 = part ? yc.y : yc.x, y2 = part ? -yc.x : yc.y;
+    ca = __fadd_rn(ca, __fadd_rn(__fmul_rn(hc.x, y1), __fmul_rn(hc.y, y2)));
+    g32_load<false>(j0, r0 + mn * Np, nb, o0);
+    g32_mac<HALF1>(o1, cj, acc1);
+    hc = nh;
+    yc = ny;
+  }
+}
+
 // producer side: convert stage s (H rows then y rows, binary64 from TMA) to
 // binary32 in place (float2 k over the first half of double2 k's bytes).  A
 // warp step handles 128 consecutive elements: its stores overwrite the bytes
@@ -297,7 +323,7 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const __grid_cons
   // N = 128: the 512 Gram jobs of a realization run as two passes of 256
   // over all antenna rows (H streams twice; the FP64 work is unchanged); the
   // hand-off of pass 0's entries goes out before pass 1 starts
-  constexpr int kNpass = NB == 32 ? 2 : (NB > 0 ? 1 : 0);  // 0: run time
+  constexpr int kNpass = (NB == 32 && !G32) ? 2 : (NB > 0 ? 1 : 0);  // 0: run time (G32: both jobs in one pass)
   const int npass = kNpass ? kNpass : args.ws_npass;
   const long total = (long)my_groups * npass * nch;
   // role layout: ws_order 0 = [Gram | producer | CG], 1 = [CG | producer |
@@ -374,9 +400,10 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const __grid_cons
       double2 acc[16];
 #pragma unroll
       for (int k = 0; k < 16; ++k) acc[k] = make_double2(0.0, 0.0);
-      f2x acc32[16];  // G32: binary32 pairs
+      f2x acc32[16], acc32b[16];  // G32: binary32 pairs of the thread's jobs t and t + 256
 #pragma unroll
-      for (int k = 0; k < 16; ++k) acc32[k] = 0ull;
+      for (int k = 0; k < 16; ++k) acc32[k] = acc32b[k] = 0ull;
+      const GramJob job1 = G32 ? gram_job(tid + gt, R, nb) : job;
       // serial mode (debug bit 8): the Gram of group j starts only once the CG
       // has released the slot of group j - nsl, i.e. no Gram / CG overlap --
       // faster when both compete for the FP64 pipe (fp64 matvec)
@@ -399,10 +426,13 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const __grid_cons
           const float2* sbf = reinterpret_cast<const float2*>(sb);
           const float2* syf = sbf + 2 * (R * G.MC * Np);  // the stage's y rows (converted)
           const Cj32 cj{args.g32_one, args.g32_pm};
-          if (active && !job.half)
-            g32_rows<false>(job, sbf + joff, Np, nb, rows, cj, acc32, sbf + cq_hoff, syf + cq_yoff, cq_part, ca32);
+          const float2* r1 = sbf + job1.g * G.MC * Np;
+          if (active && !job1.half)
+            g32_rows2<false>(job, job1, sbf + joff, r1, Np, nb, rows, cj, acc32, acc32b, sbf + cq_hoff, syf + cq_yoff,
+                             cq_part, ca32);
           else if (active)
-            g32_rows<true>(job, sbf + joff, Np, nb, rows, cj, acc32, sbf + cq_hoff, syf + cq_yoff, cq_part, ca32);
+            g32_rows2<true>(job, job1, sbf + joff, r1, Np, nb, rows, cj, acc32, acc32b, sbf + cq_hoff, syf + cq_yoff,
+                            cq_part, ca32);
         } else if (diag_bits(args.debug) & 4) {
           // diagnostic: Gram math skipped (CG measured without FP64 contention)
         } else if (active && !job.half) {
@@ -655,8 +685,12 @@ FPM_PIPE_UNROLL
             dg[(il * L + il) * nbt + kb] = vii;
           }
         };
-        if constexpr (G32) gram32_entries(job, acc32, nb, N, __double2float_rn(args.sigma2), put, put_diag);
-        else gram_entries(job, acc, nb, N, args.sigma2, put, put_diag);
+        if constexpr (G32) {
+          gram32_entries(job, acc32, nb, N, __double2float_rn(args.sigma2), put, put_diag);
+          gram32_entries(job1, acc32b, nb, N, __double2float_rn(args.sigma2), put, put_diag);
+        } else {
+          gram_entries(job, acc, nb, N, args.sigma2, put, put_diag);
+        }
       }
       if (pass + 1 < npass) continue;
       } // pass loop (the last pass falls through with its slot pointers)
@@ -726,28 +760,29 @@ FPM_PIPE_UNROLL
           ws_issue(args.H, args.y, t0, Rv, G, c, stages + s * stage_elems, &full[s], pl, pn);
         }
       };
-      // G32: chunk gc - 1 is converted to binary32 while chunk gc's copy is in flight
-      auto convert = [&](long gc) {
-        const int s = (int)(gc % G.S);
-        FPM_PWAIT(&full[s], (uint32_t)((gc / G.S) & 1));
-        double2* sbuf = stages + s * stage_elems;
-        g32_convert(sbuf, R * G.MC * Np, pl);
-        g32_convert(sbuf + R * G.MC * Np, R * G.MC, pl);
-        fence_proxy_async();  // these generic-proxy writes precede the next TMA into the stage
-        __syncwarp();
-        if (pl == 0) mbar_arrive(&conv[s]);
-      };
       fence_proxy_async();
 #pragma unroll 1
       for (long gc = 0; gc < total; ++gc) {
         if (gc >= G.S) FPM_PWAIT(&empty[gc % G.S], (uint32_t)(((gc - G.S) / G.S) & 1));
         diag_jitter(args.debug, 1, (int)gc);
         issue(gc);
-        if constexpr (G32)
-          if (gc >= 1) convert(gc - 1);
       }
-      if constexpr (G32)
-        if (total >= 1) convert(total - 1);
+    }
+    } else if (G32 && tid >= gt + 32 + ct && tid < gt + 64 + ct) {
+    // ===================== converter warp (G32 only) ======================
+    // the warp past the CG group: each landed stage (binary64 from TMA) is
+    // converted in place to binary32 for the Gram warps (conv[s]), in ring order
+    const int lane = tid & 31;
+#pragma unroll 1
+    for (long gc = 0; gc < total; ++gc) {
+      const int s = (int)(gc % G.S);
+      FPM_PWAIT(&full[s], (uint32_t)((gc / G.S) & 1));
+      double2* sbuf = stages + s * stage_elems;
+      g32_convert(sbuf, R * G.MC * Np, lane);
+      g32_convert(sbuf + R * G.MC * Np, R * G.MC, lane);
+      fence_proxy_async();  // these generic-proxy writes precede the next TMA into the stage
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&conv[s]);
     }
     } else if (tid >= cbase && tid < cbase + ct && !args.gram_A) {
     // ============================ CG warps ============================
@@ -901,8 +936,8 @@ int launch_detect_ws_t(const DetectArgs& a, const WsLayout& sl, int grid, cudaSt
   const int threads = a.ws_gt + 32 + a.ws_ct;
   if constexpr (NB == 32 && K != FK_F64 && K != FK_GEN) {
     if (a.gram32) {  // binary32 Gram (FP32-Gram extension): N = 128, two passes of 256 Gram threads
-      if (a.ws_gt != 256 || threads > 512) return FPM_EUNSUPPORTED;
-      if (threads < 512) b.ws_order = 0;
+      if (a.ws_gt != 256 || a.ws_ncg != 1 || threads > 480) return FPM_EUNSUPPORTED;  // + the converter warp
+      b.ws_order = 0;
       auto k = fpm_detect_ws_kernel<WK, K, NB, LB, FPM_WS_GRAM_REGS, 2, 1>;
       if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, a.smem_bytes) != cudaSuccess)
         return FPM_ECUDA;

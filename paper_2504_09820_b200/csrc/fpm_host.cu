@@ -582,6 +582,10 @@ static bool plan_detect_ws(int M, int N, int L, int bj, int iters, int mvk, int 
           const int ct_def = (ncg == 1 && gt == 256 && N != 32) ? 192 : cg_threads(R, gt);
           // FPM_WS_CT override: whole warps, at least two, within the 512-thread block
           a.ws_ct = std::min(std::max(env_int("FPM_WS_CT", ct_def) / 32 * 32, 64), 512 - gt - 32);
+          if (a.gram32) {  // G32: one CG group and a spare warp (the binary32 converter)
+            if (ncg != 1) continue;
+            a.ws_ct = std::min(a.ws_ct, 512 - gt - 64);
+          }
           a.ws_ncg = ncg;
           a.ws_ct0 = ncg == 2 ? 128 : a.ws_ct;
           a.ws_nslot = nslot;
