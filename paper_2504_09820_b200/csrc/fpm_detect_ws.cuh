@@ -118,6 +118,17 @@ __device__ __forceinline__ void xchain_add(double (&c)[X], const double2 (&h)[X]
   }
 }
 
+// pairs (0,1), (2,3) exchanged when s (register selects; the loads were pair-swapped)
+__device__ __forceinline__ void swap_pairs(double2 (&h)[4], int s) {
+  if (s) {
+    const double2 t0 = h[0], t2 = h[2];
+    h[0] = h[1];
+    h[1] = t0;
+    h[2] = h[3];
+    h[3] = t2;
+  }
+}
+
 // ---- FP32-Gram extension (G32): rows of a stage converted in place to binary32 ----
 // operands of one row of a binary32 Gram job (circulant: hi[4] hj[4]; half:
 // hx[4] hy[2] hz[4])
@@ -397,6 +408,15 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const __grid_cons
       const GramJob job = kNpass == 1 ? job0 : gram_job(tid + pass * gt, R, nb);
       const int joff = job.g * G.MC * Np;
       const bool active = job.g >= 0 && job.g < Rv;
+      // nb = 4 (c1: 8 jobs per realization, two realizations per quarter-warp,
+      // realization blocks 0 mod 128 bytes apart): odd realizations load their
+      // operand pairs swapped (u ^ 1), so the two realizations' LDS.128 of one
+      // instruction fall in different bank halves (2-way conflicts otherwise);
+      // the triangle operands are swapped back in registers, the rest is
+      // undone in the hand-off's index map
+      constexpr bool kPerm = NB == 4;
+      const int psw = kPerm ? (job.g & 1) : 0;
+      const int pu[4] = {nb * (0 ^ psw), nb * (1 ^ psw), nb * (2 ^ psw), nb * (3 ^ psw)};
       double2 acc[16];
 #pragma unroll
       for (int k = 0; k < 16; ++k) acc[k] = make_double2(0.0, 0.0);
@@ -449,9 +469,9 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const __grid_cons
           double2 hi[4], hj[4], hc = make_double2(0.0, 0.0);
           double y1 = 0.0, y2 = 0.0;
 #pragma unroll
-          for (int u = 0; u < 4; ++u) hi[u] = pa[nb * u];
+          for (int u = 0; u < 4; ++u) hi[u] = pa[pu[u]];
 #pragma unroll
-          for (int v = 0; v < 4; ++v) hj[v] = pc[nb * v];
+          for (int v = 0; v < 4; ++v) hj[v] = pc[pu[v]];
           if (kChainInLoop) {
             hc = hcp[0];
             y1 = y1p[0];
@@ -463,9 +483,9 @@ FPM_PIPE_UNROLL
             double2 ni[4], nj[4], nhc = hc;
             double ny1 = y1, ny2 = y2;
 #pragma unroll
-            for (int u = 0; u < 4; ++u) ni[u] = pa[mn * Np + nb * u];
+            for (int u = 0; u < 4; ++u) ni[u] = pa[mn * Np + pu[u]];
 #pragma unroll
-            for (int v = 0; v < 4; ++v) nj[v] = pc[mn * Np + nb * v];
+            for (int v = 0; v < 4; ++v) nj[v] = pc[mn * Np + pu[v]];
             if (kChainInLoop) {
               nhc = hcp[mn * Np];
               ny1 = y1p[2 * mn];
@@ -502,11 +522,12 @@ FPM_PIPE_UNROLL
           double2 hx[4], hy[2], hz[4], hc = make_double2(0.0, 0.0);
           double y1 = 0.0, y2 = 0.0;
 #pragma unroll
-          for (int u = 0; u < 4; ++u) hx[u] = pa[nb * u];
+          for (int u = 0; u < 4; ++u) hx[u] = pa[pu[u]];
+          if (kPerm) swap_pairs(hx, psw);
 #pragma unroll
-          for (int w = 0; w < 2; ++w) hy[w] = py[nb * w];
+          for (int w = 0; w < 2; ++w) hy[w] = py[nb * (w ^ psw)];
 #pragma unroll
-          for (int v = 0; v < 4; ++v) hz[v] = pc[nb * v];
+          for (int v = 0; v < 4; ++v) hz[v] = pc[pu[v]];
           if (kChainInLoop) {
             hc = hcp[0];
             y1 = y1p[0];
@@ -518,11 +539,12 @@ FPM_PIPE_UNROLL
             double2 nx[4], ny[2], nz[4], nhc = hc;
             double ny1 = y1, ny2 = y2;
 #pragma unroll
-            for (int u = 0; u < 4; ++u) nx[u] = pa[mn * Np + nb * u];
+            for (int u = 0; u < 4; ++u) nx[u] = pa[mn * Np + pu[u]];
+            if (kPerm) swap_pairs(nx, psw);
 #pragma unroll
-            for (int w = 0; w < 2; ++w) ny[w] = py[mn * Np + nb * w];
+            for (int w = 0; w < 2; ++w) ny[w] = py[mn * Np + nb * (w ^ psw)];
 #pragma unroll
-            for (int v = 0; v < 4; ++v) nz[v] = pc[mn * Np + nb * v];
+            for (int v = 0; v < 4; ++v) nz[v] = pc[mn * Np + pu[v]];
             if (kChainInLoop) {
               nhc = hcp[mn * Np];
               ny1 = y1p[2 * mn];
@@ -617,7 +639,7 @@ FPM_PIPE_UNROLL
                 Agl[(long)i * N + jx] = vij;
                 Agl[(long)jx * N + i] = vji;
               },
-              [&](int i, double2 vii) { Agl[(long)i * N + i] = vii; });
+              [&](int i, double2 vii) { Agl[(long)i * N + i] = vii; }, psw);
         }
         if (pass + 1 < npass) continue;
         if (kNpass != 1) {
@@ -689,7 +711,7 @@ FPM_PIPE_UNROLL
           gram32_entries(job, acc32, nb, N, __double2float_rn(args.sigma2), put, put_diag);
           gram32_entries(job1, acc32b, nb, N, __double2float_rn(args.sigma2), put, put_diag);
         } else {
-          gram_entries(job, acc, nb, N, args.sigma2, put, put_diag);
+          gram_entries(job, acc, nb, N, args.sigma2, put, put_diag, psw);
         }
       }
       if (pass + 1 < npass) continue;

@@ -296,13 +296,16 @@ FPM_ROW_UNROLL
 // for i != j (both orientations' bits), d(i, value_ii) for diagonal entries.
 template <class F, class D>
 __device__ __forceinline__ void gram_entries(const GramJob& job, const double2 (&acc)[16], int nb, int N,
-                                             double sigma2, F&& f, D&& d) {
+                                             double sigma2, F&& f, D&& d, int sp = 0) {
+  // sp = 1: the job's circulant rows / columns and its cross-block rows and
+  // columns were accumulated in pair-swapped order (u ^ 1; see the
+  // warp-specialised kernel's bank-conflict note at nb = 4)
   if (!job.half) {
 #pragma unroll
     for (int u = 0; u < 4; ++u)
 #pragma unroll
       for (int v = 0; v < 4; ++v) {
-        const int i = job.a + nb * u, j = job.c + nb * v;
+        const int i = job.a + nb * (u ^ sp), j = job.c + nb * (v ^ sp);
         if (i < N && j < N) f(i, j, gram_final(acc[u * 4 + v]), gram_mirror(acc[u * 4 + v]));
       }
   } else {
@@ -319,7 +322,7 @@ __device__ __forceinline__ void gram_entries(const GramJob& job, const double2 (
     for (int w = 0; w < 2; ++w)
 #pragma unroll
       for (int v = 0; v < 4; ++v) {
-        const int i = job.y + nb * (job.yo + w), j = job.c + nb * v;
+        const int i = job.y + nb * (job.yo + (w ^ sp)), j = job.c + nb * (v ^ sp);
         if (i < N && j < N) f(i, j, gram_final(acc[6 + w * 4 + v]), gram_mirror(acc[6 + w * 4 + v]));
       }
     const double dg[4] = {acc[14].x, acc[14].y, acc[15].x, acc[15].y};
