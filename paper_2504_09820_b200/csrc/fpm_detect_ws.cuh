@@ -320,7 +320,7 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const __grid_cons
       mbar_init(&empty[s], gt / 32);
     }
     for (int k = 0; k < 2; ++k) {
-      mbar_init(&sfull[k], 1);
+      mbar_init(&sfull[k], gt / 32);
       mbar_init(&sempty[k], 1);
     }
     if constexpr (G32)
@@ -746,9 +746,12 @@ FPM_PIPE_UNROLL
           reinterpret_cast<double*>(bS + g * N + (e - part * N))[part] = bsm[q];
         }
       }
-      gbar.sync();
+      // every Gram warp publishes its own part of the slot (sfull counts the
+      // Gram warps): a warp that is done goes straight on to the next group
+      // instead of waiting for the slowest one at a group barrier
+      __syncwarp();
       diag_jitter(args.debug, 5, j);
-      if (tid == 0) mbar_arrive(&sfull[slot]);
+      if ((tid & 31) == 0) mbar_arrive(&sfull[slot]);
       if (tr && tid == 0 && j < 8) tr[j * 8 + 3] = clock64();
     }
   } else {
