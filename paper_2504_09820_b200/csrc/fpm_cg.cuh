@@ -295,6 +295,56 @@ __device__ __noinline__ double2 mv_row_f64(const double2* row, const double2* pv
   return assemble(s.x, s.y);
 }
 
+// one matvec row at binary64 with the row in TENSOR MEMORY (the fused
+// kernel's fp64 A, one row per TMEM lane, entry k at columns 4k..4k+3 from
+// ta): 4-entry chunks by tcgen05.ld 32x32b.x16, the next chunk in flight
+// while this chunk's products and adds run; p from shared memory in a ring
+// of kD terms (same order of operations as mv_row_f64).  Warp-collective:
+// every lane of the warp calls it.
+template <int NC>
+__device__ __noinline__ double2 mv_row_tm64(uint32_t ta, const double2* pv) {
+  constexpr int kD = 5;
+  static_assert(NC % 4 == 0 && NC >= 8, "TMEM row: whole 4-entry chunks");
+  const uint32_t pa = smem_u32(pv);
+  uint32_t cur[16], nxt[16];
+  tmx_ld16(cur, ta);
+  double2 p[kD];
+#pragma unroll
+  for (int j = 0; j < kD; ++j) p[j] = v64::ld(pa + 16 * j);
+  tmx_wait_ld();
+  tmx_launder(cur);
+  double2 s = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int c = 0; c < NC / 4; ++c) {
+    if (c + 1 < NC / 4) tmx_ld16(nxt, ta + 16 * (c + 1));
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int k = 4 * c + j;
+      const double2 a = make_double2(__hiloint2double(cur[4 * j + 1], cur[4 * j]),
+                                     __hiloint2double(cur[4 * j + 3], cur[4 * j + 2]));
+      const double2 t = v64::cmul(a, p[k % kD]);
+      if (k + kD < NC) p[k % kD] = v64::ld(pa + 16 * (k + kD));
+      s = k == 0 ? t : make_double2(v64::add(s.x, t.x), v64::add(s.y, t.y));
+    }
+    if (c + 1 < NC / 4) {
+      tmx_wait_ld();
+      tmx_launder(nxt);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) cur[j] = nxt[j];
+    }
+  }
+  return assemble(s.x, s.y);
+}
+
+// where a CG group finds the fused kernel's fp64 A in tensor memory: base =
+// TMEM address of the hand-off slot (lane field 0), qw0 = CTA warp index of
+// the group's first warp, nw = its warps.  Row q = g*N + i lives in TMEM lane
+// q % 128 at columns base + (q / 128) * 4N.
+struct TmRows {
+  uint32_t base;
+  int qw0, nw;
+};
+
 // Compile-time N (NC > 0): the whole sum is one basic block, so the
 // scheduler overlaps every load and product with the dependent add chain
 // (the loop versions above issue in order: a block's adds stall the next
@@ -501,9 +551,10 @@ struct NamedBar {
 // beta, divergence) | F (commit x, r; p update).  NC > 0: N known at
 // compile time (fully unrolled sums).  Ragged blocks (LB == 0 with BJ)
 // take one more barrier between the r updates and z.
-template <int WK, int K, int LB, int NC = 0, class Bar>
+template <int WK, int K, int LB, int NC = 0, bool TM = false, class Bar>
 __device__ void cg_group(CgSmem<K>& S, int Rv, int iters, bool bj, bool textbook, const Prec& pr, int nthreads,
-                         int tid, Bar& bar, long long* tr = nullptr) {
+                         int tid, Bar& bar, long long* tr = nullptr, TmRows tmr = TmRows{0, 0, 0}) {
+  static_assert(!TM || (K == FK_F64 && NC > 0), "A in tensor memory: binary64 matvec, compile-time N");
   typedef Ar<K> A;
   typedef typename A::C C;
   const int N = NC > 0 ? NC : S.N;
@@ -595,6 +646,26 @@ __device__ void cg_group(CgSmem<K>& S, int Rv, int iters, bool bj, bool textbook
 #pragma unroll 1
   for (int it = 1; it <= iters; ++it) {
     // ---- A: w = A p (u_MV) + phi terms;  rho0 = sum r^H p (BJ as_written) ----
+    if constexpr (TM) {
+      // rows by TMEM lane ownership: this warp reads lane quarter Q; the
+      // group's warps of one quarter share its 128-row blocks
+      const int wi = tid >> 5, lane = tid & 31;
+      const int Q = (tmr.qw0 + wi) & 3;
+      const int nQ = (tmr.nw - 1 - (wi & 3)) / 4 + 1;
+      const int nRB = (S.R * N + 127) / 128;
+#pragma unroll 1
+      for (int RB = wi >> 2; RB < nRB; RB += nQ) {
+        const int q = RB * 128 + Q * 32 + lane;
+        const int g = q / N;
+        const C wc = mv_row_tm64<NC>(tmr.base + ((uint32_t)(Q * 32) << 16) + (uint32_t)(RB * 4 * N), S.pmv + g * N);
+        if (g < Rv && S.fl[g * 4]) {
+          S.w[q] = A::wide(wc);
+          const C pi = A::rnd(S.p[q], fm);
+          S.tphi[q] = A::mulc(pi, mv_to_ip(wc), fi);
+        }
+      }
+      tmx_fence_before();  // this sweep's TMEM reads precede the slot's release
+    } else
 #pragma unroll 1
     for (int k = 0; k < nrow; ++k) {
       const int q = tid + k * nthreads;

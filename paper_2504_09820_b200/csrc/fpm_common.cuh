@@ -57,6 +57,8 @@ struct DetectArgs {
   int cg_stride;       // bytes between the two CG groups' state regions
   int ws_nslot;        // hand-off slots (2 double-buffered, 1 when two do not fit)
   int ws_npass;        // Gram passes per group (2 at N = 128: 512 jobs on 256 Gram threads)
+  int ws_tmem;         // fp64 A of the hand-off in tensor memory (two TMEM slots), staged through off_stg
+  int ws_rr, off_stg;  // rows per staging round, staging offset (pitch N + 1 double2)
   int debug;  // diagnostic bits (FPM_DEBUG): 1 = WS kernel skips the CG side
   int composed;  // no fused plan fits: fpm_gram -> fpm_bj_setup -> fpm_cg -> slicer
   int gram32;    // FPM_FLAG_GRAM_FP32: binary32 Gram (extension): fused WS kernel at N = 128, else composed

@@ -256,8 +256,13 @@ __device__ __forceinline__ int nsl_of(const DetectArgs& a) { return a.ws_nslot; 
 // RS > 0: register split (setmaxnreg) for a 512-thread block: the GWG Gram
 // warp groups (gt = 128 * GWG) run with RS registers per thread, the other
 // 4 - GWG (producer + CG + idle warps) with the rest of the register file.
-template <int WK, int K, int NB, int LB, int RS, int GWG = 2, int G32 = 0>
+template <int WK, int K, int NB, int LB, int RS, int GWG = 2, int G32 = 0, int TA = 0>
 __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const __grid_constant__ DetectArgs args, const WsLayout sl) {
+  // TA: the fp64 matrix of the hand-off lives in TENSOR MEMORY (two 256-column
+  // slots, row q of a group in lane q % 128), staged through a small
+  // shared-memory area in rounds -- the 128 KB of shared memory an fp64 A
+  // slot took go to the H ring, and two slots decouple the Gram and the CG
+  static_assert(!TA || (K == FK_F64 && (NB == 16 || NB == 4)), "A in tensor memory: fp64 matvec, N = 16 / 64");
   // G32: binary32 Gram (FP32-Gram extension, BASELINE c4); only N = 128 (one
   // realization per group, two Gram passes) is instantiated
   static_assert(!G32 || NB == 32, "binary32 Gram: N = 128 only");
@@ -293,6 +298,7 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const __grid_cons
   double2* stages = reinterpret_cast<double2*>(smem + args.off_union);
   unsigned char* slots = smem + args.off_slot;
   __shared__ unsigned long long cnt[FPM_NCOUNTERS];
+  __shared__ uint32_t tm_slot;  // TA: tensor-memory base address (tcgen05.alloc)
   // diagnostic timeline of CTA 0, groups 0..7: [j*8 + 0] gram loop start,
   // 1 gram loop end, 2 slot acquired, 3 hand-off done, 4 cg start, 5 cg end
   long long* tr = (diag_trace(args.trace) && blockIdx.x == 0) ? diag_trace(args.trace) : nullptr;
@@ -328,7 +334,16 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const __grid_cons
     fence_mbar_init();
   }
   if (tid < FPM_NCOUNTERS) cnt[tid] = 0ULL;
+  if constexpr (TA) {
+    if (tid < 32) tmx_alloc(&tm_slot, 512);
+    tmx_fence_before();
+  }
   __syncthreads();
+  uint32_t tm_base = 0;
+  if constexpr (TA) {
+    tmx_fence_after();
+    tm_base = tm_slot;
+  }
 
   const int stage_elems = ws_stage_elems(G);  // H rows, then the rows' y entries
   // N = 128: the 512 Gram jobs of a realization run as two passes of 256
@@ -685,7 +700,82 @@ FPM_PIPE_UNROLL
       double2* dS = reinterpret_cast<double2*>(sp + sl.d);
       const int nbt = R * nblk;
       const bool onchip = args.bj && !args.minv_in;
-      if (active) {
+      if constexpr (TA) {
+        // fp64 A -> tensor memory slot `slot`, in rounds of RR rows through the
+        // staging area (pitch N + 1: conflict-free row reads); the Gram warps
+        // of a lane quarter move that quarter's rows (tcgen05.st 32x32b)
+        const int RR = args.ws_rr, RNt = R * N, pitch = N + 1;
+        double2* stg = reinterpret_cast<double2*>(smem + args.off_stg);
+        const int wg = tid >> 5, lane = tid & 31;
+        const int Q = (gbase / 32 + wg) & 3;
+        const int nwq = gt / 128, kq = wg >> 2;  // Gram warps per lane quarter, this warp's rank
+        const uint32_t tslot = tm_base + (uint32_t)(slot * 256);
+        double2* dg = dS + job.g * nblk;
+        tmx_fence_after();  // the CG's reads of this slot (released through sempty) came first
+        long long tw = 0, tmv = 0, tc0 = 0;  // diagnostic: time in entry writes / moves (thread 0)
+#pragma unroll 1
+        for (int r0 = 0; r0 < RNt; r0 += RR) {
+          if (tr && tid == 0 && j < 8) tc0 = clock64();
+          if (active) {
+            const int qg = job.g * N - r0;
+            gram_entries(
+                job, acc, nb, N, args.sigma2,
+                [&](int i, int jx, double2 vij, double2 vji) {
+                  if ((unsigned)(qg + i) < (unsigned)RR) stg[(qg + i) * pitch + jx] = vij;
+                  if ((unsigned)(qg + jx) < (unsigned)RR) stg[(qg + jx) * pitch + i] = vji;
+                  if (onchip && r0 == 0) {
+                    const int kb = i / L;
+                    if (kb == jx / L) {
+                      const int il = i - kb * L, jl = jx - kb * L;
+                      dg[(il * L + jl) * nbt + kb] = vij;
+                      dg[(jl * L + il) * nbt + kb] = vji;
+                    }
+                  }
+                },
+                [&](int i, double2 vii) {
+                  if ((unsigned)(qg + i) < (unsigned)RR) stg[(qg + i) * pitch + i] = vii;
+                  if (onchip && r0 == 0) {
+                    const int kb = i / L, il = i - kb * L;
+                    dg[(il * L + il) * nbt + kb] = vii;
+                  }
+                },
+                psw);
+          }
+          gbar.sync();
+          if (tr && tid == 0 && j < 8) {
+            const long long t1 = clock64();
+            tw += t1 - tc0;
+            tc0 = t1;
+          }
+#pragma unroll 1
+          for (int qb = r0; qb < r0 + RR; qb += 32) {
+            if (((qb >> 5) & 3) != Q) continue;  // warp-uniform
+            const int srow = qb - r0 + lane, RB = qb >> 7, per = N / nwq;
+            const uint32_t ta = tslot + ((uint32_t)(Q * 32) << 16) + (uint32_t)(RB * 4 * N);
+#pragma unroll 2
+            for (int e = kq * per; e < (kq + 1) * per; e += 4) {
+              uint32_t v[16];
+#pragma unroll
+              for (int jj = 0; jj < 4; ++jj) {
+                const double2 a = stg[srow * pitch + e + jj];
+                v[4 * jj] = __double2loint(a.x);
+                v[4 * jj + 1] = __double2hiint(a.x);
+                v[4 * jj + 2] = __double2loint(a.y);
+                v[4 * jj + 3] = __double2hiint(a.y);
+              }
+              tmx_st16(ta + (uint32_t)(4 * e), v);
+            }
+          }
+          gbar.sync();  // the staging area is free for the next round
+          if (tr && tid == 0 && j < 8) tmv += clock64() - tc0;
+        }
+        tmx_wait_st();
+        tmx_fence_before();
+        if (tr && tid == 0 && j < 8) {
+          tr[j * 8 + 6] = tw;
+          tr[j * 8 + 7] = tmv;
+        }
+      } else if (active) {
         C* Ag = At + job.g * N * ldA;
         double2* dg = dS + job.g * nblk;
         auto put = [&](int i, int jx, double2 vij, double2 vji) {
@@ -828,18 +918,20 @@ FPM_PIPE_UNROLL
     S.dbg = diag_bits(args.debug);
     double2* vec = reinterpret_cast<double2*>(cgs + args.off_vec);
     const int RN = R * N;
-    S.x = vec + RN;
-    S.r = vec + 2 * RN;
-    S.p = vec + 3 * RN;
-    S.z = vec + 4 * RN;
-    S.w = vec + 5 * RN;
-    S.xn = vec + 6 * RN;
-    S.rn = vec + 7 * RN;
+    // z only with block-Jacobi, the rho0 terms only for BJ as_written: they
+    // come last so the planner can leave them out (ws_cg_layout)
+    S.x = vec;
+    S.r = vec + RN;
+    S.p = vec + 2 * RN;
+    S.w = vec + 3 * RN;
+    S.xn = vec + 4 * RN;
+    S.rn = vec + 5 * RN;
+    S.z = vec + 6 * RN;
     S.pmv = reinterpret_cast<P*>(cgs + args.off_pmv);
     S.tphi = reinterpret_cast<C*>(cgs + args.off_tip);
-    S.trho = S.tphi + RN;
-    S.tr1 = S.trho + RN;
+    S.tr1 = S.tphi + RN;
     S.rip = S.tr1 + RN;
+    S.trho = S.rip + RN;
     S.sc = reinterpret_cast<double2*>(cgs + args.off_sc);
     S.fl = reinterpret_cast<int*>(cgs + args.off_fl);
     double2* scr2 = reinterpret_cast<double2*>(cgs + args.off_scr2);
@@ -856,6 +948,7 @@ FPM_PIPE_UNROLL
       S.b = reinterpret_cast<double2*>(sp + sl.b);
       double2* dS = reinterpret_cast<double2*>(sp + sl.d);
       FPM_CWAIT(&sfull[slot], (uint32_t)(use & 1));
+      if constexpr (TA) tmx_fence_after();
       diag_jitter(args.debug, 6, j);
       if (tr && lt == 0 && j < 8) tr[j * 8 + 4] = clock64();
 #pragma unroll 1
@@ -899,7 +992,9 @@ FPM_PIPE_UNROLL
         __shared__ int _fpm_dummy_ws;
         tc[60] = (long long)clock64() + (*(volatile int*)&_fpm_dummy_ws == 0x7fffffff);
       }
-      if (!(diag_bits(args.debug) & 1)) cg_group<WK, K, LB, kCgNC>(S, Rv, args.iters, args.bj != 0, args.textbook != 0, args.pr, ctg, lt, cbar, tc);
+      if (!(diag_bits(args.debug) & 1))
+        cg_group<WK, K, LB, kCgNC, TA != 0>(S, Rv, args.iters, args.bj != 0, args.textbook != 0, args.pr, ctg, lt, cbar,
+                                            tc, TmRows{tm_base + (uint32_t)(slot * 256), cbase / 32, ctg / 32});
       // slot no longer needed (A, b, diagonal blocks consumed)
       diag_jitter(args.debug, 7, j);
       if (lt == 0) mbar_arrive(&sempty[slot]);
@@ -937,8 +1032,15 @@ FPM_PIPE_UNROLL
     }
     }
   }
+  if constexpr (TA) tmx_fence_before();
   __syncthreads();
   if (tid < FPM_NCOUNTERS && cnt[tid]) atomicAdd(&args.counters[tid], cnt[tid]);
+  if constexpr (TA) {
+    if (tid < 32) {
+      tmx_fence_after();
+      tmx_dealloc(tm_base, 512);
+    }
+  }
 }
 
 #ifndef FPM_WS_GRAM_REGS_WIDE  // 16-byte matvec terms (fp64 / generic): the CG side needs more
@@ -959,6 +1061,19 @@ int launch_detect_ws_t(const DetectArgs& a, const WsLayout& sl, int grid, cudaSt
   DetectArgs b = a;
   b.ws_order = env_order(a.ws_order);
   const int threads = a.ws_gt + 32 + a.ws_ct;
+  if constexpr (K == FK_F64 && (NB == 16 || NB == 4)) {
+    if (a.ws_tmem) {  // fp64 A in tensor memory: two Gram warp groups, Gram-first order
+      if (a.ws_gt != 256 || a.ws_ncg != 1 || a.ws_nslot != 2 || threads > 512) return FPM_EUNSUPPORTED;
+      if (threads < 512) b.ws_order = 0;
+      auto k = fpm_detect_ws_kernel<WK, K, NB, LB, FPM_WS_GRAM_REGS_WIDE, 2, 0, 1>;
+      if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, a.smem_bytes) != cudaSuccess)
+        return FPM_ECUDA;
+      k<<<(unsigned)grid, 512, a.smem_bytes, st>>>(b, sl);
+      count_launch();
+      return cudaGetLastError() == cudaSuccess ? FPM_OK : FPM_ECUDA;
+    }
+  }
+  if (a.ws_tmem) return FPM_EUNSUPPORTED;
   if constexpr (NB == 32 && K != FK_F64 && K != FK_GEN) {
     if (a.gram32) {  // binary32 Gram (FP32-Gram extension): N = 128, two passes of 256 Gram threads
       if (a.ws_gt != 256 || a.ws_ncg != 1 || threads > 480) return FPM_EUNSUPPORTED;  // + the converter warp

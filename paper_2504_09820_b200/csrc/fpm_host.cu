@@ -500,6 +500,17 @@ static bool plan_detect_ws(int M, int N, int L, int bj, int iters, int mvk, int 
   auto try_R = [&](const int R, const int npass) -> bool {
     const int Lb = bj ? L : 1;
     const int gt = R * nb * nb / 2 / npass;
+    // FPM_TMEM_A (opt-in, measured slower): fp64 A in tensor memory (two
+    // 256-column slots; row q in lane q % 128) for fp64 matvec / inner at
+    // N = 16 / 64 with whole 128-row blocks.  c5 fp64: the freed 128 KB of
+    // shared memory speed the Gram loop up (114 K -> 103 K cycles per group),
+    // but the staged hand-off (entries -> shared-memory rounds -> tcgen05.st by
+    // the lane-quarter owners) costs 20-25 K cycles per group against 3-4 K
+    // for a shared-memory slot: 0.55 vs 0.63 of FP64; c1 at R = 32 spills
+    // its 4-chain tile loop at 136 registers (0.32 vs 0.40)
+    const bool tm = knob("FPM_TMEM_A") && mvk == FK_F64 && ipk == FK_F64 && ((N == 16 && !bj) || (N == 64 && bj && L == 4)) && N == Np &&
+                    gt == 256 &&
+                    (long)R * N * N <= 8192 && (R * N) % 128 == 0 && !a.gram32;
     // two CG groups (alternating hand-off slots) when the Gram side is two full
     // warp groups: 512 threads = 256 Gram + 32 producer + 128 + 96 CG
     const int ncg_env = env_int("FPM_WS_NCG", 0);
@@ -517,13 +528,14 @@ static bool plan_detect_ws(int M, int N, int L, int bj, int iters, int mvk, int 
     const int(*cand)[2] = cg_short ? cand_short : cand_long;
     const int stage_short[6] = {32, 24, 20, 16, 12, 8};
     for (int ci = 0; ci < 4; ++ci) {
-      const int ncg = cand[ci][0], nslot = cand[ci][1];
+      const int ncg = tm ? 1 : cand[ci][0], nslot = tm ? 2 : cand[ci][1];
+      if (tm && ci > 0) break;
       if (ncg == 2 && gt != 256) continue;
       if (ncg_env && ncg != ncg_env) continue;
       if (env_int("FPM_WS_NSLOT", 0) && nslot != env_int("FPM_WS_NSLOT", 0)) continue;
       for (int si = 0; si < 6; ++si) {
         const int stage_kb = env_int("FPM_STAGE_KB", 0) ? env_int("FPM_STAGE_KB", 0)
-                             : (ncg == 1 && nslot == 1 && cg_short ? stage_short[si] : stage_list[si]);
+                             : ((ncg == 1 && nslot == 1 && cg_short) || tm ? stage_short[si] : stage_list[si]);
         if (env_int("FPM_STAGE_KB", 0) && si > 0) break;
         GramGeom G;
         gram_geom(R, M, N, G, stage_kb);
@@ -532,7 +544,8 @@ static bool plan_detect_ws(int M, int N, int L, int bj, int iters, int mvk, int 
         // for every realization.  A second slot / CG group is not worth stages
         // of fewer than 4 antenna rows (per-stage hand-shakes and TMA latency
         // then starve the Gram warps: c1 0.16 -> 0.09 of FP64 measured)
-        if ((ncg > 1 || nslot > 1) && G.MC < std::min(4, M)) continue;
+        // (tensor-memory A: one 3-D TMA per stage, so 2-row stages are fine)
+        if ((ncg > 1 || nslot > 1) && G.MC < std::min(tm ? 2 : 4, M)) continue;
         const int ldA = lda_for(N, mv_bytes(mvk));
         size_t off = 256;  // mbarriers: full[S], empty[S], (2 unused), sfull[2], sempty[2]
         if ((a.gram32 ? 3 * G.S + 6 : 2 * G.S + 8) * 8 > 256) continue;  // + conv[S] (G32)
@@ -540,19 +553,30 @@ static bool plan_detect_ws(int M, int N, int L, int bj, int iters, int mvk, int 
         off = align_up(off + (size_t)G.S * ws_stage_elems(G) * 16, 128);
         a.off_ys = (int)off;  // (no separate y buffer: y rows ride in the stages)
         sl.at = 0;
-        sl.b = (int)align_up((size_t)R * N * ldA * mv_bytes(mvk), 128);
+        sl.b = tm ? 0 : (int)align_up((size_t)R * N * ldA * mv_bytes(mvk), 128);  // tm: A lives in TMEM
         sl.d = (int)align_up(sl.b + (size_t)R * N * 16, 128);
         sl.bytes = (int)align_up(sl.d + (bj ? (size_t)R * N * Lb * 16 : 0), 128);
         a.off_slot = (int)off;
         off = align_up(off + (size_t)nslot * sl.bytes, 128);
         a.off_bsm = (int)off;  // matched-filter chain accumulators
         off = align_up(off + (size_t)2 * R * N * 8, 128);
+        a.ws_tmem = tm;
+        a.ws_rr = 0;
+        a.off_stg = 0;
+        if (tm) {  // staging of the TMEM hand-off: RR rows at pitch N + 1
+          a.ws_rr = env_int("FPM_TM_RR", 64);
+          a.off_stg = (int)off;
+          off = align_up(off + (size_t)a.ws_rr * (N + 1) * 16, 128);
+        }
         // ---- per-CG-group state (replicated ncg times, cg_stride apart) ----
         const size_t cg0 = off;
         a.off_minv = (int)off;
         off = align_up(off + (bj ? (size_t)R * N * Lb * 16 : 0), 128);
         a.off_vec = (int)off;
-        off = align_up(off + (size_t)8 * R * N * 16, 128);
+        // x r p w xn rn (+ z with block-Jacobi); the inverse's scratch reuses it
+        off = align_up(off + std::max<size_t>((size_t)(bj ? 7 : 6) * R * N * 16,
+                                              (bj && Lb <= 8) ? (size_t)R * N * Lb * 16 : 0),
+                       128);
         // the inverse's scratch is dead before the CG vectors are initialised
         if (!bj || Lb <= 8) {
           a.off_scr2 = a.off_vec;
@@ -563,7 +587,8 @@ static bool plan_detect_ws(int M, int N, int L, int bj, int iters, int mvk, int 
         a.off_pmv = (int)off;
         off = align_up(off + (size_t)R * N * p_bytes(mvk), 128);
         a.off_tip = (int)off;
-        off = align_up(off + (size_t)4 * R * N * mv_bytes(ipk), 128);
+        // phi, rho1 / carry, r at u_IP (+ the rho0 terms for BJ as_written)
+        off = align_up(off + (size_t)(bj && !a.textbook ? 4 : 3) * R * N * mv_bytes(ipk), 128);
         a.off_sc = (int)off;
         off = align_up(off + (size_t)R * 8 * 16, 128);
         a.off_fl = (int)off;
@@ -709,7 +734,8 @@ static int launch_detect_ws(const Kinds& k, const DetectArgs& a0, const WsLayout
   if (a.gram_A && nb == 16) lb = 4;  // Gram-only: any LB; take the N = 64 specialisation
   if (a.G.N != a.G.Np) nb = 0;
   if (knob("FPM_NO_SPEC")) nb = lb = 0;
-  note_kernel(a.gram32 ? "fpm_detect_ws_kernel[gram32]" : "fpm_detect_ws_kernel", k, nb, lb);
+  note_kernel(a.gram32 ? "fpm_detect_ws_kernel[gram32]" : a.ws_tmem ? "fpm_detect_ws_kernel[tmemA]" : "fpm_detect_ws_kernel",
+              k, nb, lb);
   if (k.w == FK_GEN) return launch_detect_ws_gen_w(a, sl, grid, 0, 0, st);
   switch (k.mv) {
     case FK_F64: return launch_detect_ws_f64(a, sl, grid, nb, lb, st);

@@ -296,6 +296,40 @@ def test_child_multi_group_fallback():
     save_child_out(x=res2.x, k=np.array(_lib_last_kernel()))
 
 
+def test_tmem_matrix_variant_bit_exact():
+    """Opt-in variant (FPM_TMEM_A=1, measured slower): the fp64
+    matrix of the hand-off in tensor memory, staged through shared-memory
+    rounds and read back by the CG warps' lanes (tcgen05.st / tcgen05.ld).
+    Bit-exact vs the oracle with injected inverses at c5 fp64 over several
+    groups per CTA and a partial last group, and at N = 16 plain CG (R = 32)."""
+    o = run_knob_child("tests/test_gpu_parity.py::test_child_tmem_matrix", {"FPM_TMEM_A": "1"})
+    for tag in ("c5", "c1"):
+        assert "tmemA" in str(o["k_" + tag]), o["k_" + tag]
+        assert bits_equal(o["x_" + tag], o["ref_" + tag]), tag
+
+
+@knob_child
+def test_child_tmem_matrix():
+    import fpm_oracle as O
+    from paper_2504_09820_b200.detect import DetectorSpec, detect
+    out = {}
+    T = 148 * 2 * 2 + 1
+    H, y, bits, s2 = _oracle_inputs(128, 64, 0.5, 15.0, T)
+    A, b = O.gram_mf_einsum(H, y, s2)
+    mats = O.bj_inverses(A, 4)
+    det = DetectorSpec("fp_bj_cg", iters=8, L=4)
+    out["x_c5"] = detect(det, H, y, s2, bits, minv=mats).x
+    out["k_c5"] = np.array(_lib_last_kernel())
+    out["ref_c5"] = O.cg_batch(A, b, 8, O.FP64, O.FP64, O.FP64, mats).x
+    T = 32 * 148 + 5
+    H, y, bits, s2 = _oracle_inputs(128, 16, 0.0, 10.0, T)
+    A, b = O.gram_mf_einsum(H, y, s2)
+    out["x_c1"] = detect(DetectorSpec("cg", iters=8), H, y, s2, bits).x
+    out["k_c1"] = np.array(_lib_last_kernel())
+    out["ref_c1"] = O.cg_batch(A, b, 8, O.FP64, O.FP64, O.FP64, None).x
+    save_child_out(**out)
+
+
 HIST_EXACT = ("x", "breakdown_at", "diverged_at", "alphas", "betas", "converged_at", "iterates", "residual_vectors")
 HIST_NORMS = ("residual_norms", "iterate_norms", "b_norm")
 
