@@ -241,9 +241,15 @@ __device__ __forceinline__ double2 cmul(double2 a, double2 p) {
 
 // left-to-right sum of NC binary64 complex terms (chain_sum at u_IP = fp64);
 // terms requested kD ahead of their add
+#ifndef FPM_F64_DOT_RING  // binary64 terms in flight in a dot chain
+#define FPM_F64_DOT_RING 6
+#endif
+#ifndef FPM_F64_MV_RING  // (A, p) pairs in flight in a binary64 matvec row
+#define FPM_F64_MV_RING 5
+#endif
 template <int NC>
 __device__ __noinline__ double2 chain_sum_f64(const double2* t) {
-  constexpr int kD = 6;
+  constexpr int kD = FPM_F64_DOT_RING;
   const uint32_t a0 = smem_u32(t);
   double2 v[kD];
 #pragma unroll
@@ -262,7 +268,7 @@ __device__ __noinline__ double2 chain_sum_f64(const double2* t) {
 // kP terms ahead of their add
 template <int NC>
 __device__ __noinline__ double2 mv_row_f64(const double2* row, const double2* pv) {
-  constexpr int kD = 5, kP = 2;
+  constexpr int kD = FPM_F64_MV_RING, kP = 2;
   static_assert(NC >= kD, "row shorter than the operand ring");
   const uint32_t ra = smem_u32(row), pa = smem_u32(pv);
   double2 a[kD], p[kD], t[kP];

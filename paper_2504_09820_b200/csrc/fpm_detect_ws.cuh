@@ -381,11 +381,15 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const __grid_cons
     //   re += fl(fl(hr yr) + fl(hi yi)),  im += fl(fl(hr yi) - fl(hi yr))
     // (bit-identical to the split chains: fl(hi (-yr)) = -fl(hi yr)); the
     // split form needs 2.4x the shared-memory wavefronts per row
-    constexpr bool kPair = NB == 8 && RS > 0;
+    // N = 16 (nb = 4): two paired chains per thread, (g, n) and (g, n + 8),
+    // sharing the y load (the four split chains took 24 wavefronts per
+    // warp-row beside the tile's 32: shared memory near its bandwidth)
+    constexpr bool kPair = (NB == 8 || NB == 4) && RS > 0;
+    constexpr int kPPT = NB == 4 ? 2 : 1;  // paired chains per thread
     constexpr int kCPT = kPair ? 1 : (NB == 16 || NB == 32 || ((NB == 4 || NB == 8) && RS > 0)) ? (NB == 32 ? 1 : 16 / NB) : 0;
     constexpr bool kChainInLoop = kCPT > 0;
     constexpr int kXC = kCPT > 1 ? kCPT - 1 : 1;  // extra chains (array size >= 1)
-    const int cq_g = kPair ? tid / N : tid / (2 * N), cq_e = kPair ? tid - cq_g * N : tid - cq_g * 2 * N;
+    const int cq_g = kPair ? tid / (N / kPPT) : tid / (2 * N), cq_e = kPair ? tid - cq_g * (N / kPPT) : tid - cq_g * 2 * N;
     const int cq_part = kPair ? 0 : cq_e / N, cq_n = cq_e - cq_part * N;
     const int cq_hoff = cq_g * G.MC * Np + cq_n, cq_yoff = cq_g * G.MC;  // y: the stage's y block
     int xq_hoff[kXC], xq_yoff[kXC], xq_part[kXC];
@@ -405,8 +409,9 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const __grid_cons
       const int slot = nsl == 2 ? (j & 1) : 0;  // hand-off slot and its use count
       const int use = nsl == 2 ? (j >> 1) : j;
       const int nchain = 2 * Rv * N;
-      const bool chain_ok = kChainInLoop && tid < (kPair ? Rv * N : nchain);
+      const bool chain_ok = kChainInLoop && tid < (kPair ? Rv * N / kPPT : nchain);
       double ca = 0.0, cb = 0.0;  // cb: imaginary part of a paired chain
+      double ca2 = 0.0, cb2 = 0.0;  // kPPT = 2: the second paired chain (entry n + N/2)
       double cx[kXC];
 #pragma unroll
       for (int k = 0; k < kXC; ++k) cx[k] = 0.0;
@@ -487,10 +492,12 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const __grid_cons
           for (int u = 0; u < 4; ++u) hi[u] = pa[pu[u]];
 #pragma unroll
           for (int v = 0; v < 4; ++v) hj[v] = pc[pu[v]];
+          double2 hc2 = make_double2(0.0, 0.0);
           if (kChainInLoop) {
             hc = hcp[0];
             y1 = y1p[0];
             y2 = y2p[0];
+            if constexpr (kPPT == 2) hc2 = hcp[N / 2];
           }
 FPM_PIPE_UNROLL
           for (int mm = 0; mm < rows; ++mm) {
@@ -501,10 +508,12 @@ FPM_PIPE_UNROLL
             for (int u = 0; u < 4; ++u) ni[u] = pa[mn * Np + pu[u]];
 #pragma unroll
             for (int v = 0; v < 4; ++v) nj[v] = pc[mn * Np + pu[v]];
+            double2 nhc2 = hc2;
             if (kChainInLoop) {
               nhc = hcp[mn * Np];
               ny1 = y1p[2 * mn];
               ny2 = y2p[2 * mn];
+              if constexpr (kPPT == 2) nhc2 = hcp[mn * Np + N / 2];
             }
             double2 xh[kXC], xy[kXC];
             if constexpr (kCPT > 1) xchain_load<kXC>(sb, sy, 0, mm, Np, xq_hoff, xq_yoff, xh, xy);
@@ -516,6 +525,10 @@ FPM_PIPE_UNROLL
               const double y2s = __longlong_as_double(__double_as_longlong(y2) ^ yneg);
               ca = __dadd_rn(ca, __dadd_rn(__dmul_rn(hc.x, y1), __dmul_rn(hc.y, y2s)));
               if constexpr (kPair) cb = __dadd_rn(cb, __dsub_rn(__dmul_rn(hc.x, y2), __dmul_rn(hc.y, y1)));
+              if constexpr (kPPT == 2) {
+                ca2 = __dadd_rn(ca2, __dadd_rn(__dmul_rn(hc2.x, y1), __dmul_rn(hc2.y, y2)));
+                cb2 = __dadd_rn(cb2, __dsub_rn(__dmul_rn(hc2.x, y2), __dmul_rn(hc2.y, y1)));
+              }
             }
             if constexpr (kCPT > 1) xchain_add<kXC>(cx, xh, xy, xq_part);
 #pragma unroll
@@ -523,6 +536,7 @@ FPM_PIPE_UNROLL
 #pragma unroll
             for (int v = 0; v < 4; ++v) hj[v] = nj[v];
             hc = nhc;
+            hc2 = nhc2;
             y1 = ny1;
             y2 = ny2;
           }
@@ -543,10 +557,12 @@ FPM_PIPE_UNROLL
           for (int w = 0; w < 2; ++w) hy[w] = py[nb * (w ^ psw)];
 #pragma unroll
           for (int v = 0; v < 4; ++v) hz[v] = pc[pu[v]];
+          double2 hc2 = make_double2(0.0, 0.0);
           if (kChainInLoop) {
             hc = hcp[0];
             y1 = y1p[0];
             y2 = y2p[0];
+            if constexpr (kPPT == 2) hc2 = hcp[N / 2];
           }
 FPM_PIPE_UNROLL
           for (int mm = 0; mm < rows; ++mm) {
@@ -560,10 +576,12 @@ FPM_PIPE_UNROLL
             for (int w = 0; w < 2; ++w) ny[w] = py[mn * Np + nb * (w ^ psw)];
 #pragma unroll
             for (int v = 0; v < 4; ++v) nz[v] = pc[mn * Np + pu[v]];
+            double2 nhc2 = hc2;
             if (kChainInLoop) {
               nhc = hcp[mn * Np];
               ny1 = y1p[2 * mn];
               ny2 = y2p[2 * mn];
+              if constexpr (kPPT == 2) nhc2 = hcp[mn * Np + N / 2];
             }
             double2 xh[kXC], xy[kXC];
             if constexpr (kCPT > 1) xchain_load<kXC>(sb, sy, 0, mm, Np, xq_hoff, xq_yoff, xh, xy);
@@ -584,6 +602,10 @@ FPM_PIPE_UNROLL
               const double y2s = __longlong_as_double(__double_as_longlong(y2) ^ yneg);
               ca = __dadd_rn(ca, __dadd_rn(__dmul_rn(hc.x, y1), __dmul_rn(hc.y, y2s)));
               if constexpr (kPair) cb = __dadd_rn(cb, __dsub_rn(__dmul_rn(hc.x, y2), __dmul_rn(hc.y, y1)));
+              if constexpr (kPPT == 2) {
+                ca2 = __dadd_rn(ca2, __dadd_rn(__dmul_rn(hc2.x, y1), __dmul_rn(hc2.y, y2)));
+                cb2 = __dadd_rn(cb2, __dsub_rn(__dmul_rn(hc2.x, y2), __dmul_rn(hc2.y, y1)));
+              }
             }
             if constexpr (kCPT > 1) xchain_add<kXC>(cx, xh, xy, xq_part);
 #pragma unroll
@@ -593,6 +615,7 @@ FPM_PIPE_UNROLL
 #pragma unroll
             for (int v = 0; v < 4; ++v) hz[v] = nz[v];
             hc = nhc;
+            hc2 = nhc2;
             y1 = ny1;
             y2 = ny2;
           }
@@ -604,6 +627,11 @@ FPM_PIPE_UNROLL
             const double y1 = cq_part ? yv.y : yv.x, y2 = cq_part ? -yv.x : yv.y;
             ca = __dadd_rn(ca, __dadd_rn(__dmul_rn(h.x, y1), __dmul_rn(h.y, y2)));
             if constexpr (kPair) cb = __dadd_rn(cb, __dsub_rn(__dmul_rn(h.x, yv.y), __dmul_rn(h.y, yv.x)));
+            if constexpr (kPPT == 2) {
+              const double2 h2 = sb[cq_hoff + mm * Np + N / 2];
+              ca2 = __dadd_rn(ca2, __dadd_rn(__dmul_rn(h2.x, yv.x), __dmul_rn(h2.y, yv.y)));
+              cb2 = __dadd_rn(cb2, __dsub_rn(__dmul_rn(h2.x, yv.y), __dmul_rn(h2.y, yv.x)));
+            }
             if constexpr (kCPT > 1) {
               double2 xh[kXC], xy[kXC];
               xchain_load<kXC>(sb, sy, 0, mm, Np, xq_hoff, xq_yoff, xh, xy);
@@ -665,6 +693,7 @@ FPM_PIPE_UNROLL
         }
         if (kPair) {
           if (chain_ok) args.gram_b[(t0 + cq_g) * N + cq_n] = make_double2(ca, cb);
+          if (kPPT == 2 && chain_ok) args.gram_b[(t0 + cq_g) * N + cq_n + N / 2] = make_double2(ca2, cb2);
         } else if (kChainInLoop) {
           if (chain_ok) reinterpret_cast<double*>(args.gram_b + (t0 + cq_g) * N + cq_n)[cq_part] = ca;
 #pragma unroll
@@ -818,6 +847,7 @@ FPM_PIPE_UNROLL
       if constexpr (G32) ca = (double)ca32;  // exact widening
       if (kPair) {
         if (chain_ok) bS[cq_g * N + cq_n] = make_double2(ca, cb);
+        if (kPPT == 2 && chain_ok) bS[cq_g * N + cq_n + N / 2] = make_double2(ca2, cb2);
       } else if (kChainInLoop) {
         if (chain_ok) reinterpret_cast<double*>(bS + cq_g * N + cq_n)[cq_part] = ca;
 #pragma unroll
