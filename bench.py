@@ -427,7 +427,7 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_configs:
         sys.path.insert(0, os.path.join(ROOT, "tools"))
         import cfgbench
-        other = {name: cfgbench.measure(name, 16384, lib, peak_dp, dev) for name in cfgbench.CFGS}
+        other = {name: cfgbench.measure(name, 32768, lib, peak_dp, dev) for name in cfgbench.CFGS}
 
     cgk = None
     if rank == 0 and world == 1 and not args.no_configs:
