@@ -1156,8 +1156,6 @@ static int detect_args(const double* H, const double* y, const uint8_t* tx_bits,
 // solve per chunk, then the slicer / counters; flags are -1 (no iteration).
 static int run_lmmse(const DetectArgs& a, int M, int N, cudaStream_t st) {
   const long T = a.T;
-  std::snprintf(g_last_kernel, sizeof(g_last_kernel), "%s+fpm_lmmse_kernel",
-                a.gram32 ? "fpm_gram32_kernel" : "fpm_gram_kernel");
   const long chunk = std::min<long>(T, 8192);
   double2 *A = nullptr, *b = nullptr;
   if (pool_alloc(&A, (size_t)chunk * N * N * 16, st) != cudaSuccess) return FPM_ECUDA;
@@ -1177,6 +1175,9 @@ static int run_lmmse(const DetectArgs& a, int M, int N, cudaStream_t st) {
   cudaFreeAsync(A, st);
   cudaFreeAsync(b, st);
   if (rc) return rc;
+  // (named after the Gram launches, which note their own kernel)
+  std::snprintf(g_last_kernel, sizeof(g_last_kernel), "%s+fpm_lmmse_kernel",
+                a.gram32 ? "fpm_gram32_kernel" : "fpm_gram_kernel");
   cudaMemsetAsync(a.brk, 0xFF, (size_t)T * 4, st);
   cudaMemsetAsync(a.div, 0xFF, (size_t)T * 4, st);
   const long TN = T * (long)N;

@@ -47,9 +47,10 @@ __global__ void __launch_bounds__(256) fpm_lmmse_kernel(const double2* __restric
     const double lkk = __dsqrt_rn(d);
     const double inv = __ddiv_rn(1.0, lkk);
 #pragma unroll 1
+    // (L(k,k) itself is never written: every thread reads the pivot above,
+    // and the solves use dinv only -- writing it here raced with those reads)
     for (int i = k + tid; i < N; i += nt) {
       if (i == k) {
-        Lp[tri(k, k)] = make_double2(lkk, 0.0);
         dinv[k] = inv;
       } else {
         const double2 v = Lp[tri(i, k)];
