@@ -172,35 +172,12 @@ __device__ __forceinline__ void g32_mac(const float2 (&o)[10], const Cj32& cj, f
     acc[15] = fma2(fma2(q3, cj.one, q2), cj.one, acc[15]);
   }
 }
-// rows 0 .. rows-1 of one stage for one job, software-pipelined (row mm+1's
-// operands in flight during row mm's products), with the thread's split
-// matched-filter chain in binary32: re += fl(fl(hr yr) + fl(hi yi)),
-// im += fl(fl(hr yi) + fl(hi (-yr))) (gram_mf_fp32's b)
-template <bool HALF>
-__device__ __forceinline__ void g32_rows(const GramJob& jb, const float2* rows0, int Np, int nb, int rows,
-                                         const Cj32& cj, f2x (&acc)[16], const float2* hcp, const float2* ycp,
-                                         int part, float& ca) {
-  float2 c[10], n[10];
-  g32_load<HALF>(jb, rows0, nb, c);
-  float2 hc = hcp[0], yc = ycp[0];
-#pragma unroll 1
-  for (int mm = 0; mm < rows; ++mm) {
-    const int mn = (mm + 1 < rows) ? mm + 1 : mm;
-    g32_load<HALF>(jb, rows0 + mn * Np, nb, n);
-    const float2 nh = hcp[mn * Np], ny = ycp[mn];
-    g32_mac<HALF>(c, cj, acc);
-    const float y1 = part ? yc.y : yc.x, y2 = part ? -yc.x : yc.y;
-    ca = __fadd_rn(ca, __fadd_rn(__fmul_rn(hc.x, y1), __fmul_rn(hc.y, y2)));
-#pragma unroll
-    for (int k = 0; k < 10; ++k) c[k] = n[k];
-    hc = nh;
-    yc = ny;
-  }
-}
 // N = 128 in binary32 (G32): the thread's two jobs (t and t + 256) in ONE
 // pass over the antenna rows (binary32 accumulators take half the registers,
 // so H streams once): job 1's operands load while job 0's products run and
-// vice versa
+// vice versa; the thread's split matched-filter chain runs alongside in
+// binary32: re += fl(fl(hr yr) + fl(hi yi)), im += fl(fl(hr yi) + fl(hi (-yr)))
+// (gram_mf_fp32's b)
 template <bool HALF1>
 __device__ __forceinline__ void g32_rows2(const GramJob& j0, const GramJob& j1, const float2* r0, const float2* r1,
                                           int Np, int nb, int rows, const Cj32& cj, f2x (&acc0)[16],
