@@ -620,7 +620,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--precision", choices=["fp16", "fp64"], default="fp16")
     ap.add_argument("--T", type=int, default=1 << 20)
-    ap.add_argument("--e2e-T", dest="e2e_T", type=int, default=1 << 15)  # global, split over ranks
+    ap.add_argument("--e2e-T", dest="e2e_T", type=int, default=1 << 16)  # global, split over ranks (8.6 GB of pinned H)
     ap.add_argument("--cpu-per-worker", dest="cpu_per_worker", type=int, default=2048)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
