@@ -49,6 +49,10 @@ constexpr int kProducerLanes = FPM_PRODUCER_LANES;
 #define FPM_PWAIT(b, p)                                                                                       \
   (FPM_WAIT_HINT_NS ? mbar_wait_suspend((b), (p), FPM_WAIT_HINT_NS)                                          \
    : FPM_PRODUCER_SLEEP_NS ? mbar_wait_sleep((b), (p), FPM_PRODUCER_SLEEP_NS) : mbar_wait((b), (p)))
+#ifndef FPM_G32_SLEEP_NS  // converter warp's wait for a landed stage (0: spin)
+#define FPM_G32_SLEEP_NS 300
+#endif
+#define FPM_G32WAIT(b, p) (FPM_G32_SLEEP_NS ? mbar_wait_sleep((b), (p), FPM_G32_SLEEP_NS) : mbar_wait((b), (p)))
 #define FPM_CWAIT(b, p)                                                                                       \
   (FPM_WAIT_HINT_NS ? mbar_wait_suspend((b), (p), FPM_WAIT_HINT_NS)                                          \
    : FPM_CG_SLEEP_NS ? mbar_wait_sleep((b), (p), FPM_CG_SLEEP_NS) : mbar_wait((b), (p)))
@@ -898,7 +902,7 @@ FPM_PIPE_UNROLL
 #pragma unroll 1
     for (long gc = 0; gc < total; ++gc) {
       const int s = (int)(gc % G.S);
-      FPM_PWAIT(&full[s], (uint32_t)((gc / G.S) & 1));
+      FPM_G32WAIT(&full[s], (uint32_t)((gc / G.S) & 1));
       double2* sbuf = stages + s * stage_elems;
       g32_convert(sbuf, R * G.MC * Np, lane);
       g32_convert(sbuf + R * G.MC * Np, R * G.MC, lane);
