@@ -28,10 +28,9 @@ namespace fpm {
 #ifndef FPM_WIDE_NC_MAX_RS  // unrolled wide sums only when the CG side keeps >= 256 - this registers
 #define FPM_WIDE_NC_MAX_RS 0
 #endif
-#ifndef FPM_PIPE_UNROLL_N
-#define FPM_PIPE_UNROLL_N 1
+#ifndef FPM_PIPE_UNROLL_N  // 0: per instance (kRowUnroll below)
+#define FPM_PIPE_UNROLL_N 0
 #endif
-#define FPM_PIPE_UNROLL FPM_UNROLL_(FPM_PIPE_UNROLL_N)
 
 #ifndef FPM_PRODUCER_LANES  // threads of the producer warp issuing bulk copies (1 or 32)
 #define FPM_PRODUCER_LANES 32
@@ -331,6 +330,11 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const __grid_cons
   // over all antenna rows (H streams twice; the FP64 work is unchanged); the
   // hand-off of pass 0's entries goes out before pass 1 starts
   constexpr int kNpass = (NB == 32 && !G32) ? 2 : (NB > 0 ? 1 : 0);  // 0: run time (G32: both jobs in one pass)
+  // the pipelined row loops unrolled by two where the Gram warps have the
+  // registers (176 at nb = 16 / 32): c5 fp16 0.755 -> 0.779, c3 0.831 -> 0.864,
+  // c4 0.808 -> 0.856 of FP64; at 136 registers (fp64 matvec) and at nb = 4 / 8
+  // it measured slower (c5 fp64 0.634 -> 0.621, c1 0.452 -> 0.424, c2 -0.6 %)
+  constexpr int kRowUnroll = FPM_PIPE_UNROLL_N > 0 ? FPM_PIPE_UNROLL_N : ((NB == 16 || NB == 32) && RS >= 176 ? 2 : 1);
   const int npass = kNpass ? kNpass : args.ws_npass;
   const long total = (long)my_groups * npass * nch;
   // role layout: ws_order 0 = [Gram | producer | CG], 1 = [CG | producer |
@@ -480,7 +484,7 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const __grid_cons
             y2 = y2p[0];
             if constexpr (kPPT == 2) hc2 = hcp[N / 2];
           }
-FPM_PIPE_UNROLL
+#pragma unroll kRowUnroll
           for (int mm = 0; mm < rows; ++mm) {
             const int mn = (mm + 1 < rows) ? mm + 1 : mm;
             double2 ni[4], nj[4], nhc = hc;
@@ -545,7 +549,7 @@ FPM_PIPE_UNROLL
             y2 = y2p[0];
             if constexpr (kPPT == 2) hc2 = hcp[N / 2];
           }
-FPM_PIPE_UNROLL
+#pragma unroll kRowUnroll
           for (int mm = 0; mm < rows; ++mm) {
             const int mn = (mm + 1 < rows) ? mm + 1 : mm;
             double2 nx[4], ny[2], nz[4], nhc = hc;
