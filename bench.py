@@ -240,14 +240,16 @@ def raw_h2d_gbs(dev, nbytes=1 << 30, reps=5):
     dst.copy_(src, non_blocking=True)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(reps):
-        dst.copy_(src, non_blocking=True)
-    e1.record()
-    e1.synchronize()
-    gbs = nbytes * reps / (e0.elapsed_time(e1) / 1e3) / 1e9
+    best = 0.0
+    for _ in range(3):  # best of three rounds (the first touches of the pinned pages are slower)
+        e0.record()
+        for _ in range(reps):
+            dst.copy_(src, non_blocking=True)
+        e1.record()
+        e1.synchronize()
+        best = max(best, nbytes * reps / (e0.elapsed_time(e1) / 1e3) / 1e9)
     del src, dst
-    return gbs
+    return best
 
 
 def launch_ranks(args):
