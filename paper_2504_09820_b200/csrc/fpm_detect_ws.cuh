@@ -28,6 +28,9 @@ namespace fpm {
 #ifndef FPM_WIDE_NC_MAX_RS  // unrolled wide sums only when the CG side keeps >= 256 - this registers
 #define FPM_WIDE_NC_MAX_RS 0
 #endif
+#ifndef FPM_G32_UNROLL  // binary32 Gram row loop unroll
+#define FPM_G32_UNROLL 1
+#endif
 #ifndef FPM_PIPE_UNROLL_N  // 0: per instance (kRowUnroll below)
 #define FPM_PIPE_UNROLL_N 0
 #endif
@@ -188,7 +191,7 @@ __device__ __forceinline__ void g32_rows2(const GramJob& j0, const GramJob& j1, 
   float2 o0[10], o1[10];
   g32_load<false>(j0, r0, nb, o0);
   float2 hc = hcp[0], yc = ycp[0];
-#pragma unroll 1
+FPM_UNROLL_(FPM_G32_UNROLL)
   for (int mm = 0; mm < rows; ++mm) {
     const int mn = (mm + 1 < rows) ? mm + 1 : mm;
     g32_load<HALF1>(j1, r1 + mm * Np, nb, o1);
