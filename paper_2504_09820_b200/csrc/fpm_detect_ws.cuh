@@ -55,6 +55,14 @@ constexpr int kProducerLanes = FPM_PRODUCER_LANES;
 #define FPM_G32_SLEEP_NS 300
 #endif
 #define FPM_G32WAIT(b, p) (FPM_G32_SLEEP_NS ? mbar_wait_sleep((b), (p), FPM_G32_SLEEP_NS) : mbar_wait((b), (p)))
+#ifndef FPM_GSLOT_SLEEP_NS  // Gram warps' wait for the hand-off slot (0: spin)
+#define FPM_GSLOT_SLEEP_NS 0
+#endif
+#define FPM_GSWAIT(b, p) (FPM_GSLOT_SLEEP_NS ? mbar_wait_sleep((b), (p), FPM_GSLOT_SLEEP_NS) : mbar_wait((b), (p)))
+#ifndef FPM_GFULL_SLEEP_NS  // Gram warps' wait for a landed stage (0: spin)
+#define FPM_GFULL_SLEEP_NS 0
+#endif
+#define FPM_GFWAIT(b, p) (FPM_GFULL_SLEEP_NS ? mbar_wait_sleep((b), (p), FPM_GFULL_SLEEP_NS) : mbar_wait((b), (p)))
 #define FPM_CWAIT(b, p)                                                                                       \
   (FPM_WAIT_HINT_NS ? mbar_wait_suspend((b), (p), FPM_WAIT_HINT_NS)                                          \
    : FPM_CG_SLEEP_NS ? mbar_wait_sleep((b), (p), FPM_CG_SLEEP_NS) : mbar_wait((b), (p)))
@@ -390,6 +398,10 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const __grid_cons
       xq_yoff[k] = g * G.MC;
     }
 
+    // ring position of the next stage this warp consumes: stage index and
+    // phase parity advance with every stage (no 64-bit division per stage)
+    int rs = 0;
+    uint32_t rph = 0;
 #pragma unroll 1
     for (int j = 0; j < my_groups; ++j) {
       const long t0 = ((long)blockIdx.x + (long)j * gridDim.x) * R;
@@ -440,10 +452,13 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const __grid_cons
 
 #pragma unroll 1
       for (int c = 0; c < nch; ++c) {
-        const long gc = ((long)j * npass + pass) * nch + c;
-        const int s = (int)(gc % G.S);
-        mbar_wait(G32 ? &conv[s] : &full[s], (uint32_t)((gc / G.S) & 1));
-        diag_jitter(args.debug, 2, (int)gc);
+        const int s = rs, gc = (j * npass + pass) * nch + c;  // gc: diagnostics only
+        FPM_GFWAIT(G32 ? &conv[s] : &full[s], rph);
+        if (++rs == G.S) {
+          rs = 0;
+          rph ^= 1u;
+        }
+        diag_jitter(args.debug, 2, gc);
         const double2* sb = stages + s * stage_elems;
         const double2* sy = sb + R * G.MC * Np;  // y rows m0 .. m0 + rows of every realization of the group
         const int m0 = c * G.MC;
@@ -647,7 +662,7 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const __grid_cons
             bsm[q] = a;
           }
         }
-        diag_jitter(args.debug, 3, (int)gc);
+        diag_jitter(args.debug, 3, gc);
         __syncwarp();
         if ((tid & 31) == 0) mbar_arrive(&empty[s]);
       }
@@ -708,7 +723,7 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const __grid_cons
         if (tr && tid == 0 && j < 8) tr[j * 8 + 1] = clock64();
         if (tr && (tid & 31) == 0 && j == 2) tr[72 + tid / 32] = clock64();
         diag_jitter(args.debug, 4, j);
-        if (j >= nsl) mbar_wait(&sempty[slot], (uint32_t)((use - 1) & 1));
+        if (j >= nsl) FPM_GSWAIT(&sempty[slot], (uint32_t)((use - 1) & 1));
         if (tr && tid == 0 && j < 8) tr[j * 8 + 2] = clock64();
       }
       unsigned char* sp = slots + slot * sl.bytes;
@@ -795,23 +810,28 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const __grid_cons
       } else if (active) {
         C* Ag = At + job.g * N * ldA;
         double2* dg = dS + job.g * nblk;
+        // (onchip implies block-Jacobi: the block size is the compile-time LB
+        // when there is one, so the index divisions are shifts; not for 16-byte
+        // entries, whose 136-register Gram warps spill the unrolled form:
+        // c5 fp64 0.632 -> 0.595)
+        const int Ld = (LB > 0 && sizeof(C) < 16) ? LB : L;
         auto put = [&](int i, int jx, double2 vij, double2 vji) {
           Ag[i * ldA + jx] = Ar<K>::rnd(vij, args.pr.mv);
           Ag[jx * ldA + i] = Ar<K>::rnd(vji, args.pr.mv);
           if (onchip) {
-            const int kb = i / L;
-            if (kb == jx / L) {
-              const int il = i - kb * L, jl = jx - kb * L;
-              dg[(il * L + jl) * nbt + kb] = vij;
-              dg[(jl * L + il) * nbt + kb] = vji;
+            const int kb = i / Ld;
+            if (kb == jx / Ld) {
+              const int il = i - kb * Ld, jl = jx - kb * Ld;
+              dg[(il * Ld + jl) * nbt + kb] = vij;
+              dg[(jl * Ld + il) * nbt + kb] = vji;
             }
           }
         };
         auto put_diag = [&](int i, double2 vii) {
           Ag[i * ldA + i] = Ar<K>::rnd(vii, args.pr.mv);
           if (onchip) {
-            const int kb = i / L, il = i - kb * L;
-            dg[(il * L + il) * nbt + kb] = vii;
+            const int kb = i / Ld, il = i - kb * Ld;
+            dg[(il * Ld + il) * nbt + kb] = vii;
           }
         };
         if constexpr (G32) {
@@ -873,12 +893,10 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const __grid_cons
     const int pl = tid - pbase;
     const int pn = kProducerLanes;
     if (pl < pn) {
-      // issue global chunk gc (group gc/nch, local chunk gc%nch) into its stage
-      auto issue = [&](long gc) {
-        const int jj = (int)(gc / (npass * nch)), c = (int)(gc % nch);
+      // issue chunk c of group jj into stage s
+      auto issue = [&](int jj, int c, int s) {
         const long t0 = ((long)blockIdx.x + (long)jj * gridDim.x) * R;
         const int Rv = (int)min((long)R, args.T - t0);
-        const int s = (int)(gc % G.S);
         if (args.use_tma) {
           // one tensor-map TMA per operand and stage: the whole group's rows
           // m0 .. m0+MC of H and of y (realizations past T / rows past M are
@@ -894,11 +912,26 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const __grid_cons
         }
       };
       fence_proxy_async();
+      // ring position: stage index, parity of the stage's previous use, and
+      // the (group, pass, chunk) counters advance together
+      int ps = 0, pc = 0, pp = 0, pj = 0;
+      uint32_t pph = 1;  // parity of use (gc / S) - 1
 #pragma unroll 1
       for (long gc = 0; gc < total; ++gc) {
-        if (gc >= G.S) FPM_PWAIT(&empty[gc % G.S], (uint32_t)(((gc - G.S) / G.S) & 1));
+        if (gc >= G.S) FPM_PWAIT(&empty[ps], pph);
         diag_jitter(args.debug, 1, (int)gc);
-        issue(gc);
+        issue(pj, pc, ps);
+        if (++ps == G.S) {
+          ps = 0;
+          pph ^= 1u;
+        }
+        if (++pc == nch) {
+          pc = 0;
+          if (++pp == npass) {
+            pp = 0;
+            ++pj;
+          }
+        }
       }
     }
     } else if (G32 && tid >= gt + 32 + ct && tid < gt + 64 + ct) {
@@ -907,9 +940,15 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const __grid_cons
     // converted in place to binary32 for the Gram warps (conv[s]), in ring order
     const int lane = tid & 31;
 #pragma unroll 1
+    int cs = 0;
+    uint32_t cph = 0;
     for (long gc = 0; gc < total; ++gc) {
-      const int s = (int)(gc % G.S);
-      FPM_G32WAIT(&full[s], (uint32_t)((gc / G.S) & 1));
+      const int s = cs;
+      FPM_G32WAIT(&full[s], cph);
+      if (++cs == G.S) {
+        cs = 0;
+        cph ^= 1u;
+      }
       double2* sbuf = stages + s * stage_elems;
       g32_convert(sbuf, R * G.MC * Np, lane);
       g32_convert(sbuf + R * G.MC * Np, R * G.MC, lane);
