@@ -59,6 +59,7 @@ struct DetectArgs {
   int ws_npass;        // Gram passes per group (2 at N = 128: 512 jobs on 256 Gram threads)
   int ws_tmem;         // fp64 A of the hand-off in tensor memory (two TMEM slots), staged through off_stg
   int ws_rr, off_stg;  // rows per staging round, staging offset (pitch N + 1 double2)
+  int ws_sw;           // CG side = four solver warps, one realization each (fpm_detect_sw.cuh); scratch at off_vec
   int debug;  // diagnostic bits (FPM_DEBUG): 1 = WS kernel skips the CG side
   int composed;  // no fused plan fits: fpm_gram -> fpm_bj_setup -> fpm_cg -> slicer
   int gram32;    // FPM_FLAG_GRAM_FP32: binary32 Gram (extension): fused WS kernel at N = 128, else composed

@@ -21,6 +21,7 @@
 #include <cstdlib>
 
 #include "fpm_detect.cuh"
+#include "fpm_detect_sw.cuh"
 #include "fpm_gram32.cuh"
 
 namespace fpm {
@@ -59,6 +60,9 @@ constexpr int kProducerLanes = FPM_PRODUCER_LANES;
 #define FPM_GSLOT_SLEEP_NS 0
 #endif
 #define FPM_GSWAIT(b, p) (FPM_GSLOT_SLEEP_NS ? mbar_wait_sleep((b), (p), FPM_GSLOT_SLEEP_NS) : mbar_wait((b), (p)))
+#ifndef FPM_SW_WG3_REGS  // SW: registers of the producer's warp group
+#define FPM_SW_WG3_REGS 24
+#endif
 #ifndef FPM_GFULL_SLEEP_NS  // Gram warps' wait for a landed stage (0: spin)
 #define FPM_GFULL_SLEEP_NS 0
 #endif
@@ -247,8 +251,16 @@ __device__ __forceinline__ int nsl_of(const DetectArgs& a) { return a.ws_nslot; 
 // RS > 0: register split (setmaxnreg) for a 512-thread block: the GWG Gram
 // warp groups (gt = 128 * GWG) run with RS registers per thread, the other
 // 4 - GWG (producer + CG + idle warps) with the rest of the register file.
-template <int WK, int K, int NB, int LB, int RS, int GWG = 2, int G32 = 0, int TA = 0>
+template <int WK, int K, int NB, int LB, int RS, int GWG = 2, int G32 = 0, int TA = 0, int SW = 0>
 __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const __grid_constant__ DetectArgs args, const WsLayout sl) {
+  // SW: the CG side is four independent solver warps (fpm_detect_sw.cuh), one
+  // realization each, instead of a lockstep CG group: thread layout
+  // [Gram 0..255 | solver warps 256..383 | producer warp 384..415 | idle],
+  // registers RS / kSwRegs / 24 per thread by warp group
+  static_assert(!SW || (WK == FK_F64 && (K == FK_F16 || K == FK_BF16) && RS > 0 && GWG == 2 && !G32 && !TA &&
+                        ((NB == 16 && LB == 4) || (NB == 8 && LB == 0))),
+                "solver warps: fp64 work, 32-bit native u_MV == u_IP, N = 64 with L = 4 or N = 32 plain");
+  constexpr int kSwRegs = SW ? ((65536 - RS * 256 - FPM_SW_WG3_REGS * 128) / 128) / 8 * 8 : 0;
   // TA: the fp64 matrix of the hand-off lives in TENSOR MEMORY (two 256-column
   // slots, row q of a group in lane q % 128), staged through a small
   // shared-memory area in rounds -- the 128 KB of shared memory an fp64 A
@@ -318,7 +330,7 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const __grid_cons
     }
     for (int k = 0; k < 2; ++k) {
       mbar_init(&sfull[k], gt / 32);
-      mbar_init(&sempty[k], 1);
+      mbar_init(&sempty[k], SW ? R : 1);  // SW: one arrival per realization's solver warp
     }
     if constexpr (G32)
       for (int s = 0; s < G.S; ++s) mbar_init(&conv[s], 1);
@@ -352,9 +364,9 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const __grid_cons
   // Gram].  CG-first gives the latency-bound CG warps the lower warp ids,
   // which the warp schedulers favour when several warps are ready, so the
   // throughput-bound Gram warps fill the issue slots the CG chains leave.
-  const int cbase = args.ws_order ? 0 : gt + 32;
-  const int pbase = args.ws_order ? ct : gt;
-  const int gbase = args.ws_order ? ct + 32 : 0;
+  const int cbase = SW ? gt : args.ws_order ? 0 : gt + 32;
+  const int pbase = SW ? gt + 128 : args.ws_order ? ct : gt;
+  const int gbase = SW ? 0 : args.ws_order ? ct + 32 : 0;
   if (tid >= gbase && tid < gbase + gt) {
     if constexpr (RS > 0) reg_alloc<RS>();
     const int tid = threadIdx.x - gbase;  // Gram-local thread id
@@ -808,16 +820,20 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const __grid_cons
           tr[j * 8 + 7] = tmv;
         }
       } else if (active) {
-        C* Ag = At + job.g * N * ldA;
+        C* Ag = At + job.g * N * (SW ? N : ldA);  // SW: unpadded, swizzled (CgwLayout::at)
         double2* dg = dS + job.g * nblk;
+        auto aidx = [&](int i, int jx) -> int {
+          if constexpr (SW) return CgwLayout<K, 4 * NB, 0>::at(i, jx);
+          else return i * ldA + jx;
+        };
         // (onchip implies block-Jacobi: the block size is the compile-time LB
         // when there is one, so the index divisions are shifts; not for 16-byte
         // entries, whose 136-register Gram warps spill the unrolled form:
         // c5 fp64 0.632 -> 0.595)
         const int Ld = (LB > 0 && sizeof(C) < 16) ? LB : L;
         auto put = [&](int i, int jx, double2 vij, double2 vji) {
-          Ag[i * ldA + jx] = Ar<K>::rnd(vij, args.pr.mv);
-          Ag[jx * ldA + i] = Ar<K>::rnd(vji, args.pr.mv);
+          Ag[aidx(i, jx)] = Ar<K>::rnd(vij, args.pr.mv);
+          Ag[aidx(jx, i)] = Ar<K>::rnd(vji, args.pr.mv);
           if (onchip) {
             const int kb = i / Ld;
             if (kb == jx / Ld) {
@@ -828,7 +844,7 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const __grid_cons
           }
         };
         auto put_diag = [&](int i, double2 vii) {
-          Ag[i * ldA + i] = Ar<K>::rnd(vii, args.pr.mv);
+          Ag[aidx(i, i)] = Ar<K>::rnd(vii, args.pr.mv);
           if (onchip) {
             const int kb = i / Ld, il = i - kb * Ld;
             dg[(il * Ld + il) * nbt + kb] = vii;
@@ -882,9 +898,122 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const __grid_cons
       if ((tid & 31) == 0) mbar_arrive(&sfull[slot]);
       if (tr && tid == 0 && j < 8) tr[j * 8 + 3] = clock64();
     }
+  } else if (SW && tid >= cbase && tid < cbase + 128) {
+    // warp group 2: the solver warps, on their own register budget (the role's
+    // code must be dominated by this reallocation alone: ptxas budgets a join
+    // of differently sized branches at the smaller count)
+    if constexpr (kSwRegs > 128) reg_alloc<kSwRegs>();
+    else if constexpr (SW && kSwRegs < 128) reg_dealloc<kSwRegs>();
+    if (!args.gram_A) {
+    // ========================== solver warps ==========================
+    // realization ticket q = j * R + g (group j, entry g) belongs to solver
+    // warp q % 4, which takes its tickets in order (the planner only picks
+    // layouts in which a warp sees EVERY use of the slots it consumes -- R a
+    // multiple of 4, or R = 2 on two slots -- so its phase-parity waits never
+    // skip a phase): wait for the group's slot,
+    // block inverses (lanes 0 .. N/L-1, one block each), the (BJ-)CG, release
+    // the slot (sempty counts the R realizations), slicer / counters / write-back
+    if constexpr (SW) {
+      constexpr int NC = 4 * NB, RPL = NC / 32, LBm = LB > 0 ? LB : 1, NBLK = LB > 0 ? NC / LB : 1;
+      const int w = (tid - cbase) >> 5, l = tid & 31;
+      unsigned char* scr = smem + args.off_vec + w * SwScratch<K, NC, LB>::bytes;
+      const int bps = 2 * args.sl.bpa;
+      unsigned long long be = 0, se = 0;
+      const long nq = (long)my_groups * R;
+#pragma unroll 1
+      for (long q = w; q < nq; q += 4) {
+        const int j = (int)(q / R), g = (int)(q - (long)j * R);
+        const long t0 = ((long)blockIdx.x + (long)j * gridDim.x) * R;
+        const int Rv = (int)min((long)R, args.T - t0);
+        const int slot = nsl == 2 ? (j & 1) : 0;
+        const int use = nsl == 2 ? (j >> 1) : j;
+        unsigned char* sp = slots + slot * sl.bytes;
+        FPM_CWAIT(&sfull[slot], (uint32_t)(use & 1));
+        diag_jitter(args.debug, 6, j);
+        if (tr && g == 0 && l == 0 && j < 8) tr[j * 8 + 4] = clock64();
+        if (g >= Rv) {  // entry past T in the last group: nothing to solve
+          __syncwarp();
+          if (l == 0) mbar_arrive(&sempty[slot]);
+          continue;
+        }
+        const long t = t0 + g;
+        const C* Ag = reinterpret_cast<const C*>(sp + sl.at) + g * NC * NC;
+        const double2* bv = reinterpret_cast<const double2*>(sp + sl.b) + g * NC;
+        double2 m[RPL][LBm];
+        bool live = true;
+        if constexpr (LB > 0) {
+          if (args.minv_in) {
+#pragma unroll
+            for (int jr = 0; jr < RPL; ++jr)
+#pragma unroll
+              for (int k = 0; k < LB; ++k) m[jr][k] = args.minv_in[(t * NC + l + 32 * jr) * LB + k];
+          } else {
+            const double2* dS = reinterpret_cast<const double2*>(sp + sl.d);
+            double2* fac = reinterpret_cast<double2*>(scr);            // Cholesky factors, interleaved over blocks
+            double2* inv = fac + NC * LB;                               // inverses, column-major per block
+            bool ok = true;
+            if (l < NBLK) ok = hpd_inverse<LB>(dS + g * NBLK + l, R * NBLK, fac + l, NBLK, inv + l * LB * LB, LB);
+            const unsigned bad = __ballot_sync(0xffffffffu, !ok);
+            if (bad) {
+              live = false;
+              if (l == 0) atomicAdd(&cnt[FPM_CNT_NONPD], (unsigned long long)__popc(bad));
+            }
+            __syncwarp();
+#pragma unroll
+            for (int jr = 0; jr < RPL; ++jr) {
+              const int i = l + 32 * jr, kb = i / LB, il = i - kb * LB;
+#pragma unroll
+              for (int k = 0; k < LB; ++k) m[jr][k] = inv[kb * LB * LB + k * LB + il];  // row il of the block
+            }
+            __syncwarp();  // the scratch is the CG's from here on
+          }
+        } else {
+#pragma unroll
+          for (int jr = 0; jr < RPL; ++jr) m[jr][0] = make_double2(0.0, 0.0);
+        }
+        double2 xs[RPL];
+#pragma unroll
+        for (int jr = 0; jr < RPL; ++jr) xs[jr] = make_double2(0.0, 0.0);
+        int bk = -1, dv = -1;
+        if (live) sw_solve<K, NC, LB>(Ag, bv, m, scr, args.iters, args.textbook != 0, args.pr, l, xs, bk, dv);
+        // slot no longer needed by this realization (A, b, diagonal blocks consumed)
+        __syncwarp();
+        diag_jitter(args.debug, 7, j);
+        if (l == 0) mbar_arrive(&sempty[slot]);
+        if (tr && g == 0 && l == 0 && j < 8) tr[j * 8 + 5] = clock64();
+#pragma unroll
+        for (int jr = 0; jr < RPL; ++jr) {
+          const long gq = t * NC + l + 32 * jr;
+          args.x[gq] = xs[jr];
+          int sym;
+          be += slice_one(xs[jr], args.tx ? args.tx + gq * bps : nullptr, args.rx ? args.rx + gq * bps : nullptr,
+                          args.sl, &sym);
+          se += sym;
+        }
+        if (l == 0) {
+          args.brk[t] = bk;
+          args.div[t] = dv;
+          if (dv >= 0) atomicAdd(&cnt[FPM_CNT_DIVERGED], 1ULL);
+          if (bk >= 0) atomicAdd(&cnt[FPM_CNT_BREAKDOWN], 1ULL);
+          atomicAdd(&cnt[FPM_CNT_TRIALS], 1ULL);
+        }
+      }
+#pragma unroll
+      for (int off = 16; off; off >>= 1) {
+        be += __shfl_xor_sync(0xffffffffu, be, off);
+        se += __shfl_xor_sync(0xffffffffu, se, off);
+      }
+      if (l == 0) {
+        if (be) atomicAdd(&cnt[FPM_CNT_BIT_ERRORS], be);
+        if (se) atomicAdd(&cnt[FPM_CNT_SYMBOL_ERRORS], se);
+      }
+    }
+    }
   } else {
     // the producer warp and the CG warp groups hand registers to the Gram warps
-    if constexpr (RS > 0) reg_dealloc<kOtherRegs>();
+    // (SW: warp group 3 = the producer warp and three idle warps)
+    if constexpr (SW) reg_dealloc<FPM_SW_WG3_REGS>();
+    else if constexpr (RS > 0) reg_dealloc<kOtherRegs>();
     if (tid >= pbase && tid < pbase + 32) {
     // ========================= producer warp ==========================
     // the whole warp issues (many realizations per group at small N: one bulk
@@ -939,9 +1068,9 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const __grid_cons
     // the warp past the CG group: each landed stage (binary64 from TMA) is
     // converted in place to binary32 for the Gram warps (conv[s]), in ring order
     const int lane = tid & 31;
-#pragma unroll 1
     int cs = 0;
     uint32_t cph = 0;
+#pragma unroll 1
     for (long gc = 0; gc < total; ++gc) {
       const int s = cs;
       FPM_G32WAIT(&full[s], cph);
@@ -956,7 +1085,7 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const __grid_cons
       __syncwarp();
       if (lane == 0) mbar_arrive(&conv[s]);
     }
-    } else if (tid >= cbase && tid < cbase + ct && !args.gram_A) {
+    } else if (!SW && tid >= cbase && tid < cbase + ct && !args.gram_A) {
     // ============================ CG warps ============================
     // ws_ncg CG groups; group cgi owns hand-off slot cgi, i.e. realization
     // groups j = cgi, cgi + ncg, ... (two latency-bound solves in flight)
@@ -1144,6 +1273,19 @@ int launch_detect_ws_t(const DetectArgs& a, const WsLayout& sl, int grid, cudaSt
     }
   }
   if (a.gram32) return FPM_EUNSUPPORTED;
+  if constexpr (WK == FK_F64 && (K == FK_F16 || K == FK_BF16) && ((NB == 16 && LB == 4) || (NB == 8 && LB == 0))) {
+    if (a.ws_sw) {  // solver warps on the CG side (fpm_detect_sw.cuh)
+      if (a.ws_gt != 256 || a.ws_ct != 128) return FPM_EUNSUPPORTED;
+      constexpr int kRS = NB == 8 ? FPM_WS_GRAM_REGS_NB8 : FPM_WS_GRAM_REGS;
+      auto k = fpm_detect_ws_kernel<WK, K, NB, LB, kRS, 2, 0, 0, 1>;
+      if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, a.smem_bytes) != cudaSuccess)
+        return FPM_ECUDA;
+      k<<<(unsigned)grid, 512, a.smem_bytes, st>>>(b, sl);
+      count_launch();
+      return cudaGetLastError() == cudaSuccess ? FPM_OK : FPM_ECUDA;
+    }
+  }
+  if (a.ws_sw) return FPM_EUNSUPPORTED;
   if constexpr (NB > 0) {
     // 256 Gram threads (N = 64: R = 2, N = 32: R = 8, N = 16: R = 32) = two
     // warp groups of a 512-thread block -> register split between the Gram

@@ -487,8 +487,9 @@ static int sm_count() {
 // Warp-specialised persistent kernel geometry (fpm_detect_ws.cuh): R realizations
 // per group with uniform Gram warps, gt Gram threads + ct CG threads <= 512.
 static bool plan_detect_ws(int M, int N, int L, int bj, int iters, int mvk, int ipk, DetectArgs& a, WsLayout& sl,
-                           int& grid) {
+                           int& grid, bool allow_sw = false) {
   if (knob("FPM_NO_WS")) return false;
+  a.ws_sw = 0;
   const int Np = (N + 7) / 8 * 8, nb = Np / 4, Cc = nb * (nb / 2 - 1);
   const int limit = max_smem_optin();
   // the CG group takes the threads left of a 512-thread block (rows beyond
@@ -511,6 +512,71 @@ static bool plan_detect_ws(int M, int N, int L, int bj, int iters, int mvk, int 
     const bool tm = knob("FPM_TMEM_A") && mvk == FK_F64 && ipk == FK_F64 && ((N == 16 && !bj) || (N == 64 && bj && L == 4)) && N == Np &&
                     gt == 256 &&
                     (long)R * N * N <= 8192 && (R * N) % 128 == 0 && !a.gram32;
+    // Solver warps (fpm_detect_sw.cuh; opt-in FPM_WS_SW=1, bit-exact, measured
+    // slower): four warps, one realization each, on one or two hand-off slots
+    // in the run_batch kernel's A layout; fp64 work, fp16 / bf16 matvec ==
+    // inner, N = 64 with L = 4 blocks or N = 32 plain.  The solve of a
+    // realization pair drops from 85 K (lockstep group) to 52 K cycles and the
+    // Gram never waits for a slot, but the Gram loop itself runs slower beside
+    // the solver warps (c3: 173-193 K vs 163-182 K cycles per group in the
+    // diagnostic build): c5 fp16 0.743 vs 0.782, c3 0.789 vs 0.861, c2 0.731
+    // vs 0.727 of FP64
+    const bool sw = allow_sw && env_int("FPM_WS_SW", 0) && !a.gram32 && !tm && gt == 256 && npass == 1 && N == Np &&
+                    mvk == ipk && (mvk == FK_F16 || mvk == FK_BF16) &&
+                    ((N == 64 && bj && L == 4 && mvk == FK_F16) || (N == 32 && !bj));  // the instantiated shapes
+    if (sw) {
+      const int scr_b = N == 64 ? SwScratch<FK_F16, 64, 4>::bytes : SwScratch<FK_F16, 32, 0>::bytes;
+      const int sw_stage[6] = {32, 24, 20, 16, 12, 8};
+      for (int nslot = 2; nslot >= 1; --nslot) {
+        if (env_int("FPM_WS_NSLOT", 0) && nslot != env_int("FPM_WS_NSLOT", 0)) continue;
+        // every solver warp must see every use of the slots it consumes (its
+        // mbarrier parity waits cannot skip a phase): tickets q % 4 do that when
+        // R is a multiple of 4, or for R = 2 on two slots (warps 0 1 <-> slot 0)
+        if (!(R % 4 == 0 || (R == 2 && nslot == 2))) continue;
+        for (int si = 0; si < 6; ++si) {
+          const int stage_kb = env_int("FPM_STAGE_KB", 0) ? env_int("FPM_STAGE_KB", 0) : sw_stage[si];
+          if (env_int("FPM_STAGE_KB", 0) && si > 0) break;
+          GramGeom G;
+          gram_geom(R, M, N, G, stage_kb);
+          G.S = std::max(3, G.S);
+          if (nslot > 1 && G.MC < std::min(8, M)) continue;  // a second slot is not worth short stages
+          if ((2 * G.S + 8) * 8 > 256) continue;
+          size_t off = 256;
+          a.off_union = (int)off;
+          off = align_up(off + (size_t)G.S * ws_stage_elems(G) * 16, 128);
+          a.off_ys = (int)off;
+          sl.at = 0;
+          sl.b = (int)align_up((size_t)R * N * N * mv_bytes(mvk), 128);
+          sl.d = (int)align_up(sl.b + (size_t)R * N * 16, 128);
+          sl.bytes = (int)align_up(sl.d + (bj ? (size_t)R * N * Lb * 16 : 0), 128);
+          a.off_slot = (int)off;
+          off = align_up(off + (size_t)nslot * sl.bytes, 128);
+          a.off_bsm = (int)off;
+          off = align_up(off + (size_t)2 * R * N * 8, 128);
+          a.off_vec = a.off_minv = a.off_scr2 = a.off_pmv = a.off_tip = a.off_sc = a.off_fl = (int)off;
+          off += (size_t)4 * scr_b;
+          if ((long)off + 1024 > limit) continue;
+          a.G = G;
+          a.ldA = N;
+          a.smem_bytes = (int)off;
+          a.ws_gt = gt;
+          a.ws_npass = 1;
+          a.ws_ct = 128;
+          a.ws_ncg = 1;
+          a.ws_ct0 = 128;
+          a.ws_nslot = nslot;
+          a.ws_order = 0;
+          a.ws_tmem = 0;
+          a.ws_rr = 0;
+          a.off_stg = 0;
+          a.cg_stride = scr_b;
+          a.ws_sw = 1;
+          const long ngroups = (a.T + R - 1) / R;
+          grid = (int)std::min<long>(ngroups, (long)sm_count() * env_int("FPM_CTAS_PER_SM", 1));
+          return true;
+        }
+      }
+    }
     // two CG groups (alternating hand-off slots) when the Gram side is two full
     // warp groups: 512 threads = 256 Gram + 32 producer + 128 + 96 CG
     const int ncg_env = env_int("FPM_WS_NCG", 0);
@@ -734,7 +800,8 @@ static int launch_detect_ws(const Kinds& k, const DetectArgs& a0, const WsLayout
   if (a.gram_A && nb == 16) lb = 4;  // Gram-only: any LB; take the N = 64 specialisation
   if (a.G.N != a.G.Np) nb = 0;
   if (knob("FPM_NO_SPEC")) nb = lb = 0;
-  note_kernel(a.gram32 ? "fpm_detect_ws_kernel[gram32]" : a.ws_tmem ? "fpm_detect_ws_kernel[tmemA]" : "fpm_detect_ws_kernel",
+  note_kernel(a.gram32 ? "fpm_detect_ws_kernel[gram32]" : a.ws_tmem ? "fpm_detect_ws_kernel[tmemA]"
+              : a.ws_sw ? "fpm_detect_ws_kernel[sw]" : "fpm_detect_ws_kernel",
               k, nb, lb);
   if (k.w == FK_GEN) return launch_detect_ws_gen_w(a, sl, grid, 0, 0, st);
   switch (k.mv) {
@@ -1143,7 +1210,7 @@ static int detect_args(const double* H, const double* y, const uint8_t* tx_bits,
     return FPM_OK;
   }
   DetectArgs aw = a;
-  ws = plan_detect_ws(M, N, a.L, bj, iters, k.mv, k.ip, aw, sl, grid);
+  ws = plan_detect_ws(M, N, a.L, bj, iters, k.mv, k.ip, aw, sl, grid, k.w == FK_F64 && k.mv == k.ip);
   if (ws) {
     a = aw;
     return FPM_OK;

@@ -296,6 +296,61 @@ def test_child_multi_group_fallback():
     save_child_out(x=res2.x, k=np.array(_lib_last_kernel()))
 
 
+def test_solver_warp_variant_bit_exact():
+    """Opt-in variant (FPM_WS_SW=1, measured slower): the CG side
+    of the fused kernel as four solver warps, one realization each
+    (csrc/fpm_detect_sw.cuh: the run_batch warp kernel's arithmetic on the
+    hand-off slot).  Bit-exact vs the oracle with injected inverses at c5 fp16
+    (several groups per CTA, a partial last group, breakdown / divergence flags
+    and counts included; on-chip inverses within tolerance with identical
+    decisions) and at c2 (N = 32, plain fp_cg, fp16 and bf16)."""
+    o = run_knob_child("tests/test_gpu_parity.py::test_child_solver_warps", {"FPM_WS_SW": "1"})
+    for tag in ("c5_fp16", "c2", "c2_bf16"):
+        assert "[sw]" in str(o["k_" + tag]), o["k_" + tag]
+        assert bits_equal(o["x_" + tag], o["ref_" + tag]), tag
+        assert np.array_equal(o["brk_" + tag], o["rbrk_" + tag]), tag
+        assert np.array_equal(o["div_" + tag], o["rdiv_" + tag]), tag
+        assert np.array_equal(o["bits_" + tag], o["rbits_" + tag]), tag
+        assert int(o["be_" + tag]) == int(o["rbe_" + tag]), tag
+        if "obits_" + tag in o:
+            assert np.array_equal(o["obits_" + tag], o["rbits_" + tag]), tag
+            assert float(o["oerr_" + tag]) < 2.0 ** -9, (tag, float(o["oerr_" + tag]))
+
+
+@knob_child
+def test_child_solver_warps():
+    import fpm_oracle as O
+    from paper_2504_09820_b200.detect import DetectorSpec, detect
+    out = {}
+
+    def run(tag, M, N, zeta, snr, T, det, fmt, L):
+        H, y, bits, s2 = _oracle_inputs(M, N, zeta, snr, T)
+        A, b = O.gram_mf_einsum(H, y, s2)
+        mats = O.bj_inverses(A, L) if L else None
+        res = detect(det, H, y, s2, bits, minv=mats, want_bits=True)
+        ref = O.cg_batch(A, b, det.iters, O.FP64, fmt, fmt, mats)
+        rbits = O.demod16(ref.x)
+        out["x_" + tag], out["ref_" + tag] = res.x, ref.x
+        out["k_" + tag] = np.array(_lib_last_kernel())
+        out["brk_" + tag], out["rbrk_" + tag] = res.breakdown_at, ref.breakdown_at
+        out["div_" + tag], out["rdiv_" + tag] = res.diverged_at, ref.diverged_at
+        out["bits_" + tag], out["rbits_" + tag] = res.bits, rbits
+        out["be_" + tag] = np.array(res.counters["bit_errors"])
+        out["rbe_" + tag] = np.array(int(O.bit_errors(rbits, bits).sum()))
+        if L:  # on-chip block inverses (one lane per block): same decisions, x within tolerance
+            r2 = detect(det, H, y, s2, bits, want_bits=True)
+            out["obits_" + tag] = r2.bits
+            out["oerr_" + tag] = np.array((np.linalg.norm(r2.x - ref.x, axis=1) / np.linalg.norm(ref.x, axis=1)).max())
+
+    T = 148 * 2 * 3 + 1
+    run("c5_fp16", 128, 64, 0.5, 15.0, T, DetectorSpec("fp_bj_cg", iters=8, L=4, matvec="fp16", inner="fp16"), O.FP16, 4)
+    run("c2", 128, 32, 0.5, 10.0, 148 * 8 * 2 + 3, DetectorSpec("fp_cg", iters=10, matvec="fp16", inner="fp16"),
+        O.FP16, 0)
+    run("c2_bf16", 128, 32, 0.5, 10.0, 148 * 8 + 5, DetectorSpec("fp_cg", iters=10, matvec="bfloat16", inner="bfloat16"),
+        O.BF16, 0)
+    save_child_out(**out)
+
+
 def test_tmem_matrix_variant_bit_exact():
     """Opt-in variant (FPM_TMEM_A=1, measured slower): the fp64
     matrix of the hand-off in tensor memory, staged through shared-memory
