@@ -12,6 +12,8 @@
  *                      diverged_at)
  *   fpm_cg_ex       <- run_batch with the BatchResult histories,
  *                      solvers.py:188-204, 306-319, 371-393
+ *   fpm_residual_gaps <- run_batch's record_gaps diagnostic,
+ *                      solvers.py:289-294, 375-377
  *   fpm_lmmse       <- _solve_direct_batch, linalg.py:223-231 (the
  *                      detector "lmmse", detect.py:230-231)
  *   fpm_gen_trials  <- the draws of simulate_trials, detect.py:189-214,
@@ -155,6 +157,16 @@ typedef struct fpm_cg_history {
 int fpm_cg_ex(const double* A, const double* b, const double* Minv, int64_t T, int32_t N, int32_t L,
               int32_t iters, const fpm_precision* prec, int32_t rho_update, double* x, int32_t* breakdown_at,
               int32_t* diverged_at, const fpm_cg_history* hist, void* stream);
+
+/* True-residual gaps of the recorded sweeps (run_batch with record_gaps,
+ * solvers.py:289-294, 375-377): gaps[i, t] = ||b_t - A_t x_{i,t} - r_{i,t}||_2 /
+ * scale[t] for i = 1 .. iters (row 0 is left untouched: the caller zeroes it),
+ * from fpm_cg_ex's iterates / residual_vectors ((iters+1, T, N) complex128).
+ * A (T,N,N), b (T,N) complex128; scale (T,), gaps (iters+1, T) float64; all on
+ * the device.  N <= 128.  Binary64; agrees with the reference's BLAS matvec to
+ * rounding. */
+int fpm_residual_gaps(const double* A, const double* b, const double* iterates, const double* residual_vectors,
+                      const double* scale, int64_t T, int32_t N, int32_t iters, double* gaps, void* stream);
 
 /* LMMSE direct solve x = A^-1 b by fp64 Cholesky (linalg.py:223-231
  * _solve_direct_batch: scipy cho_factor / cho_solve).  A (T,N,N), b (T,N)

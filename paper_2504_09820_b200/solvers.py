@@ -273,11 +273,11 @@ def run_batch(A, b, max_iters: int, prec: PrecisionConfig | None = None, blocks=
             an = torch.maximum(w[:, 0].abs(), w[:, -1].abs())
         else:
             an = _to_dev(np.asarray(a_norm, np.float64) if not _is_torch(a_norm) else a_norm, torch.float64)
-        scale = an * _norm2_t(xr)
+        scale = (an * _norm2_t(xr)).contiguous()
         gaps = torch.zeros((it1, T), dtype=torch.float64, device=dev)
-        for i in range(1, it1):
-            true_res = bd - torch.einsum("tij,tj->ti", Ad, xit[i]) - rit[i]
-            gaps[i] = _norm2_t(true_res) / scale
+        _lib.check(lib.fpm_residual_gaps(Ad.data_ptr(), bd.data_ptr(), xit.data_ptr(), rit.data_ptr(),
+                                         scale.data_ptr(), T, N, int(max_iters), gaps.data_ptr(), _stream()),
+                   "residual_gaps")
     return BatchResult(
         x=_out(x, host), breakdown_at=_out(brk.to(torch.int64), host), diverged_at=_out(div.to(torch.int64), host),
         iterations_run=int(max_iters), residual_norms=_out(res, host), iterate_norms=_out(xnh, host),
