@@ -12,6 +12,8 @@
  *                      diverged_at)
  *   fpm_cg_ex       <- run_batch with the BatchResult histories,
  *                      solvers.py:188-204, 306-319, 371-393
+ *   fpm_herm_norm2  <- np.linalg.norm(A, 2) of the convergence study,
+ *                      experiments.py:246-256
  *   fpm_residual_gaps <- run_batch's record_gaps diagnostic,
  *                      solvers.py:289-294, 375-377
  *   fpm_lmmse       <- _solve_direct_batch, linalg.py:223-231 (the
@@ -157,6 +159,14 @@ typedef struct fpm_cg_history {
 int fpm_cg_ex(const double* A, const double* b, const double* Minv, int64_t T, int32_t N, int32_t L,
               int32_t iters, const fpm_precision* prec, int32_t rho_update, double* x, int32_t* breakdown_at,
               int32_t* diverged_at, const fpm_cg_history* hist, void* stream);
+
+/* Spectral norm ||A_t||_2 = max |lambda| of Hermitian matrices (the a_norm of
+ * the convergence study: np.linalg.norm(A, 2), experiments.py:246-256;
+ * solvers.py:289-294).  A (T,N,N) complex128 on the device (read as stored:
+ * pass exactly Hermitian matrices), norms (T,) float64.  N <= 128.  Lanczos +
+ * Sturm-count multisection in binary64; agrees with LAPACK to ~1e-12 relative
+ * on the Gram matrices of the study. */
+int fpm_herm_norm2(const double* A, int64_t T, int32_t N, double* norms, void* stream);
 
 /* True-residual gaps of the recorded sweeps (run_batch with record_gaps,
  * solvers.py:289-294, 375-377): gaps[i, t] = ||b_t - A_t x_{i,t} - r_{i,t}||_2 /

@@ -22,7 +22,7 @@ COUNTERS = ("bit_errors", "symbol_errors", "diverged", "breakdown", "trials", "n
 NCOUNTERS = 8
 
 # every symbol include/fpmimo_b200.h declares
-EXPORTS = ("fpm_version", "fpm_strerror", "fpm_limits", "fpm_gram", "fpm_bj_setup", "fpm_cg", "fpm_cg_ex", "fpm_residual_gaps", "fpm_lmmse", "fpm_gen_trials", "fpm_simulate", "fpm_gram32",
+EXPORTS = ("fpm_version", "fpm_strerror", "fpm_limits", "fpm_gram", "fpm_bj_setup", "fpm_cg", "fpm_cg_ex", "fpm_residual_gaps", "fpm_herm_norm2", "fpm_lmmse", "fpm_gen_trials", "fpm_simulate", "fpm_gram32",
            "fpm_slice_count", "fpm_detect", "fpm_detect_host", "fpm_launch_count", "fpm_last_kernel", "fpm_probe_fp64",
            "fpm_debug_set_trace")
 
@@ -58,6 +58,7 @@ _SIGS = {
     "fpm_cg_ex": (ctypes.c_int, [_P, _P, _P, _I64, _I32, _I32, _I32, ctypes.POINTER(Precision), _I32,
                                  _P, _P, _P, ctypes.POINTER(CgHistory), _P]),
     "fpm_residual_gaps": (ctypes.c_int, [_P, _P, _P, _P, _P, _I64, _I32, _I32, _P, _P]),
+    "fpm_herm_norm2": (ctypes.c_int, [_P, _I64, _I32, _P, _P]),
     "fpm_lmmse": (ctypes.c_int, [_P, _P, _I64, _I32, _P, _P, _P]),
     "fpm_gram32": (ctypes.c_int, [_P, _P, _I64, _I32, _I32, _D, _P, _P, _P]),
     "fpm_gen_trials": (ctypes.c_int, [ctypes.c_uint64, _I32, _I32, _I64, _I64, _I32, _I32, _I32, _P, _P, _P, _P, _P]),

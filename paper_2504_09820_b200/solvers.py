@@ -199,6 +199,19 @@ def _norm2_t(v):
     return torch.where(torch.isinf(mags).any(-1), torch.full_like(out, float("inf")), out)
 
 
+def herm_norm2(A):
+    """||A_t||_2 of Hermitian matrices on the device (np.linalg.norm(A, 2) in
+    the reference's convergence study, experiments.py:246-256): the library's
+    Lanczos / Sturm-count kernel (fpm_herm_norm2).  Returns a (T,) float64
+    CUDA tensor."""
+    torch = _torch()
+    Ad = _to_dev(A, torch.complex128).contiguous()
+    T, N = Ad.shape[0], Ad.shape[-1]
+    out = torch.empty((T,), dtype=torch.float64, device=Ad.device)
+    _lib.check(_lib.load().fpm_herm_norm2(Ad.data_ptr(), T, N, out.data_ptr(), _stream()), "herm_norm2")
+    return out
+
+
 def run_batch(A, b, max_iters: int, prec: PrecisionConfig | None = None, blocks=None, *,
               rho_update: str = "as_written", rtol: float = 1e-6, x_ref=None, a_norm=None,
               record_gaps: bool = False, record_iterates: bool = False,
@@ -269,8 +282,7 @@ def run_batch(A, b, max_iters: int, prec: PrecisionConfig | None = None, blocks=
     if record_gaps:  # solvers.py:289-294, 375-377: ||b - A x_i - r_i|| / (||A|| ||x_ref||)
         xr = _to_dev(x_ref, torch.complex128)
         if a_norm is None:
-            w = torch.linalg.eigvalsh(Ad)
-            an = torch.maximum(w[:, 0].abs(), w[:, -1].abs())
+            an = herm_norm2(Ad)
         else:
             an = _to_dev(np.asarray(a_norm, np.float64) if not _is_torch(a_norm) else a_norm, torch.float64)
         scale = (an * _norm2_t(xr)).contiguous()

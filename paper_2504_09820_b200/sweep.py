@@ -166,19 +166,18 @@ def iterations_to_match(mean_curve, reference_level: float, margin: float = 1.1)
 def _gpu_chunk(detectors, batch: dict, iters: int) -> dict:
     """_mean_curves._one (experiments.py:246-256) + _run_detector_chunk
     (:215-233) on the device: bit-exact Gram, LMMSE reference solution
-    (fpm_lmmse), ||A||_2 by eigvalsh, the CG with recorded iterates and
+    (fpm_lmmse), ||A||_2 by fpm_herm_norm2, the CG with recorded iterates and
     gaps.  Returns per-trial arrays on the host for the reference's
     chunk-ordered reductions."""
     import numpy as np
     from .detect import gram_mf
-    from .solvers import _norm2_t, _to_dev, _torch, build_blocks_batch, run_batch, solve_direct_batch
+    from .solvers import _norm2_t, _to_dev, _torch, build_blocks_batch, herm_norm2, run_batch, solve_direct_batch
     torch = _torch()
     A, b = gram_mf(_to_dev(batch["H_est"], torch.complex128), _to_dev(batch["y"], torch.complex128),
                    batch["sigma_n2"])
     s = torch.as_tensor(batch["symbols"], device=A.device)
     x_hat = solve_direct_batch(A, b)
-    w = torch.linalg.eigvalsh(A)
-    a_norm = torch.maximum(w[:, 0].abs(), w[:, -1].abs())
+    a_norm = herm_norm2(A)
     lm_err = (_norm2_t(x_hat - s) ** 2).cpu().numpy()
     T = b.shape[0]
     out = {}

@@ -6,7 +6,7 @@ CPU: the per-chunk work is the oracle, so the files must be byte-identical
 (pins the wire format, the chunk-ordered reductions and the gloo sharding).
 GPU: the per-chunk work is the CUDA path; the CG iterates / alphas / betas
 are bit-exact, the norms within a few ulps (CUDA hypot vs libm), the gaps and
-the LMMSE level within the Cholesky / eigvalsh tolerance."""
+the LMMSE level within the Cholesky / Lanczos-norm tolerance."""
 
 import csv
 import io
@@ -152,3 +152,52 @@ def test_gpu_run_reproduces_reference_files(tmp_path):
                     assert _num(b) == pytest.approx(_num(a), rel=1e-9), (f, col, a, b)
                 else:
                     raise AssertionError(col)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("M,N", [(128, 16), (128, 32), (128, 64), (512, 128), (24, 5)])
+def test_diagnostic_kernels_against_numpy(M, N):
+    """fpm_herm_norm2 (Lanczos + Sturm multisection) vs np.linalg.norm(A, 2)
+    (experiments.py:246-256) and fpm_residual_gaps vs the reference formula
+    ||b - A x_i - r_i|| / scale (solvers.py:289-294, 375-377) on Gram matrices
+    of every BASELINE size, an odd size, and indefinite / degenerate Hermitian
+    matrices."""
+    import ctypes  # noqa: F401
+    import torch
+    from paper_2504_09820_b200 import _lib
+    from paper_2504_09820_b200.solvers import _stream, herm_norm2
+    rng = np.random.default_rng(5 + N)
+    T = 37
+    H = (rng.standard_normal((T, M, N)) + 1j * rng.standard_normal((T, M, N))) / np.sqrt(2 * M)
+    A = np.einsum("tmi,tmj->tij", H.conj(), H) + 0.05 * np.eye(N)
+    A = 0.5 * (A + A.conj().transpose(0, 2, 1))
+    # indefinite (largest |lambda| negative), identity (Lanczos ends after one step), repeated top eigenvalue
+    Q = np.linalg.qr(rng.standard_normal((N, N)) + 1j * rng.standard_normal((N, N)))[0]
+    lam = np.linspace(-3.0, 1.0, N)
+    A[0] = (Q * lam) @ Q.conj().T
+    A[0] = 0.5 * (A[0] + A[0].conj().T)
+    A[1] = np.eye(N)
+    lam2 = np.linspace(0.1, 1.0, N)
+    lam2[-2:] = 2.5
+    A[2] = (Q * lam2) @ Q.conj().T
+    A[2] = 0.5 * (A[2] + A[2].conj().T)
+    ref = np.array([np.linalg.norm(a, 2) for a in A])
+    got = herm_norm2(A).cpu().numpy()
+    np.testing.assert_allclose(got, ref, rtol=1e-10)
+
+    iters = 4
+    b = rng.standard_normal((T, N)) + 1j * rng.standard_normal((T, N))
+    xit = rng.standard_normal((iters + 1, T, N)) + 1j * rng.standard_normal((iters + 1, T, N))
+    rit = b[None] - np.einsum("tnk,itk->itn", A, xit) + 1e-9 * (rng.standard_normal((iters + 1, T, N)) + 0j)
+    scale = ref * np.linalg.norm(xit[-1], axis=1)
+    want = np.linalg.norm(b[None] - np.einsum("tnk,itk->itn", A, xit) - rit, axis=2) / scale
+    dev = torch.device("cuda", 0)
+    d = lambda a, dt: torch.as_tensor(np.ascontiguousarray(a), dtype=dt, device=dev)  # noqa: E731
+    Ad, bd, xd, rd, sd = d(A, torch.complex128), d(b, torch.complex128), d(xit, torch.complex128), \
+        d(rit, torch.complex128), d(scale, torch.float64)
+    gaps = torch.zeros((iters + 1, T), dtype=torch.float64, device=dev)
+    _lib.check(_lib.load().fpm_residual_gaps(Ad.data_ptr(), bd.data_ptr(), xd.data_ptr(), rd.data_ptr(), sd.data_ptr(),
+                                             T, N, iters, gaps.data_ptr(), _stream()), "gaps")
+    g = gaps.cpu().numpy()
+    assert np.all(g[0] == 0.0)
+    np.testing.assert_allclose(g[1:], want[1:], rtol=1e-6, atol=1e-18)
