@@ -523,7 +523,7 @@ static bool plan_detect_ws(int M, int N, int L, int bj, int iters, int mvk, int 
     // vs 0.727 of FP64
     const bool sw = allow_sw && env_int("FPM_WS_SW", 0) && !a.gram32 && !tm && gt == 256 && npass == 1 && N == Np &&
                     mvk == ipk && (mvk == FK_F16 || mvk == FK_BF16) &&
-                    ((N == 64 && bj && L == 4 && mvk == FK_F16) || (N == 32 && !bj));  // the instantiated shapes
+                    ((N == 64 && bj && L == 4) || (N == 32 && !bj));  // the instantiated shapes
     if (sw) {
       const int scr_b = N == 64 ? SwScratch<FK_F16, 64, 4>::bytes : SwScratch<FK_F16, 32, 0>::bytes;
       const int sw_stage[6] = {32, 24, 20, 16, 12, 8};

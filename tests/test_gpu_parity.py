@@ -305,7 +305,7 @@ def test_solver_warp_variant_bit_exact():
     and counts included; on-chip inverses within tolerance with identical
     decisions) and at c2 (N = 32, plain fp_cg, fp16 and bf16)."""
     o = run_knob_child("tests/test_gpu_parity.py::test_child_solver_warps", {"FPM_WS_SW": "1"})
-    for tag in ("c5_fp16", "c2", "c2_bf16"):
+    for tag in ("c5_fp16", "c5_bf16", "c2", "c2_bf16"):
         assert "[sw]" in str(o["k_" + tag]), o["k_" + tag]
         assert bits_equal(o["x_" + tag], o["ref_" + tag]), tag
         assert np.array_equal(o["brk_" + tag], o["rbrk_" + tag]), tag
@@ -344,6 +344,8 @@ def test_child_solver_warps():
 
     T = 148 * 2 * 3 + 1
     run("c5_fp16", 128, 64, 0.5, 15.0, T, DetectorSpec("fp_bj_cg", iters=8, L=4, matvec="fp16", inner="fp16"), O.FP16, 4)
+    run("c5_bf16", 128, 64, 0.5, 15.0, 148 * 2 + 1, DetectorSpec("fp_bj_cg", iters=8, L=4, matvec="bfloat16", inner="bfloat16"),
+        O.BF16, 4)
     run("c2", 128, 32, 0.5, 10.0, 148 * 8 * 2 + 3, DetectorSpec("fp_cg", iters=10, matvec="fp16", inner="fp16"),
         O.FP16, 0)
     run("c2_bf16", 128, 32, 0.5, 10.0, 148 * 8 + 5, DetectorSpec("fp_cg", iters=10, matvec="bfloat16", inner="bfloat16"),

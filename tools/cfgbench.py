@@ -24,6 +24,7 @@ CFGS = {  # name: (M, N, zeta, snr, qam, detector kwargs)
     "c4_gram32": (512, 128, 0.8, 25.0, 64, dict(algorithm="fp_bj_cg", iters=8, L=8, matvec="fp16", inner="fp16",
                                                  gram="fp32")),
     "c5_fp16": (128, 64, 0.5, 15.0, 16, dict(algorithm="fp_bj_cg", iters=8, L=4, matvec="fp16", inner="fp16")),
+    "c5_bf16": (128, 64, 0.5, 15.0, 16, dict(algorithm="fp_bj_cg", iters=8, L=4, matvec="bfloat16", inner="bfloat16")),
     "c5_fp64": (128, 64, 0.5, 15.0, 16, dict(algorithm="fp_bj_cg", iters=8, L=4)),
     "c5_lmmse": (128, 64, 0.5, 15.0, 16, dict(algorithm="lmmse")),
 }
