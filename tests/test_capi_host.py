@@ -68,6 +68,17 @@ def test_argument_validation_without_gpu(lib):
                           None, dummy, None) == 1
     assert lib.fpm_slice_count(dummy, None, 1, 4, 32, None, dummy, None) == 1
     assert lib.fpm_bj_setup(dummy, 1, 8, 3, 0, dummy, None, None) == 1
+    # convergence-study diagnostics (csrc/fpm_diag.cu): empty batches are no-ops,
+    # misaligned / missing arrays and N > 128 are rejected before any launch
+    assert lib.fpm_herm_norm2(None, 0, 8, None, None) == 0
+    assert lib.fpm_herm_norm2(dummy, 1, 8, None, None) == 1
+    assert lib.fpm_herm_norm2(odd, 1, 8, dummy, None) == 1
+    assert lib.fpm_herm_norm2(dummy, 1, 129, dummy, None) == _lib.FPM_EUNSUPPORTED
+    assert lib.fpm_residual_gaps(None, None, None, None, None, 0, 8, 4, None, None) == 0
+    assert lib.fpm_residual_gaps(dummy, dummy, dummy, dummy, dummy, 1, 8, 0, dummy, None) == 0
+    assert lib.fpm_residual_gaps(dummy, dummy, dummy, None, dummy, 1, 8, 4, dummy, None) == 1
+    assert lib.fpm_residual_gaps(dummy, odd, dummy, dummy, dummy, 1, 8, 4, dummy, None) == 1
+    assert lib.fpm_residual_gaps(dummy, dummy, dummy, dummy, dummy, 1, 129, 4, dummy, None) == _lib.FPM_EUNSUPPORTED
 
 
 def test_detector_spec_mirrors_reference_validation():
