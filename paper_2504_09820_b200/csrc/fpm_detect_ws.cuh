@@ -29,8 +29,8 @@ namespace fpm {
 #ifndef FPM_WIDE_NC_MAX_RS  // unrolled wide sums only when the CG side keeps >= 256 - this registers
 #define FPM_WIDE_NC_MAX_RS 0
 #endif
-#ifndef FPM_G32_UNROLL  // binary32 Gram row loop unroll
-#define FPM_G32_UNROLL 1
+#ifndef FPM_G32_UNROLL  // binary32 Gram row loop unroll (two: slower with the clamped prefetch, faster without)
+#define FPM_G32_UNROLL 4  // measured with the unclamped prefetch: 1: 0.740, 2: 0.761, 3: 0.770, 4: 0.773 of the packed binary32 ceiling
 #endif
 #ifndef FPM_PIPE_UNROLL_N  // 0: per instance (kRowUnroll below)
 #define FPM_PIPE_UNROLL_N 0
@@ -62,6 +62,9 @@ constexpr int kProducerLanes = FPM_PRODUCER_LANES;
 #define FPM_GSWAIT(b, p) (FPM_GSLOT_SLEEP_NS ? mbar_wait_sleep((b), (p), FPM_GSLOT_SLEEP_NS) : mbar_wait((b), (p)))
 #ifndef FPM_SW_WG3_REGS  // SW: registers of the producer's warp group
 #define FPM_SW_WG3_REGS 24
+#endif
+#ifndef FPM_G32_ROW_CLAMP  // binary32 Gram row loop: clamp the prefetched row index (1) or read one row past (0)
+#define FPM_G32_ROW_CLAMP 0  // measured c4 FP32 Gram: 0.716 -> 0.740, with the loop unrolled by two 0.760
 #endif
 #ifndef FPM_ROW_CLAMP  // -1: per instance (kRowClamp below); 0 / 1: force
 #define FPM_ROW_CLAMP -1
@@ -208,7 +211,7 @@ __device__ __forceinline__ void g32_rows2(const GramJob& j0, const GramJob& j1, 
   float2 hc = hcp[0], yc = ycp[0];
 FPM_UNROLL_(FPM_G32_UNROLL)
   for (int mm = 0; mm < rows; ++mm) {
-    const int mn = (mm + 1 < rows) ? mm + 1 : mm;
+    const int mn = FPM_G32_ROW_CLAMP ? ((mm + 1 < rows) ? mm + 1 : mm) : mm + 1;  // (see kRowClamp)
     g32_load<HALF1>(j1, r1 + mm * Np, nb, o1);
     const float2 nh = hcp[mn * Np], ny = ycp[mn];
     g32_mac<false>(o0, cj, acc0);
