@@ -32,6 +32,12 @@ namespace fpm {
 #ifndef FPM_G32_UNROLL  // binary32 Gram row loop unroll (two: slower with the clamped prefetch, faster without)
 #define FPM_G32_UNROLL 4  // measured with the unclamped prefetch: 1: 0.740, 2: 0.761, 3: 0.770, 4: 0.773 of the packed binary32 ceiling
 #endif
+#ifndef FPM_CG_SPLIT  // c5 at fp64 matvec: CG group = warp group 3 at its own register budget (kCgOwn below)
+#define FPM_CG_SPLIT 0
+#endif
+#ifndef FPM_CG_SPLIT_GRAM_REGS
+#define FPM_CG_SPLIT_GRAM_REGS 176
+#endif
 #ifndef FPM_PIPE_UNROLL_N  // 0: per instance (kRowUnroll below)
 #define FPM_PIPE_UNROLL_N 0
 #endif
@@ -276,6 +282,11 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const __grid_cons
   // realization per group, two Gram passes) is instantiated
   static_assert(!G32 || NB == 32, "binary32 Gram: N = 128 only");
   constexpr int kOtherRegs = RS > 0 ? ((512 - RS * GWG) / (4 - GWG)) / 8 * 8 : 0;
+  // FPM_CG_SPLIT (c5 at fp64 matvec): the CG group = warp group 3 (128 threads)
+  // with its own budget, the producer + idle warps of warp group 2 at the
+  // minimum, so that the Gram warps keep FPM_WS_GRAM_REGS registers
+  constexpr bool kCgOwn = FPM_CG_SPLIT && K == FK_F64 && NB == 16 && LB == 4 && RS > 0 && GWG == 2 && !G32 && !TA && !SW;
+  constexpr int kCgOwnRegs = kCgOwn ? ((65536 - RS * 256 - FPM_SW_WG3_REGS * 128) / 128) / 8 * 8 : 0;
   extern __shared__ __align__(128) unsigned char smem[];
   typedef typename Ar<K>::C C;
   typedef typename Ar<K>::P P;
@@ -381,7 +392,7 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const __grid_cons
   // Gram].  CG-first gives the latency-bound CG warps the lower warp ids,
   // which the warp schedulers favour when several warps are ready, so the
   // throughput-bound Gram warps fill the issue slots the CG chains leave.
-  const int cbase = SW ? gt : args.ws_order ? 0 : gt + 32;
+  const int cbase = SW ? gt : kCgOwn ? 384 : args.ws_order ? 0 : gt + 32;
   const int pbase = SW ? gt + 128 : args.ws_order ? ct : gt;
   const int gbase = SW ? 0 : args.ws_order ? ct + 32 : 0;
   if (tid >= gbase && tid < gbase + gt) {
@@ -1026,10 +1037,19 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const __grid_cons
       }
     }
     }
+  } else if (kCgOwn && tid >= cbase && tid < cbase + ct && !args.gram_A) {
+    // FPM_CG_SPLIT: the CG group is warp group 3 at its own register budget
+    // (its own top-level branch: ptxas budgets code after a join of differently
+    // sized setmaxnreg branches at the smaller count)
+    if constexpr (kCgOwnRegs > 128) reg_alloc<kCgOwnRegs>();
+    else if constexpr (kCgOwnRegs < 128) reg_dealloc<kCgOwnRegs>();
+#include "fpm_detect_ws_cgrole.cuh"
   } else {
     // the producer warp and the CG warp groups hand registers to the Gram warps
-    // (SW: warp group 3 = the producer warp and three idle warps)
+    // (SW: warp group 3 = the producer warp and three idle warps; FPM_CG_SPLIT:
+    // warp group 2 = the same)
     if constexpr (SW) reg_dealloc<FPM_SW_WG3_REGS>();
+    else if constexpr (kCgOwn) reg_dealloc<FPM_SW_WG3_REGS>();
     else if constexpr (RS > 0) reg_dealloc<kOtherRegs>();
     if (tid >= pbase && tid < pbase + 32) {
     // ========================= producer warp ==========================
@@ -1102,137 +1122,8 @@ __global__ void __launch_bounds__(512, 1) fpm_detect_ws_kernel(const __grid_cons
       __syncwarp();
       if (lane == 0) mbar_arrive(&conv[s]);
     }
-    } else if (!SW && tid >= cbase && tid < cbase + ct && !args.gram_A) {
-    // ============================ CG warps ============================
-    // ws_ncg CG groups; group cgi owns hand-off slot cgi, i.e. realization
-    // groups j = cgi, cgi + ncg, ... (two latency-bound solves in flight)
-    const int ncg = args.ws_ncg;
-    const int cgi = (ncg == 2 && tid - cbase >= args.ws_ct0) ? 1 : 0;
-    const int lt = tid - cbase - (cgi ? args.ws_ct0 : 0);
-    const int ctg = ncg == 2 ? (cgi ? ct - args.ws_ct0 : args.ws_ct0) : ct;
-    unsigned char* cgs = smem + cgi * args.cg_stride;  // this group's CG state
-    NamedBar cbar{2 + cgi, ctg};
-    CgSmem<K> S;
-    S.R = R;
-    S.N = N;
-    S.L = L;
-    S.ldA = ldA;
-    S.minv = reinterpret_cast<double2*>(cgs + args.off_minv);
-    S.dbg = diag_bits(args.debug);
-    double2* vec = reinterpret_cast<double2*>(cgs + args.off_vec);
-    const int RN = R * N;
-    // z only with block-Jacobi, the rho0 terms only for BJ as_written: they
-    // come last so the planner can leave them out (ws_cg_layout)
-    S.x = vec;
-    S.r = vec + RN;
-    S.p = vec + 2 * RN;
-    S.w = vec + 3 * RN;
-    S.xn = vec + 4 * RN;
-    S.rn = vec + 5 * RN;
-    S.z = vec + 6 * RN;
-    S.pmv = reinterpret_cast<P*>(cgs + args.off_pmv);
-    S.tphi = reinterpret_cast<C*>(cgs + args.off_tip);
-    S.tr1 = S.tphi + RN;
-    S.rip = S.tr1 + RN;
-    S.trho = S.rip + RN;
-    S.sc = reinterpret_cast<double2*>(cgs + args.off_sc);
-    S.fl = reinterpret_cast<int*>(cgs + args.off_fl);
-    double2* scr2 = reinterpret_cast<double2*>(cgs + args.off_scr2);
-    const int bps = 2 * args.sl.bpa;
-    unsigned long long be = 0, se = 0;
-#pragma unroll 1
-    for (int j = cgi; j < my_groups; j += ncg) {
-      const long t0 = ((long)blockIdx.x + (long)j * gridDim.x) * R;
-      const int Rv = (int)min((long)R, args.T - t0);
-      const int slot = nsl == 2 ? (j & 1) : 0;
-      const int use = nsl == 2 ? (j >> 1) : j;
-      unsigned char* sp = slots + slot * sl.bytes;
-      S.At = reinterpret_cast<C*>(sp + sl.at);
-      S.b = reinterpret_cast<double2*>(sp + sl.b);
-      double2* dS = reinterpret_cast<double2*>(sp + sl.d);
-      FPM_CWAIT(&sfull[slot], (uint32_t)(use & 1));
-      if constexpr (TA) tmx_fence_after();
-      diag_jitter(args.debug, 6, j);
-      if (tr && lt == 0 && j < 8) tr[j * 8 + 4] = clock64();
-#pragma unroll 1
-      for (int g = lt; g < R; g += ctg) S.fl[g * 4] = g < Rv ? 1 : 0;
-      cbar.sync();
-      // block-Jacobi inverses (on-chip fp64 Cholesky, or injected)
-      if (args.bj) {
-        if (args.minv_in) {
-#pragma unroll 1
-          for (int q = lt; q < Rv * N * L; q += ctg) {
-            const int g = q / (N * L);
-            const int e = q - g * N * L;
-            const int kb = e / (L * L), o = e - kb * L * L;
-            const int Lk = min(L, N - kb * L);
-            if (o >= Lk * Lk) continue;
-            const int i = o / Lk, jj = o - i * Lk;
-            S.minv[g * N * L + kb * L * L + jj * Lk + i] =
-                Ar<WK>::rnd(args.minv_in[(t0 + g) * (long)N * L + e], args.pr.work);
-          }
-        } else {
-          const int nbt = R * nblk;
-#pragma unroll 1
-          for (int q = lt; q < Rv * nblk; q += ctg) {
-            const int g = q / nblk, kb = q - g * nblk;
-            const int Lk = min(L, N - kb * L);
-            double2* out = S.minv + g * N * L + kb * L * L;
-            const bool ok = (diag_bits(args.debug) & 32) ? true : (LB > 0) ? hpd_inverse<LB>(dS + q, nbt, scr2 + q, nbt, out, Lk)
-                                     : hpd_inverse<0>(dS + q, nbt, scr2 + q, nbt, out, Lk);
-            if (!ok) {
-              atomicExch(&S.fl[g * 4], 0);
-              atomicAdd(&cnt[FPM_CNT_NONPD], 1ULL);
-            } else if (WK != FK_F64) {
-              for (int e = 0; e < Lk * Lk; ++e) out[e] = Ar<WK>::rnd(out[e], args.pr.work);
-            }
-          }
-        }
-        cbar.sync();
-      }
-      long long* tc = (tr && j == 2 && args.iters <= 8) ? tr + 96 : nullptr;  // CG phase stamps, group 2
-      if (tc && lt == 0) {
-        __shared__ int _fpm_dummy_ws;
-        tc[60] = (long long)clock64() + (*(volatile int*)&_fpm_dummy_ws == 0x7fffffff);
-      }
-      if (!(diag_bits(args.debug) & 1))
-        cg_group<WK, K, LB, kCgNC, TA != 0>(S, Rv, args.iters, args.bj != 0, args.textbook != 0, args.pr, ctg, lt, cbar,
-                                            tc, TmRows{tm_base + (uint32_t)(slot * 256), cbase / 32, ctg / 32});
-      // slot no longer needed (A, b, diagonal blocks consumed)
-      diag_jitter(args.debug, 7, j);
-      if (lt == 0) mbar_arrive(&sempty[slot]);
-      if (tr && lt == 0 && j < 8) tr[j * 8 + 5] = clock64();
-      // slicer + counters + write-back
-#pragma unroll 1
-      for (int q = lt; q < Rv * N; q += ctg) {
-        const long gq = t0 * N + q;
-        const double2 xv = S.x[q];
-        args.x[gq] = xv;
-        int sym;
-        be += slice_one(xv, args.tx ? args.tx + gq * bps : nullptr, args.rx ? args.rx + gq * bps : nullptr,
-                        args.sl, &sym);
-        se += sym;
-      }
-#pragma unroll 1
-      for (int g = lt; g < Rv; g += ctg) {
-        const int bk = S.fl[g * 4 + 2], dv = S.fl[g * 4 + 3];
-        args.brk[t0 + g] = bk;
-        args.div[t0 + g] = dv;
-        if (dv >= 0) atomicAdd(&cnt[FPM_CNT_DIVERGED], 1ULL);
-        if (bk >= 0) atomicAdd(&cnt[FPM_CNT_BREAKDOWN], 1ULL);
-      }
-      if (lt == 0) atomicAdd(&cnt[FPM_CNT_TRIALS], (unsigned long long)Rv);
-      cbar.sync();  // x / flags read before the next group overwrites them
-    }
-#pragma unroll
-    for (int off = 16; off; off >>= 1) {
-      be += __shfl_xor_sync(0xffffffffu, be, off);
-      se += __shfl_xor_sync(0xffffffffu, se, off);
-    }
-    if ((lt & 31) == 0) {
-      if (be) atomicAdd(&cnt[FPM_CNT_BIT_ERRORS], be);
-      if (se) atomicAdd(&cnt[FPM_CNT_SYMBOL_ERRORS], se);
-    }
+    } else if (!kCgOwn && !SW && tid >= cbase && tid < cbase + ct && !args.gram_A) {
+#include "fpm_detect_ws_cgrole.cuh"
     }
   }
   if constexpr (TA) tmx_fence_before();
@@ -1312,7 +1203,11 @@ int launch_detect_ws_t(const DetectArgs& a, const WsLayout& sl, int grid, cudaSt
       // still take part in the register hand-over); CG-first order needs the
       // CG group to fill warp groups 0-1 so the Gram starts at warp group 2
       if (threads < 512) b.ws_order = 0;
-      constexpr int kRS = sizeof(typename Ar<K>::C) >= 16 ? FPM_WS_GRAM_REGS_WIDE
+      constexpr bool kSplit = FPM_CG_SPLIT && K == FK_F64 && NB == 16 && LB == 4;
+      // the split instance's budgets add up only for a 128-thread CG group in warp group 3
+      if (kSplit && (a.ws_ct != 128 || a.ws_ncg != 1)) return FPM_EUNSUPPORTED;
+      constexpr int kRS = kSplit                             ? FPM_CG_SPLIT_GRAM_REGS
+                          : sizeof(typename Ar<K>::C) >= 16 ? FPM_WS_GRAM_REGS_WIDE
                           : NB == 8                        ? FPM_WS_GRAM_REGS_NB8
                                                            : FPM_WS_GRAM_REGS;
       auto k = fpm_detect_ws_kernel<WK, K, NB, LB, kRS>;
